@@ -1,0 +1,93 @@
+"""Seeded input generators shared by the golden-vector script, the parity
+tests and bench.py.
+
+Follows the reference's generation idiom (bench.py:117, 215-216 and
+BASELINE.md section 3.4): ``rng = np.random.default_rng(seed)``; coordinates
+``rng.uniform(lo, hi, M)`` for dims 1..d in order; strengths / modes
+``standard_normal + 1j * standard_normal`` (real drawn before imag).  For
+complex64 configs the values are drawn in float64 and cast; the CPU side is
+fed the cast values upcast back to float64 so both sides see bit-identical
+inputs.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+PI = math.pi
+
+# The BASELINE.json configs.  "M_full" is the north-star size; the golden
+# fixtures use "M_golden" so the reference finishes in seconds.
+CONFIGS = {
+    "c1": dict(ttype=1, dim=1, nm=(10000,), M_full=100_000, M_golden=100_000,
+               tol=1e-6, isign=1, dtype="float64", lo=-PI, hi=PI, ntransf=1, seed=1001),
+    "c2": dict(ttype=2, dim=2, nm=(1000, 1000), M_full=10_000_000, M_golden=20_000,
+               tol=1e-5, isign=-1, dtype="float64", lo=-PI, hi=PI, ntransf=1, seed=1002),
+    "c3": dict(ttype=1, dim=3, nm=(128, 128, 128), M_full=10_000_000, M_golden=20_000,
+               tol=1e-6, isign=1, dtype="float64", lo=-PI, hi=PI, ntransf=1, seed=1003,
+               cdtype="complex64"),
+    "c3f": dict(ttype=1, dim=3, nm=(128, 128, 128), M_full=10_000_000, M_golden=20_000,
+                tol=1e-4, isign=1, dtype="float32", lo=-PI, hi=PI, ntransf=1, seed=1003,
+                cdtype="complex64"),
+    "c4": dict(ttype=1, dim=3, nm=(128, 128, 128), M_full=10_000_000, M_golden=20_000,
+               tol=1e-9, isign=1, dtype="float64", lo=-PI, hi=-PI + 2 * PI / 8,
+               ntransf=1, seed=1004),
+    "c5": dict(ttype=1, dim=2, nm=(512, 512), M_full=1_000_000, M_golden=10_000,
+               tol=1e-4, isign=1, dtype="float32", lo=-PI, hi=PI, ntransf=64, seed=1005,
+               ntransf_golden=3, cdtype="complex64"),
+}
+
+
+def make_inputs(name: str, M: int | None = None, ntransf: int | None = None):
+    """Return (coords list float64, data complex128, cfg) for a config.
+
+    data is strengths (ntransf, M) / (M,) for type 1, or the mode array
+    (N_d..N_1) for type 2.  For float32 configs coordinates are rounded to
+    float32 (then upcast) and complex data to complex64 (then upcast)."""
+    cfg = dict(CONFIGS[name])
+    M = cfg["M_full"] if M is None else M
+    T = cfg["ntransf"] if ntransf is None else ntransf
+    rng = np.random.default_rng(cfg["seed"])
+    coords = [rng.uniform(cfg["lo"], cfg["hi"], M) for _ in range(cfg["dim"])]
+    if cfg["ttype"] == 1:
+        shape = (T, M) if T > 1 else (M,)
+    else:
+        shape = tuple(reversed(cfg["nm"]))
+        if T > 1:
+            shape = (T,) + shape
+    data = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    if cfg["dtype"] == "float32":
+        coords = [x.astype(np.float32).astype(np.float64) for x in coords]
+    cd = cfg.get("cdtype", "complex128")
+    if cd == "complex64" or cfg["dtype"] == "float32":
+        data = data.astype(np.complex64).astype(np.complex128)
+    return coords, data, cfg
+
+
+def rand_problem(dim: int, m: int, seed: int, lo=-PI, hi=PI):
+    """test_transforms.py:23-27 style random problem."""
+    rng = np.random.default_rng(seed)
+    coords = [rng.uniform(lo, hi, m) for _ in range(dim)]
+    c = rng.standard_normal(m) + 1j * rng.standard_normal(m)
+    return coords, c
+
+
+def rand_modes(nm, seed: int):
+    rng = np.random.default_rng(seed)
+    shape = tuple(reversed(nm))
+    return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+
+
+def sample_flat(total: int, count: int, seed: int) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    return np.sort(rng.choice(total, size=min(count, total), replace=False))
+
+
+# Special coordinates that exercise the fold edge cases (grid.py:152-168).
+EDGE_COORDS = np.array([
+    0.0, -0.0, 2 * PI, -2 * PI, PI, -PI, 3 * PI, -3 * PI, 1e-300, -1e-300,
+    -1e-17, 2 * PI - 1e-15, np.nextafter(2 * PI, 0.0), np.nextafter(-2 * PI, 0.0),
+    1e6, -1e6, 12.345, -12.345, 0.5, np.nextafter(0.0, -1.0), 6.283185307179586,
+])
