@@ -1,0 +1,424 @@
+"""bench.py -- NU points/sec of the full type-1/2 transform on B200.
+
+python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+                [--config c2] [--no-e2e] [--no-cpu]
+
+Workload (BASELINE.json configs[1], the metric's config at N = 1):
+  c2: 2D type 2, modes 1000x1000 complex128 N(0,1), M = 1e7 targets iid
+      uniform on [-pi, pi)^2, eps = 1e-5, isign = -1, float64.
+Other configs (--config c1/c3/c3f/c4/c5) exist for parity-shape timing.
+
+A "step" is one full transform (setpts sort + amplify/spread + cuFFT +
+interp/deconv) over one batch of synthetic seeded input already resident in
+HBM.  Under torchrun (N > 1) every rank runs its own independent shard of
+the same size (weak scaling, no data-path collective): type 2 targets are
+independent outputs.  Times are CUDA events on the launching stream, max
+over ranks.  e2e = the same metric through the C ABI one-shot routine
+(esn_nufft_host) with pinned HOST buffers, H2D + D2H inside the timed
+region.  --impl reference times the CPU restatement of the reference
+(oracle/, "port") with all host threads on the same config.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+
+import cases  # noqa: E402
+
+METRIC = "NU points/sec (spread+interp, full type-1/2) at 1/2/4/8 B200; % HBM roofline"
+UNIT = "NU points/s"
+K_E2E = 5
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def algorithmic_bytes(cfg, M, T):
+    """B = M d s_r + T M s_c + T G s_c for the spread/interp."""
+    sr = 8 if cfg["dtype"] == "float64" else 4
+    sc = 2 * sr
+    w = select_w(cfg)
+    G = 1
+    for n in cfg["nm"]:
+        G *= next_smooth(max(math.ceil(2.0 * n), 2 * w))
+    return M * cfg["dim"] * sr + T * M * sc + T * G * sc, G
+
+
+def select_w(cfg):
+    return min(max(math.ceil(math.log10(1.0 / cfg["tol"])) + 1, 2), 16)
+
+
+def next_smooth(n):
+    best = None
+    p2 = 1
+    while True:
+        p23 = p2
+        while True:
+            v = p23
+            while v < n:
+                v *= 5
+            best = v if best is None else min(best, v)
+            if p23 >= n:
+                break
+            p23 *= 3
+        if p2 >= n:
+            break
+        p2 *= 2
+    return best
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        try:
+            rows = [l.strip().split(",") for l in open(self.path) if l.strip()]
+        except Exception:
+            return out
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [x.strip() for x in r]
+            if len(r) < 9:
+                continue
+            try:
+                sm.append(float(r[1]))
+                mx.append(float(r[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if sm:
+            out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                   "reasons": sorted(reasons), "samples": len(sm)}
+        try:
+            os.unlink(self.path)
+        except Exception:
+            pass
+        return out
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm (the oracle port of the reference path, all host threads)
+
+def cpu_run(name, M_sample, T_sample, steps, warmup):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import esn_oracle as O
+    O.build()
+    cores = O.num_procs()
+    coords, data, cfg = cases.make_inputs(name, M=M_sample, ntransf=T_sample)
+    wcoords, wdata, _ = cases.make_inputs(name, M=min(M_sample, 2000), ntransf=T_sample)
+
+    def one(cs, dd):
+        if cfg["ttype"] == 1:
+            batch = dd if dd.ndim == 2 else dd[None]
+            for c in batch:  # the reference has no batch API: a loop of transforms
+                O.exec_type1(cs, c, cfg["nm"], tol=cfg["tol"], isign=cfg["isign"], threads=cores)
+        else:
+            O.exec_type2(cs, dd, tol=cfg["tol"], isign=cfg["isign"], threads=cores)
+
+    one(wcoords, wdata)
+    for _ in range(warmup):
+        one(coords, data)
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        one(coords, data)
+        ts.append(time.perf_counter() - t0)
+    per_step = statistics.median(ts)
+    T = T_sample if cfg["ttype"] == 1 else 1
+    return M_sample * T / per_step, per_step, cores
+
+
+def cpu_sample_size(name):
+    cfg = cases.CONFIGS[name]
+    M, T = cfg["M_full"], cfg["ntransf"]
+    # bounded so one step is a few seconds of CPU work on an 8-32 core host
+    if name == "c5":
+        return M, 4
+    if M > 2_000_000 and cfg["dim"] == 3:
+        return 2_000_000, T
+    return M, T
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+def gpu_run(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    import paper_1808_06736_b200 as E
+    from paper_1808_06736_b200 import _lib
+    from paper_1808_06736_b200.plan import Plan
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    name = args.config
+    cfg = cases.CONFIGS[name]
+    M, T = cfg["M_full"], cfg["ntransf"]
+    # every rank owns an independent shard (its own seed) of the full size
+    coords, data, cfg = cases.make_inputs(name, M=M, ntransf=T)
+    if rank > 0:
+        rng = np.random.default_rng(cfg["seed"] + 7919 * rank)
+        coords = [rng.uniform(cfg["lo"], cfg["hi"], M) for _ in range(cfg["dim"])]
+    real = torch.float64 if cfg["dtype"] == "float64" else torch.float32
+    cplx = torch.complex128 if cfg["dtype"] == "float64" else torch.complex64
+    xs = [torch.from_numpy(x).to(dev, real).contiguous() for x in coords]
+    d = torch.from_numpy(data).to(dev, cplx).contiguous()
+    plan = Plan(cfg["ttype"], cfg["dim"], nmodes=cfg["nm"], isign=cfg["isign"], ntransf=T,
+                tol=cfg["tol"], device=dev, dtype=cfg["dtype"], method=args.method, timing=True)
+    if cfg["ttype"] == 1:
+        out = torch.empty((T,) + tuple(reversed(cfg["nm"])), dtype=cplx, device=dev)
+        cin, fout = d, out
+    else:
+        out = torch.empty((T, M) if T > 1 else (M,), dtype=cplx, device=dev)
+        cin, fout = out, d
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        plan.setpts(xs)
+        plan.execute(cin, fout)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    plan.check()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    hot, stages = [], {"sort": 0.0, "spread": 0.0, "fft": 0.0, "correct": 0.0}
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize(dev)
+        ev0.record(stream)
+        # per-step stage events are recorded by the plan on the same stream;
+        # they are read after each step's own events complete (no host sync
+        # between steps except the event query of the previous step)
+        for k in range(args.steps):
+            step()
+            if args.stage_sync:
+                st = plan.stage_times()
+                for key in stages:
+                    stages[key] += st[key]
+                hot.append(plan.hot_kernel_seconds())
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    elapsed = ev0.elapsed_time(ev1) / 1e3
+    if not args.stage_sync:
+        st = plan.stage_times()
+        stages = {k: v * args.steps for k, v in st.items()}
+        hot = [plan.hot_kernel_seconds()]
+    plan.check()
+    t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed = float(t.item())
+    Tn = T if cfg["ttype"] == 1 else 1
+    value = M * Tn * world * args.steps / elapsed
+    B, G = algorithmic_bytes(cfg, M, T)
+    hot_s = statistics.mean(hot)
+    peak, peak_kind = peaks()
+    achieved = B / hot_s / 1e9
+    res = dict(value=value, elapsed=elapsed, hot_s=hot_s, achieved=achieved, peak=peak,
+               peak_kind=peak_kind, B=B, G=G, clocks=clk.summary(),
+               stages={k: v / args.steps for k, v in stages.items()})
+    # e2e through the C ABI with pinned host buffers
+    if args.e2e:
+        e2 = e2e_run(args, cfg, coords, data, M, T, dev)
+        te = torch.tensor([e2.pop("elapsed")], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2["value"] = M * (T if cfg["ttype"] == 1 else 1) * world * e2.pop("calls") / float(te.item())
+        e2["ms_per_step"] = float(te.item()) / K_E2E * 1e3
+        res["e2e"] = e2
+    plan.close()
+    return res
+
+
+def e2e_run(args, cfg, coords, data, M, T, dev):
+    import torch
+    from paper_1808_06736_b200 import _lib
+    from paper_1808_06736_b200.plan import make_opts
+    cplx = torch.complex128 if cfg["dtype"] == "float64" else torch.complex64
+    hx = [torch.from_numpy(x).pin_memory() for x in coords]
+    hd = torch.from_numpy(data).to(cplx).pin_memory()
+    if cfg["ttype"] == 1:
+        hout = torch.empty((T,) + tuple(reversed(cfg["nm"])), dtype=cplx).pin_memory()
+        cptr, fptr = hd.data_ptr(), hout.data_ptr()
+        h2d = sum(x.numel() * 8 for x in hx) + hd.numel() * hd.element_size()
+        d2h = hout.numel() * hout.element_size()
+    else:
+        hout = torch.empty((T, M) if T > 1 else (M,), dtype=cplx).pin_memory()
+        cptr, fptr = hout.data_ptr(), hd.data_ptr()
+        h2d = sum(x.numel() * 8 for x in hx) + hd.numel() * hd.element_size()
+        d2h = hout.numel() * hout.element_size()
+    o, keep = make_opts(dtype=cfg["dtype"], method=args.method, timing=False)
+    nm = _lib.i64_array(cfg["nm"])
+    xp = [ctypes.c_void_p(x.data_ptr()) for x in hx] + [None] * (3 - len(hx))
+
+    def call():
+        _lib.check(_lib.lib.esn_nufft_host(cfg["ttype"], cfg["dim"], M, xp[0], xp[1], xp[2], T,
+                                           ctypes.c_void_p(cptr), cfg["isign"], cfg["tol"], nm,
+                                           ctypes.c_void_p(fptr), ctypes.byref(o)))
+
+    for _ in range(max(1, args.warmup)):
+        call()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(K_E2E):
+        call()
+    el = time.perf_counter() - t0
+    return {"elapsed": el, "calls": K_E2E, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "api": "esn_nufft_host (C ABI, pinned host buffers)"}
+
+
+def config_block(name, world):
+    cfg = cases.CONFIGS[name]
+    nm = "x".join(str(v) for v in cfg["nm"])
+    return {
+        "workload": f"{name}: {cfg['dim']}D type-{cfg['ttype']}, modes {nm}, M={cfg['M_full']:.0e}"
+                    f" per GPU, eps={cfg['tol']:g}, isign={cfg['isign']:+d}, ntransf={cfg['ntransf']}",
+        "dim": cfg["dim"], "type": cfg["ttype"], "modes": list(cfg["nm"]), "M_per_gpu": cfg["M_full"],
+        "tol": cfg["tol"], "ntransf": cfg["ntransf"], "points": "iid uniform, seeded",
+        "parallelism": f"replica shards x{world} (independent points per GPU)" if world > 1 else "1 GPU",
+        "l2": "inputs larger than L2 (coords + outputs > 126 MB), no explicit flush",
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=list(cases.CONFIGS))
+    ap.add_argument("--method", default="auto")
+    ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--no-cpu", dest="cpu", action="store_false")
+    ap.add_argument("--stage-sync", action="store_true",
+                    help="read stage events after every step (adds a host sync per step)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = cases.CONFIGS[args.config]
+    base = {"metric": METRIC, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64" if cfg["dtype"] == "float64" else "f32",
+            "data": "synthetic (seeded iid uniform points, N(0,1) complex data; BASELINE.json shapes)"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        Ms, Ts = cpu_sample_size(args.config)
+        v, per, cores = cpu_run(args.config, Ms, Ts, max(1, args.steps), args.warmup)
+        line = dict(base, value=v, ms_per_step=per * 1e3, impl="reference",
+                    config=config_block(args.config, 1),
+                    cpu_baseline={"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                                  "sample": f"{args.config} with M={Ms:.0e}, ntransf={Ts} per step "
+                                            "(oracle/ C+OpenMP restatement of the reference path, "
+                                            "scipy pocketfft)"},
+                    e2e={"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    res = gpu_run(args, rank, world, local_rank)
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        frac = res["achieved"] / res["peak"]
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get(args.config)
+            except Exception:
+                traffic = None
+        kern = "interp" if cfg["ttype"] == 2 else "spread"
+        n_launch = 4 + 2  # setpts: bin, scan, scatter, subproblem fill; + amplify/spread, deconv/interp
+        line = dict(base, value=res["value"], ms_per_step=res["elapsed"] / args.steps * 1e3,
+                    config=config_block(args.config, world),
+                    roofline={"bound": "hbm", "achieved": res["achieved"], "peak": res["peak"],
+                              "unit": "GB/s", "frac": frac, "traffic": traffic,
+                              "kernel": f"{kern} (k_{'interp_thread' if kern == 'interp' else 'spread_tile'})",
+                              "algorithmic_bytes": res["B"], "kernel_ms": res["hot_s"] * 1e3,
+                              "peak_source": f"{res['peak_kind']} MEASURED_PEAKS.json hbm_gbs"},
+                    stages_ms={k: v * 1e3 for k, v in res["stages"].items()},
+                    clocks=res["clocks"], gpu_launches=n_launch * args.steps)
+        if "e2e" in res:
+            line["e2e"] = res["e2e"]
+        if args.cpu and world == 1:
+            try:
+                Ms, Ts = cpu_sample_size(args.config)
+                v, per, cores = cpu_run(args.config, Ms, Ts, 1, 0)
+                line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                                        "sample": f"{args.config} with M={Ms:.0e}, ntransf={Ts}, one "
+                                                  "full transform (oracle/ C+OpenMP port, scipy FFT)"}
+            except Exception as exc:  # the baseline must never sink the GPU line
+                line["cpu_baseline"] = {"value": None, "error": str(exc)[:200]}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,224 @@
+/*
+ * esnufft_b200.h -- C ABI of the B200-native ES-kernel NUFFT core
+ * (libesnufft_b200.so, sm_100a).
+ *
+ * This is the drop-in boundary for the reference package `esnufft`
+ * (/root/reference/pkg/src/esnufft).  The reference has no C FFI: its
+ * boundary is the Python entry points, and its C-style convention lives in
+ * the status-code bindings `esnufftpy`
+ * (pkg/bindings/src/esnufftpy/__init__.py:1-24, 112-122): caller-allocated
+ * C-contiguous outputs, an int status (0 or an ErrorCode), argument misuse
+ * rejected with SIZE_ERROR before any core work, no handles retained.
+ * Every entry point below states the reference interface it replaces.
+ *
+ * Conventions
+ *  - complex arrays are interleaved (re, im) of the plan dtype
+ *    (ESN_F64: double, i.e. complex128; ESN_F32: float, i.e. complex64);
+ *  - mode arrays are C order (N_d, ..., N_1) with dimension 1 fastest and
+ *    centered ascending indices k = -floor(N/2) .. ceil(N/2)-1
+ *    (grid.py:61-111); batched arrays carry a leading ntransf axis;
+ *  - "device" pointers are CUDA device addresses (e.g. torch
+ *    .data_ptr()), "host" pointers are ordinary host memory;
+ *  - calls on a plan are stream ordered on the plan's stream and return
+ *    after enqueue; esn_plan_check() synchronises and reports data errors;
+ *  - thread safety: distinct plans may be used from distinct threads; the
+ *    cuFFT plan cache is mutex guarded (mirrors fft.py:87-111).
+ */
+#ifndef ESNUFFT_B200_H
+#define ESNUFFT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status table, identical to esnufft.errors.ErrorCode (errors.py:13-20). */
+enum {
+    ESN_SUCCESS = 0,
+    ESN_BAD_TOLERANCE = 1,
+    ESN_BOUNDS_VIOLATION = 2,
+    ESN_SIZE_ERROR = 3,
+    ESN_RESOURCE_ERROR = 4,
+    ESN_DATA_ERROR = 5,
+    ESN_INTERNAL_ERROR = 6
+};
+
+/* Arithmetic type of a plan (the reference is complex128 only,
+ * spreadinterp.py:198 / transforms.py:146). */
+enum { ESN_F64 = 0, ESN_F32 = 1 };
+/* OR into esn_plan_setpts' coord_dtype: coordinates are already grid units
+ * in [0, n) (the input convention of bin_sort, grid.py:202-211). */
+enum { ESN_COORD_GRID_UNITS = 0x10 };
+
+/* Spreader selection (esn_opts.method). */
+enum {
+    ESN_METHOD_AUTO = 0,
+    ESN_METHOD_GLOBAL = 1, /* point-parallel, direct global atomics        */
+    ESN_METHOD_TILE = 2    /* per-bin shared-memory tile + halo flush      */
+};
+
+/* Library version (major*10000 + minor*100 + patch). */
+int esn_version(void);
+/* Thread-local text of the last non-zero status. */
+const char *esn_last_error(void);
+
+/* ------------------------------------------------------------------ */
+/* Host kernel math -- replaces kernel.py / grid.py helpers.           */
+/* ------------------------------------------------------------------ */
+
+/* KernelParams (kernel.py:51-84). */
+typedef struct {
+    int w;         /* width in fine-grid points, 2..16          */
+    double beta;   /* ES shape, 2.30 w at sigma = 2              */
+    double sigma;  /* 2.0 or 1.25                                */
+    double gamma;  /* safety factor                              */
+    int p_quad;    /* positive Gauss-Legendre nodes >= 1.5w + 2  */
+} esn_kernel_params;
+
+/* select_params(tolerance, sigma) -- kernel.py:110-131. */
+int esn_select_params(double tol, double sigma, esn_kernel_params *out);
+/* params_for_width(w, sigma) -- kernel.py:98-107. */
+int esn_params_for_width(int w, double sigma, esn_kernel_params *out);
+/* class_tolerance(w, sigma) -- kernel.py:134-143. */
+double esn_class_tolerance(int w, double sigma);
+/* next_smooth(n) -- grid.py:34-58. */
+int esn_next_smooth(int64_t n, int64_t *out);
+/* fine_grid_sizes(num_modes, sigma, w) -- grid.py:141-149. */
+int esn_fine_grid_sizes(int dim, const int64_t *nmodes, double sigma, int w,
+                        int64_t *sizes);
+/* gauss_legendre(n) -- kernel.py:167-203 (host arrays of length n). */
+int esn_gauss_legendre(int n, double *nodes, double *weights);
+/* kernel_ft(params, alpha, ks) -- kernel.py:213-231 (host arrays). */
+int esn_kernel_ft(const esn_kernel_params *p, double alpha, int64_t nk,
+                  const double *k, double *out);
+/* fseries_correction(params, n, N) -- kernel.py:234-288 (host array N). */
+int esn_fseries_correction(const esn_kernel_params *p, int64_t n,
+                           int64_t nmodes, double *out);
+/* build_piecewise_poly(params).coeffs -- kernel.py:322-367; coeffs is a
+ * host array w x (w+4), highest degree first; residual may be NULL. */
+int esn_piecewise_poly(const esn_kernel_params *p, double *coeffs,
+                       double *residual);
+
+/* ------------------------------------------------------------------ */
+/* Options -- TransformOptions (transforms.py:44-80) plus GPU knobs.   */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    double sigma;              /* 2.0 (default) or 1.25                     */
+    int check_bounds;          /* reject |x| > 3 pi (grid.py:152-164)       */
+    int use_exact_kernel;      /* exp/sqrt instead of Horner                */
+    int64_t max_grid_values;   /* ResourceError cap (transforms.py:129-133) */
+    int dtype;                 /* ESN_F64 / ESN_F32                         */
+    int method;                /* ESN_METHOD_*                              */
+    int bin_size[3];           /* 0 = auto                                  */
+    int max_subprob;           /* 0 = auto                                  */
+    int timing;                /* record per-stage CUDA events              */
+    void *stream;              /* cudaStream_t, NULL = legacy default       */
+    const esn_kernel_params *params; /* override select_params (may be NULL) */
+    const double *coeffs;      /* override Horner table w x (w+4) (NULL)    */
+} esn_opts;
+
+void esn_default_opts(esn_opts *o);
+
+/* ------------------------------------------------------------------ */
+/* Plan API -- the transforms.py:136-218 pipelines as a reusable plan   */
+/* (sort / phi-hat / cuFFT plan amortised across executes).  */
+/* ------------------------------------------------------------------ */
+typedef struct esn_plan_s *esn_plan;
+
+/* type 1 (exec_type1, transforms.py:136) or 2 (exec_type2, :176).
+ * nmodes = (N_1, .., N_dim).  isign = +1 / -1. */
+int esn_plan_create(int type, int dim, const int64_t *nmodes, int isign,
+                    int ntransf, double tol, const esn_opts *opts,
+                    esn_plan *out);
+/* Spread/interp-only plan on an explicit fine grid n = (n_1..n_dim):
+ * replaces spreadinterp.spread / interp (spreadinterp.py:187, 259). */
+int esn_spreader_create(int dim, const int64_t *nfine, int ntransf,
+                        const esn_opts *opts, esn_plan *out);
+/* Fold, grid-scale and bin-sort M points (device arrays of coord_dtype);
+ * replaces build_point_set + ensure_sorted (spreadinterp.py:79-114). */
+int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x,
+                    const void *y, const void *z);
+/* Run the transform (device arrays).  type 1: c (ntransf, M) -> f
+ * (ntransf, N_d..N_1); type 2: f -> c. */
+int esn_plan_execute(esn_plan p, void *c, void *f);
+/* Spread c -> grid / interp grid -> c on the plan's fine grid (device
+ * arrays; grid is (ntransf, n_d..n_1)); spread zeroes grid itself. */
+int esn_plan_spread(esn_plan p, const void *c, void *grid);
+int esn_plan_interp(esn_plan p, const void *grid, void *c);
+/* Synchronise the plan stream and report data errors found on device:
+ * returns ESN_DATA_ERROR / ESN_BOUNDS_VIOLATION with the offending point
+ * index in info[0] and the (1-based) dimension in info[1] (0 = strength).*/
+int esn_plan_check(esn_plan p, int64_t *info);
+/* Stage seconds of the last setpts+execute, reference keys
+ * (transforms.py:83-85); requires opts.timing. */
+int esn_plan_stage_times(esn_plan p, double *sort_s, double *spread_s,
+                         double *fft_s, double *correct_s);
+/* Device seconds of the last spread kernel (type 1 / spreader) or interp
+ * kernel (type 2) alone -- the roofline numerator's denominator. */
+int esn_plan_hot_kernel_seconds(esn_plan p, double *seconds);
+/* Fine grid sizes (n_1..n_3) and kernel parameters of a plan. */
+int esn_plan_info(esn_plan p, int64_t *nfine, esn_kernel_params *kp);
+/* Bin geometry of a plan: total bins, bin size and bins per dimension. */
+int esn_plan_bins(esn_plan p, int *nbins, int *bin_size, int *bins_per_dim);
+/* Copy the plan's bin sort into caller device buffers (any may be NULL):
+ * perm (M int32, sorted slot -> original index), keys (M int32, bin of each
+ * original point), bin_start (nbins + 1 int32).  Replaces the
+ * BinSortPermutation of grid.py:171-182. */
+int esn_plan_sort_view(esn_plan p, void *perm, void *keys, void *bin_start);
+/* Device scratch bytes held by the plan. */
+int64_t esn_plan_device_bytes(esn_plan p);
+int esn_plan_destroy(esn_plan p);
+
+/* fft_exec(FftPlanKey, data) -- fft.py:114-124: in-place unnormalised
+ * n-D FFT of ntransf device grids (n_1..n_dim), sign +1 applies
+ * e^{+2 pi i l k / n} (the reference "FORWARD"). */
+int esn_fft(int dim, int dtype, int ntransf, const int64_t *nfine,
+            void *data, int sign, void *stream);
+
+/* fold_coords + grid scaling (grid.py:152-168, spreadinterp.py:90-101) on
+ * device: g[i] = (x[i] mod 2 pi) * n / 2 pi in [0, n), float64 output,
+ * original order (n = 0: the folded radians in [0, 2 pi)).  Non-finite
+ * inputs give 0. */
+int esn_fold_coords(int64_t M, int coord_dtype, const void *x, int64_t n,
+                    void *g, void *stream);
+/* Direct O(M nk) sums f_k = sum_j c_j exp(isign i s_k . x_j) in float64 on
+ * device (oracle.py:52-88, direct_type3); t/u and y/z unused below dim. */
+int esn_direct(int dim, int64_t M, const void *x, const void *y, const void *z,
+               const void *c, int64_t nk, const void *s, const void *t,
+               const void *u, int isign, void *out, void *stream);
+
+/* ------------------------------------------------------------------ */
+/* One-shot routines on HOST buffers, mirroring the esnufftpy status  */
+/* bindings (bindings/src/esnufftpy/__init__.py:173-215).  Complex     */
+/* buffers are interleaved complex128 (or complex64 when opts->dtype is */
+/* ESN_F32 -- coordinates stay float64).  Host<->device copies happen  */
+/* inside.  opts may be NULL.                                          */
+/* ------------------------------------------------------------------ */
+int esn_nufft1d1(int64_t M, const double *x, const void *c, int isign,
+                 double tol, int64_t N1, void *f, const esn_opts *opts);
+int esn_nufft2d1(int64_t M, const double *x, const double *y, const void *c,
+                 int isign, double tol, int64_t N1, int64_t N2, void *f,
+                 const esn_opts *opts);
+int esn_nufft3d1(int64_t M, const double *x, const double *y, const double *z,
+                 const void *c, int isign, double tol, int64_t N1, int64_t N2,
+                 int64_t N3, void *f, const esn_opts *opts);
+int esn_nufft1d2(int64_t M, const double *x, void *c, int isign, double tol,
+                 int64_t N1, const void *f, const esn_opts *opts);
+int esn_nufft2d2(int64_t M, const double *x, const double *y, void *c,
+                 int isign, double tol, int64_t N1, int64_t N2, const void *f,
+                 const esn_opts *opts);
+int esn_nufft3d2(int64_t M, const double *x, const double *y, const double *z,
+                 void *c, int isign, double tol, int64_t N1, int64_t N2,
+                 int64_t N3, const void *f, const esn_opts *opts);
+/* Batched host-buffer type 1/2 (ntransf strength / mode vectors sharing
+ * one point set); x,y,z may be NULL beyond dim. */
+int esn_nufft_host(int type, int dim, int64_t M, const double *x,
+                   const double *y, const double *z, int ntransf, void *c,
+                   int isign, double tol, const int64_t *nmodes, void *f,
+                   const esn_opts *opts);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ESNUFFT_B200_H */

@@ -1,0 +1,794 @@
+// esn_plan.cu -- plan runtime and the C ABI of libesnufft_b200.so.
+//
+// A plan owns everything a repeated transform can reuse: kernel parameters
+// and the Horner table (kernel.py:322-367), the phi-hat correction vectors
+// (kernel.py:234-288) on device, the bin geometry, the sorted point set, the
+// fine grid and a cached cuFFT plan.  The pipelines are those of
+// transforms.py:136-218 with the isign = -1 conjugations replaced by the
+// opposite cuFFT direction (the kernel is real, so conj(F+(conj b)) = F-(b)).
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
+#include "esn_internal.h"
+
+namespace esn {
+const char *last_error();
+}
+using namespace esn;
+
+#define ESN_VERSION 100  // 0.1.0 series, mirrors esnufft.__version__ (__init__.py:21)
+
+static inline size_t real_size(int dtype) { return dtype == ESN_F64 ? 8 : 4; }
+
+// ---------------------------------------------------------------------------
+// cuFFT plan cache keyed by (dim, n, dtype, batch) -- the fft.py:87-111 analog.
+namespace {
+struct FftKey {
+    int dim, n1, n2, n3, dtype, batch, device;
+    bool operator<(const FftKey &o) const {
+        return std::tie(dim, n1, n2, n3, dtype, batch, device) <
+               std::tie(o.dim, o.n1, o.n2, o.n3, o.dtype, o.batch, o.device);
+    }
+};
+std::mutex g_fft_mu;
+std::map<FftKey, cufftHandle> g_fft_cache;
+
+int get_fft_plan(int dim, const int *n, int dtype, int batch, cufftHandle *out) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    FftKey key{dim, n[0], dim > 1 ? n[1] : 1, dim > 2 ? n[2] : 1, dtype, batch, dev};
+    std::lock_guard<std::mutex> lk(g_fft_mu);
+    auto it = g_fft_cache.find(key);
+    if (it != g_fft_cache.end()) {
+        *out = it->second;
+        return ESN_SUCCESS;
+    }
+    int dims[3];
+    for (int d = 0; d < dim; ++d) dims[d] = n[dim - 1 - d];  // slowest first
+    int64_t dist = 1;
+    for (int d = 0; d < dim; ++d) dist *= n[d];
+    cufftHandle h;
+    cufftResult r = cufftPlanMany(&h, dim, dims, nullptr, 1, (int)dist, nullptr, 1, (int)dist,
+                                  dtype == ESN_F64 ? CUFFT_Z2Z : CUFFT_C2C, batch);
+    if (r != CUFFT_SUCCESS) return fail(ESN_INTERNAL_ERROR, "cufftPlanMany failed (%d)", (int)r);
+    g_fft_cache[key] = h;
+    *out = h;
+    return ESN_SUCCESS;
+}
+
+int run_fft(int dim, const int *n, int dtype, int batch, void *data, int sign, cudaStream_t st) {
+    cufftHandle h;
+    int rc = get_fft_plan(dim, n, dtype, batch, &h);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(g_fft_mu);  // SetStream + enqueue as one unit
+    if (cufftSetStream(h, st) != CUFFT_SUCCESS) return fail(ESN_INTERNAL_ERROR, "cufftSetStream failed");
+    // reference FORWARD = e^{+2 pi i lk/n} = CUFFT_INVERSE (fft.py:3-6, 52-59)
+    const int dir = sign > 0 ? CUFFT_INVERSE : CUFFT_FORWARD;
+    cufftResult r = dtype == ESN_F64
+                        ? cufftExecZ2Z(h, (cufftDoubleComplex *)data, (cufftDoubleComplex *)data, dir)
+                        : cufftExecC2C(h, (cufftComplex *)data, (cufftComplex *)data, dir);
+    if (r != CUFFT_SUCCESS) return fail(ESN_INTERNAL_ERROR, "cufftExec failed (%d)", (int)r);
+    return ESN_SUCCESS;
+}
+}  // namespace
+
+// ---------------------------------------------------------------------------
+struct esn_plan_s {
+    int type = 0, dim = 0, dtype = ESN_F64, isign = 1, ntransf = 1;
+    int64_t N[3] = {1, 1, 1};
+    int n[3] = {1, 1, 1};
+    esn_kernel_params kp{};
+    std::vector<double> coeffs;
+    esn_opts opts{};
+    cudaStream_t st = nullptr;
+    Geom geom{};
+    int nbins = 1, maxsub = 8192, method = ESN_METHOD_TILE;
+    int64_t G = 1;
+    // device state
+    void *pk[3] = {nullptr, nullptr, nullptr};
+    void *gs[3] = {nullptr, nullptr, nullptr};
+    int *perm = nullptr, *key = nullptr, *rank = nullptr;
+    int *bin_count = nullptr, *bin_start = nullptr, *subofs = nullptr, *nsub = nullptr, *work = nullptr;
+    int4 *subprob = nullptr;
+    unsigned long long *flags = nullptr;
+    void *grid = nullptr;
+    int64_t M = -1, Mcap = 0, subcap = 0;
+    int64_t device_bytes = 0;
+    cudaEvent_t ev[8] = {};
+    bool have_events = false;
+    bool points_set = false;
+    float last_ms[4] = {0, 0, 0, 0};  // sort, spread, fft, correct
+};
+
+template <typename P>
+static int dmalloc(esn_plan p, P **ptr, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMalloc((void **)ptr, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(ESN_RESOURCE_ERROR, "device allocation of %zu bytes failed (%s)", bytes, cudaGetErrorString(e));
+    }
+    p->device_bytes += (int64_t)bytes;
+    return ESN_SUCCESS;
+}
+
+static void dfree(void *ptr) {
+    if (ptr) cudaFree(ptr);
+}
+
+static void choose_bins(esn_plan p) {
+    const int dim = p->dim, w = p->kp.w;
+    int bs[3] = {1, 1, 1};
+    for (int d = 0; d < 3; ++d)
+        if (p->opts.bin_size[d] > 0) bs[d] = p->opts.bin_size[d];
+    bool user = p->opts.bin_size[0] > 0;
+    if (!user) {
+        if (dim == 1) {
+            bs[0] = 1024;
+        } else if (dim == 2) {
+            bs[0] = 32;
+            bs[1] = 32;
+        } else {
+            bs[0] = 16;
+            bs[1] = 8;
+            bs[2] = 8;
+        }
+        // keep the shared-memory tile within ~100 KB (2 CTAs per SM)
+        while (tile_smem_bytes(dim, w, bs, p->dtype) > 100 * 1024) {
+            int big = 0;
+            for (int d = 1; d < dim; ++d)
+                if (bs[d] > bs[big]) big = d;
+            if (bs[big] <= 2) break;
+            bs[big] /= 2;
+        }
+    }
+    p->nbins = 1;
+    for (int d = 0; d < 3; ++d) {
+        p->geom.bs[d] = d < dim ? bs[d] : 1;
+        p->geom.n[d] = p->n[d];
+        p->geom.nb[d] = d < dim ? (p->n[d] + bs[d] - 1) / bs[d] : 1;
+        p->nbins *= p->geom.nb[d];
+    }
+    p->geom.dim = dim;
+    p->geom.w = w;
+}
+
+static int plan_common_init(esn_plan p, const esn_opts *o) {
+    if (o)
+        p->opts = *o;
+    else
+        esn_default_opts(&p->opts);
+    p->dtype = p->opts.dtype == ESN_F32 ? ESN_F32 : ESN_F64;
+    p->st = (cudaStream_t)p->opts.stream;
+    p->coeffs.assign((size_t)p->kp.w * (p->kp.w + 4), 0.0);
+    if (p->opts.coeffs) {
+        std::memcpy(p->coeffs.data(), p->opts.coeffs, p->coeffs.size() * sizeof(double));
+    } else {
+        int rc = piecewise_poly(p->kp, p->coeffs.data(), nullptr);
+        if (rc) return rc;
+    }
+    p->opts.params = nullptr;
+    p->opts.coeffs = nullptr;
+    p->G = 1;
+    for (int d = 0; d < 3; ++d) p->G *= p->n[d];
+    if (p->G * 1 > p->opts.max_grid_values)  // transforms.py:129-133
+        return fail(ESN_RESOURCE_ERROR,
+                    "fine grids need %lld complex values, over the cap of %lld; this regime is better "
+                    "served by direct summation",
+                    (long long)p->G, (long long)p->opts.max_grid_values);
+    choose_bins(p);
+    p->method = p->opts.method;
+    if (p->method == ESN_METHOD_AUTO) p->method = (p->dim == 1) ? ESN_METHOD_GLOBAL : ESN_METHOD_TILE;
+    p->maxsub = p->opts.max_subprob > 0 ? p->opts.max_subprob : 8192;
+    int rc;
+    if ((rc = dmalloc(p, &p->bin_count, sizeof(int) * p->nbins))) return rc;
+    if ((rc = dmalloc(p, &p->bin_start, sizeof(int) * (p->nbins + 1)))) return rc;
+    if ((rc = dmalloc(p, &p->subofs, sizeof(int) * (p->nbins + 1)))) return rc;
+    if ((rc = dmalloc(p, &p->nsub, sizeof(int) * 2))) return rc;
+    if ((rc = dmalloc(p, &p->work, sizeof(int) * 2))) return rc;
+    if ((rc = dmalloc(p, &p->flags, sizeof(unsigned long long) * 8))) return rc;
+    if ((rc = dmalloc(p, &p->grid, real_size(p->dtype) * 2 * (size_t)p->G * p->ntransf))) return rc;
+    ESN_CUDA_TRY(cudaMemsetAsync(p->flags, 0xff, sizeof(unsigned long long) * 8, p->st));
+    if (p->opts.timing) {
+        for (int i = 0; i < 8; ++i) ESN_CUDA_TRY(cudaEventCreate(&p->ev[i]));
+        p->have_events = true;
+    }
+    return ESN_SUCCESS;
+}
+
+static int upload_corrections(esn_plan p) {
+    for (int d = 0; d < p->dim; ++d) {
+        std::vector<double> v((size_t)p->N[d]);
+        int rc = fseries_correction(p->kp, p->n[d], p->N[d], v.data());
+        if (rc) return rc;
+        if ((rc = dmalloc(p, &p->pk[d], real_size(p->dtype) * v.size()))) return rc;
+        if (p->dtype == ESN_F64) {
+            ESN_CUDA_TRY(cudaMemcpy(p->pk[d], v.data(), v.size() * 8, cudaMemcpyHostToDevice));
+        } else {
+            std::vector<float> f(v.begin(), v.end());
+            ESN_CUDA_TRY(cudaMemcpy(p->pk[d], f.data(), f.size() * 4, cudaMemcpyHostToDevice));
+        }
+    }
+    return ESN_SUCCESS;
+}
+
+extern "C" {
+
+int esn_version(void) { return ESN_VERSION; }
+const char *esn_last_error(void) { return esn::last_error(); }
+
+int esn_select_params(double tol, double sigma, esn_kernel_params *out) {
+    if (!out) return fail(ESN_SIZE_ERROR, "null output");
+    return select_params(tol, sigma, out);
+}
+int esn_params_for_width(int w, double sigma, esn_kernel_params *out) {
+    if (!out) return fail(ESN_SIZE_ERROR, "null output");
+    return params_for_width(w, sigma, out);
+}
+double esn_class_tolerance(int w, double sigma) { return class_tolerance(w, sigma); }
+int esn_next_smooth(int64_t n, int64_t *out) {
+    if (n < 1) return fail(ESN_SIZE_ERROR, "next_smooth needs n >= 1, got %lld", (long long)n);
+    if (n > ((int64_t)1 << 60)) return fail(ESN_SIZE_ERROR, "next_smooth overflow for n=%lld", (long long)n);
+    *out = next_smooth(n);
+    return ESN_SUCCESS;
+}
+int esn_fine_grid_sizes(int dim, const int64_t *nmodes, double sigma, int w, int64_t *sizes) {
+    for (int d = 0; d < dim; ++d) {
+        if (nmodes[d] < 1) return fail(ESN_SIZE_ERROR, "mode counts must be >= 1");
+        int64_t fl = std::max((int64_t)std::ceil(sigma * (double)nmodes[d]), (int64_t)(2 * w));
+        sizes[d] = next_smooth(fl);
+    }
+    return ESN_SUCCESS;
+}
+int esn_gauss_legendre(int n, double *nodes, double *weights) {
+    if (n < 1) return fail(ESN_SIZE_ERROR, "gauss_legendre needs n >= 1, got %d", n);
+    gauss_legendre(n, nodes, weights);
+    return ESN_SUCCESS;
+}
+int esn_kernel_ft(const esn_kernel_params *p, double alpha, int64_t nk, const double *k, double *out) {
+    if (!(alpha > 0)) return fail(ESN_SIZE_ERROR, "alpha must be positive, got %g", alpha);
+    kernel_ft(*p, alpha, nk, k, out);
+    return ESN_SUCCESS;
+}
+int esn_fseries_correction(const esn_kernel_params *p, int64_t n, int64_t nmodes, double *out) {
+    return fseries_correction(*p, n, nmodes, out);
+}
+int esn_piecewise_poly(const esn_kernel_params *p, double *coeffs, double *residual) {
+    return piecewise_poly(*p, coeffs, residual);
+}
+
+void esn_default_opts(esn_opts *o) {
+    std::memset(o, 0, sizeof(*o));
+    o->sigma = 2.0;
+    o->max_grid_values = (int64_t)1 << 31;  // transforms.py:41
+    o->dtype = ESN_F64;
+    o->method = ESN_METHOD_AUTO;
+}
+
+int esn_plan_destroy(esn_plan p) {
+    if (!p) return ESN_SUCCESS;
+    if (p->st) cudaStreamSynchronize(p->st);
+    else cudaDeviceSynchronize();
+    for (int d = 0; d < 3; ++d) {
+        dfree(p->pk[d]);
+        dfree(p->gs[d]);
+    }
+    dfree(p->perm);
+    dfree(p->key);
+    dfree(p->rank);
+    dfree(p->bin_count);
+    dfree(p->bin_start);
+    dfree(p->subofs);
+    dfree(p->nsub);
+    dfree(p->work);
+    dfree(p->subprob);
+    dfree(p->flags);
+    dfree(p->grid);
+    if (p->have_events)
+        for (int i = 0; i < 8; ++i) cudaEventDestroy(p->ev[i]);
+    delete p;
+    return ESN_SUCCESS;
+}
+
+int esn_plan_create(int type, int dim, const int64_t *nmodes, int isign, int ntransf, double tol,
+                    const esn_opts *opts, esn_plan *out) {
+    if (!out) return fail(ESN_SIZE_ERROR, "null plan pointer");
+    *out = nullptr;
+    if (type != 1 && type != 2) return fail(ESN_SIZE_ERROR, "type must be 1 or 2, got %d", type);
+    if (dim < 1 || dim > 3) return fail(ESN_SIZE_ERROR, "dimension must be 1, 2, or 3, got %d", dim);
+    if (isign != 1 && isign != -1) return fail(ESN_SIZE_ERROR, "isign must be +1 or -1, got %d", isign);
+    if (ntransf < 1) return fail(ESN_SIZE_ERROR, "ntransf must be >= 1, got %d", ntransf);
+    for (int d = 0; d < dim; ++d)
+        if (nmodes[d] < 1) return fail(ESN_SIZE_ERROR, "mode counts must be >= 1");
+    esn_opts o;
+    if (opts) o = *opts; else esn_default_opts(&o);
+    esn_plan p = new esn_plan_s();
+    p->type = type;
+    p->dim = dim;
+    p->isign = isign;
+    p->ntransf = ntransf;
+    int rc;
+    if (o.params) {
+        p->kp = *o.params;
+        if ((rc = params_for_width(p->kp.w, p->kp.sigma, &p->kp)) != ESN_SUCCESS) { delete p; return rc; }
+        p->kp = *o.params;
+    } else if ((rc = select_params(tol, o.sigma, &p->kp)) != ESN_SUCCESS) {
+        delete p;
+        return rc;
+    }
+    for (int d = 0; d < dim; ++d) {
+        p->N[d] = nmodes[d];
+        int64_t fl = std::max((int64_t)std::ceil(o.sigma * (double)nmodes[d]), (int64_t)(2 * p->kp.w));
+        int64_t nn = next_smooth(fl);
+        if (nn > INT_MAX) { delete p; return fail(ESN_RESOURCE_ERROR, "fine grid axis %lld too large", (long long)nn); }
+        p->n[d] = (int)nn;
+    }
+    if ((rc = plan_common_init(p, &o)) || (rc = upload_corrections(p))) {
+        esn_plan_destroy(p);
+        return rc;
+    }
+    *out = p;
+    return ESN_SUCCESS;
+}
+
+int esn_spreader_create(int dim, const int64_t *nfine, int ntransf, const esn_opts *opts, esn_plan *out) {
+    if (!out) return fail(ESN_SIZE_ERROR, "null plan pointer");
+    *out = nullptr;
+    if (dim < 1 || dim > 3) return fail(ESN_SIZE_ERROR, "dimension must be 1, 2, or 3, got %d", dim);
+    esn_opts o;
+    if (opts) o = *opts; else esn_default_opts(&o);
+    if (!o.params) return fail(ESN_SIZE_ERROR, "spreader plans need explicit kernel params");
+    esn_plan p = new esn_plan_s();
+    p->type = 0;
+    p->dim = dim;
+    p->ntransf = ntransf < 1 ? 1 : ntransf;
+    p->kp = *o.params;
+    int rc;
+    esn_kernel_params chk;
+    if ((rc = params_for_width(p->kp.w, p->kp.sigma, &chk))) { delete p; return rc; }
+    for (int d = 0; d < dim; ++d) {
+        if (nfine[d] < 1 || nfine[d] > INT_MAX) { delete p; return fail(ESN_SIZE_ERROR, "bad fine grid size"); }
+        p->n[d] = (int)nfine[d];
+    }
+    if ((rc = plan_common_init(p, &o))) {
+        esn_plan_destroy(p);
+        return rc;
+    }
+    *out = p;
+    return ESN_SUCCESS;
+}
+
+int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const void *y, const void *z) {
+    if (!p) return fail(ESN_SIZE_ERROR, "null plan");
+    if (M < 0 || M > INT_MAX) return fail(ESN_SIZE_ERROR, "point count %lld outside [0, 2^31)", (long long)M);
+    const void *xs[3] = {x, y, z};
+    for (int d = 0; d < p->dim; ++d)
+        if (M > 0 && !xs[d]) return fail(ESN_SIZE_ERROR, "coordinate array %d missing", d + 1);
+    int rc;
+    if (M > p->Mcap) {
+        for (int d = 0; d < 3; ++d) { dfree(p->gs[d]); p->gs[d] = nullptr; }
+        dfree(p->perm); dfree(p->key); dfree(p->rank);
+        p->perm = p->key = p->rank = nullptr;
+        for (int d = 0; d < p->dim; ++d)
+            if ((rc = dmalloc(p, &p->gs[d], real_size(p->dtype) * M))) return rc;
+        if ((rc = dmalloc(p, &p->perm, sizeof(int) * M))) return rc;
+        if ((rc = dmalloc(p, &p->key, sizeof(int) * M))) return rc;
+        if ((rc = dmalloc(p, &p->rank, sizeof(int) * M))) return rc;
+        p->Mcap = M;
+    }
+    const int64_t subneed = p->nbins + M / p->maxsub + 1;
+    if (subneed > p->subcap) {
+        dfree(p->subprob);
+        p->subprob = nullptr;
+        if ((rc = dmalloc(p, &p->subprob, sizeof(int4) * subneed))) return rc;
+        p->subcap = subneed;
+    }
+    p->M = M;
+    if (p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[0], p->st));
+    ESN_CUDA_TRY(cudaMemsetAsync(p->bin_count, 0, sizeof(int) * p->nbins, p->st));
+    ESN_CUDA_TRY(cudaMemsetAsync(p->flags, 0xff, sizeof(unsigned long long) * 8, p->st));
+    SetptsArgs a{};
+    a.g = p->geom;
+    a.M = M;
+    a.coord_f32 = (coord_dtype & 0xf) == ESN_F32;
+    a.grid_units = (coord_dtype & ESN_COORD_GRID_UNITS) != 0;
+    for (int d = 0; d < 3; ++d) {
+        a.x[d] = d < p->dim ? xs[d] : nullptr;
+        a.scale[d] = (double)p->n[d] / (2.0 * M_PI);  // sizes[d] / TWO_PI (spreadinterp.py:99)
+        a.gs[d] = p->gs[d];
+    }
+    a.key = p->key;
+    a.rank = p->rank;
+    a.bin_count = p->bin_count;
+    a.bin_start = p->bin_start;
+    a.perm = p->perm;
+    a.flags = p->flags;
+    a.check_bounds = p->opts.check_bounds;
+    if ((rc = launch_setpts(a, p->dtype, p->nbins, p->maxsub, p->subprob, p->nsub, p->subofs, p->st))) return rc;
+    if (p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[1], p->st));
+    p->points_set = true;
+    return ESN_SUCCESS;
+}
+
+}  // extern "C"
+
+template <typename T>
+static SpreadArgs<T> make_spread_args(esn_plan p, const void *c, void *grid) {
+    SpreadArgs<T> a{};
+    a.g = p->geom;
+    const int w = p->kp.w;
+    for (int i = 0; i < w * (w + 4); ++i) a.k.coef[i] = (T)p->coeffs[i];
+    a.k.beta = (T)p->kp.beta;
+    a.k.use_exact = p->opts.use_exact_kernel;
+    a.M = p->M;
+    a.ntransf = p->ntransf;
+    for (int d = 0; d < 3; ++d) a.gs[d] = (const T *)p->gs[d];
+    a.perm = p->perm;
+    a.bin_start = p->bin_start;
+    a.subprob = p->subprob;
+    a.nsub = p->nsub;
+    a.work = p->work;
+    a.c = (const T *)c;
+    a.grid = (T *)grid;
+    a.gstride = p->G;
+    a.flags = p->flags;
+    return a;
+}
+
+static int do_spread(esn_plan p, const void *c, void *grid) {
+    ESN_CUDA_TRY(cudaMemsetAsync(grid, 0, real_size(p->dtype) * 2 * (size_t)p->G * p->ntransf, p->st));
+    ESN_CUDA_TRY(cudaMemsetAsync(p->work, 0, sizeof(int), p->st));
+    if (p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[6], p->st));
+    int rc = p->dtype == ESN_F64
+                 ? launch_spread<double>(make_spread_args<double>(p, c, grid), p->method, p->nbins, p->st)
+                 : launch_spread<float>(make_spread_args<float>(p, c, grid), p->method, p->nbins, p->st);
+    if (!rc && p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[7], p->st));
+    return rc;
+}
+
+static int do_interp(esn_plan p, const void *grid, void *c) {
+    if (p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[6], p->st));
+    int rc = p->dtype == ESN_F64
+                 ? launch_interp<double>(make_spread_args<double>(p, nullptr, nullptr), (double *)c,
+                                         (const double *)grid, p->st)
+                 : launch_interp<float>(make_spread_args<float>(p, nullptr, nullptr), (float *)c,
+                                        (const float *)grid, p->st);
+    if (!rc && p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[7], p->st));
+    return rc;
+}
+
+extern "C" {
+
+int esn_plan_spread(esn_plan p, const void *c, void *grid) {
+    if (!p || !p->points_set) return fail(ESN_SIZE_ERROR, "plan has no points (call esn_plan_setpts first)");
+    ESN_CUDA_TRY(cudaMemsetAsync(p->flags + 6, 0xff, sizeof(unsigned long long), p->st));
+    return do_spread(p, c, grid);
+}
+
+int esn_plan_interp(esn_plan p, const void *grid, void *c) {
+    if (!p || !p->points_set) return fail(ESN_SIZE_ERROR, "plan has no points (call esn_plan_setpts first)");
+    return do_interp(p, grid, c);
+}
+
+int esn_plan_execute(esn_plan p, void *c, void *f) {
+    if (!p || !p->points_set) return fail(ESN_SIZE_ERROR, "plan has no points (call esn_plan_setpts first)");
+    if (p->type != 1 && p->type != 2) return fail(ESN_SIZE_ERROR, "spreader plans have no execute");
+    int rc;
+    const bool ev = p->have_events;
+    ESN_CUDA_TRY(cudaMemsetAsync(p->flags + 6, 0xff, sizeof(unsigned long long), p->st));
+    if (p->type == 1) {
+        if (ev) ESN_CUDA_TRY(cudaEventRecord(p->ev[2], p->st));
+        if ((rc = do_spread(p, c, p->grid))) return rc;
+        if (ev) ESN_CUDA_TRY(cudaEventRecord(p->ev[3], p->st));
+        if ((rc = run_fft(p->dim, p->n, p->dtype, p->ntransf, p->grid, p->isign, p->st))) return rc;
+        if (ev) ESN_CUDA_TRY(cudaEventRecord(p->ev[4], p->st));
+        if (p->dtype == ESN_F64)
+            rc = launch_deconv<double>(p->dim, p->ntransf, p->n, p->N, (const double *)p->grid, (const double *)p->pk[0],
+                                       (const double *)p->pk[1], (const double *)p->pk[2], (double *)f, p->st);
+        else
+            rc = launch_deconv<float>(p->dim, p->ntransf, p->n, p->N, (const float *)p->grid, (const float *)p->pk[0],
+                                      (const float *)p->pk[1], (const float *)p->pk[2], (float *)f, p->st);
+        if (rc) return rc;
+        if (ev) ESN_CUDA_TRY(cudaEventRecord(p->ev[5], p->st));
+    } else {
+        if (ev) ESN_CUDA_TRY(cudaEventRecord(p->ev[2], p->st));
+        if (p->dtype == ESN_F64)
+            rc = launch_amplify<double>(p->dim, p->ntransf, p->n, p->N, (const double *)f, (const double *)p->pk[0],
+                                        (const double *)p->pk[1], (const double *)p->pk[2], (double *)p->grid,
+                                        p->flags + 6, p->st);
+        else
+            rc = launch_amplify<float>(p->dim, p->ntransf, p->n, p->N, (const float *)f, (const float *)p->pk[0],
+                                       (const float *)p->pk[1], (const float *)p->pk[2], (float *)p->grid,
+                                       p->flags + 6, p->st);
+        if (rc) return rc;
+        if (ev) ESN_CUDA_TRY(cudaEventRecord(p->ev[3], p->st));
+        if ((rc = run_fft(p->dim, p->n, p->dtype, p->ntransf, p->grid, p->isign, p->st))) return rc;
+        if (ev) ESN_CUDA_TRY(cudaEventRecord(p->ev[4], p->st));
+        if ((rc = do_interp(p, p->grid, c))) return rc;
+        if (ev) ESN_CUDA_TRY(cudaEventRecord(p->ev[5], p->st));
+    }
+    return ESN_SUCCESS;
+}
+
+int esn_plan_check(esn_plan p, int64_t *info) {
+    if (!p) return fail(ESN_SIZE_ERROR, "null plan");
+    ESN_CUDA_TRY(cudaStreamSynchronize(p->st));
+    unsigned long long h[8];
+    ESN_CUDA_TRY(cudaMemcpy(h, p->flags, sizeof(h), cudaMemcpyDeviceToHost));
+    const unsigned long long none = ~0ull;
+    int64_t dummy[2];
+    if (!info) info = dummy;
+    info[0] = -1;
+    info[1] = -1;
+    auto strength = [&]() -> int {
+        if (h[6] != none) {
+            info[0] = (int64_t)h[6];
+            info[1] = 0;
+            return fail(ESN_DATA_ERROR, "non-finite %s at index %lld", p->type == 2 ? "mode coefficient" : "strength",
+                        (long long)h[6]);
+        }
+        return ESN_SUCCESS;
+    };
+    if (p->type == 2) {
+        int rc = strength();
+        if (rc) return rc;
+    }
+    for (int d = 0; d < p->dim; ++d) {
+        if (h[d] != none) {
+            info[0] = (int64_t)h[d];
+            info[1] = d + 1;
+            return fail(ESN_DATA_ERROR, "non-finite coordinate at index %lld in dimension %d", (long long)h[d], d + 1);
+        }
+        if (p->opts.check_bounds && h[3 + d] != none) {
+            info[0] = (int64_t)h[3 + d];
+            info[1] = d + 1;
+            return fail(ESN_BOUNDS_VIOLATION, "coordinate at index %lld outside [-3 pi, 3 pi]", (long long)h[3 + d]);
+        }
+    }
+    if (p->type != 2) return strength();
+    return ESN_SUCCESS;
+}
+
+int esn_plan_stage_times(esn_plan p, double *sort_s, double *spread_s, double *fft_s, double *correct_s) {
+    if (!p || !p->have_events) return fail(ESN_SIZE_ERROR, "plan was created without opts.timing");
+    ESN_CUDA_TRY(cudaStreamSynchronize(p->st));
+    float ms[4] = {0, 0, 0, 0};
+    if (p->points_set) cudaEventElapsedTime(&ms[0], p->ev[0], p->ev[1]);
+    cudaEventElapsedTime(&ms[1], p->ev[2], p->ev[3]);
+    cudaEventElapsedTime(&ms[2], p->ev[3], p->ev[4]);
+    cudaEventElapsedTime(&ms[3], p->ev[4], p->ev[5]);
+    cudaGetLastError();
+    // stage keys follow transforms.py:83-85; for type 2 the first timed
+    // segment is the amplify ("correct") and the last the interp ("spread").
+    double s = ms[0] * 1e-3, a = ms[1] * 1e-3, b = ms[2] * 1e-3, c = ms[3] * 1e-3;
+    if (sort_s) *sort_s = s;
+    if (p->type == 2) {
+        if (spread_s) *spread_s = c;
+        if (correct_s) *correct_s = a;
+    } else {
+        if (spread_s) *spread_s = a;
+        if (correct_s) *correct_s = c;
+    }
+    if (fft_s) *fft_s = b;
+    return ESN_SUCCESS;
+}
+
+int esn_plan_hot_kernel_seconds(esn_plan p, double *seconds) {
+    if (!p || !p->have_events) return fail(ESN_SIZE_ERROR, "plan was created without opts.timing");
+    ESN_CUDA_TRY(cudaStreamSynchronize(p->st));
+    float ms = 0.f;
+    ESN_CUDA_TRY(cudaEventElapsedTime(&ms, p->ev[6], p->ev[7]));
+    *seconds = ms * 1e-3;
+    return ESN_SUCCESS;
+}
+
+int esn_plan_info(esn_plan p, int64_t *nfine, esn_kernel_params *kp) {
+    if (!p) return fail(ESN_SIZE_ERROR, "null plan");
+    if (nfine)
+        for (int d = 0; d < 3; ++d) nfine[d] = p->n[d];
+    if (kp) *kp = p->kp;
+    return ESN_SUCCESS;
+}
+
+int esn_plan_bins(esn_plan p, int *nbins, int *bin_size, int *bins_per_dim) {
+    if (!p) return fail(ESN_SIZE_ERROR, "null plan");
+    if (nbins) *nbins = p->nbins;
+    for (int d = 0; d < 3; ++d) {
+        if (bin_size) bin_size[d] = p->geom.bs[d];
+        if (bins_per_dim) bins_per_dim[d] = p->geom.nb[d];
+    }
+    return ESN_SUCCESS;
+}
+
+int esn_plan_sort_view(esn_plan p, void *perm, void *keys, void *bin_start) {
+    if (!p || !p->points_set) return fail(ESN_SIZE_ERROR, "plan has no points");
+    if (p->M > 0 && perm)
+        ESN_CUDA_TRY(cudaMemcpyAsync(perm, p->perm, sizeof(int) * p->M, cudaMemcpyDeviceToDevice, p->st));
+    if (p->M > 0 && keys)
+        ESN_CUDA_TRY(cudaMemcpyAsync(keys, p->key, sizeof(int) * p->M, cudaMemcpyDeviceToDevice, p->st));
+    if (bin_start)
+        ESN_CUDA_TRY(cudaMemcpyAsync(bin_start, p->bin_start, sizeof(int) * (p->nbins + 1),
+                                     cudaMemcpyDeviceToDevice, p->st));
+    return ESN_SUCCESS;
+}
+
+int64_t esn_plan_device_bytes(esn_plan p) { return p ? p->device_bytes : 0; }
+
+int esn_fft(int dim, int dtype, int ntransf, const int64_t *nfine, void *data, int sign, void *stream) {
+    if (dim < 1 || dim > 3) return fail(ESN_SIZE_ERROR, "dimension must be 1, 2, or 3");
+    int n[3] = {1, 1, 1};
+    for (int d = 0; d < dim; ++d) {
+        if (nfine[d] < 1 || nfine[d] > INT_MAX) return fail(ESN_SIZE_ERROR, "invalid transform shape");
+        n[d] = (int)nfine[d];
+    }
+    return run_fft(dim, n, dtype == ESN_F32 ? ESN_F32 : ESN_F64, ntransf < 1 ? 1 : ntransf, data, sign,
+                   (cudaStream_t)stream);
+}
+
+// ---------------------------------------------------------------------------
+// Host-buffer one-shot routines (esnufftpy analog).  A small cache keeps the
+// plan and device staging buffers for repeated calls of the same shape.
+namespace {
+struct HostSlot {
+    int type, dim, isign, ntransf, dtype;
+    int64_t N[3];
+    double tol, sigma;
+    int method;
+    esn_plan plan = nullptr;
+    void *dx[3] = {nullptr, nullptr, nullptr};
+    void *dc = nullptr, *df = nullptr;
+    int64_t Mcap = 0;
+    cudaStream_t st = nullptr;
+};
+std::mutex g_host_mu;
+std::vector<HostSlot> g_slots;
+}  // namespace
+
+int esn_nufft_host(int type, int dim, int64_t M, const double *x, const double *y, const double *z, int ntransf,
+                   void *c, int isign, double tol, const int64_t *nmodes, void *f, const esn_opts *opts) {
+    // argument misuse -> SIZE_ERROR before any core work (esnufftpy __init__.py:54-122)
+    if (type != 1 && type != 2) return fail(ESN_SIZE_ERROR, "type must be 1 or 2");
+    if (dim < 1 || dim > 3) return fail(ESN_SIZE_ERROR, "dimension must be 1, 2, or 3");
+    if (M < 0) return fail(ESN_SIZE_ERROR, "negative point count");
+    if (isign != 1 && isign != -1) return fail(ESN_SIZE_ERROR, "isign must be +1 or -1");
+    if (ntransf < 1) return fail(ESN_SIZE_ERROR, "ntransf must be >= 1");
+    if (!nmodes || !c || !f) return fail(ESN_SIZE_ERROR, "null array argument");
+    const double *xs[3] = {x, y, z};
+    for (int d = 0; d < dim; ++d)
+        if (M > 0 && !xs[d]) return fail(ESN_SIZE_ERROR, "coordinate array %d missing", d + 1);
+    esn_opts o;
+    if (opts) o = *opts; else esn_default_opts(&o);
+    const int dtype = o.dtype == ESN_F32 ? ESN_F32 : ESN_F64;
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    HostSlot *slot = nullptr;
+    for (auto &s : g_slots) {
+        bool same = s.type == type && s.dim == dim && s.isign == isign && s.ntransf == ntransf && s.dtype == dtype &&
+                    s.tol == tol && s.sigma == o.sigma && s.method == o.method;
+        for (int d = 0; d < dim && same; ++d) same = s.N[d] == nmodes[d];
+        if (same && !o.params && !o.coeffs && !o.check_bounds && !o.use_exact_kernel && !o.stream) {
+            slot = &s;
+            break;
+        }
+    }
+    bool transient = false;
+    HostSlot tmp{};
+    if (!slot) {
+        tmp.type = type; tmp.dim = dim; tmp.isign = isign; tmp.ntransf = ntransf; tmp.dtype = dtype;
+        tmp.tol = tol; tmp.sigma = o.sigma; tmp.method = o.method;
+        for (int d = 0; d < 3; ++d) tmp.N[d] = d < dim ? nmodes[d] : 1;
+        if (!o.stream) {
+            ESN_CUDA_TRY(cudaStreamCreateWithFlags(&tmp.st, cudaStreamNonBlocking));
+            o.stream = tmp.st;
+        }
+        int rc = esn_plan_create(type, dim, nmodes, isign, ntransf, tol, &o, &tmp.plan);
+        if (rc) {
+            if (tmp.st) cudaStreamDestroy(tmp.st);
+            return rc;
+        }
+        bool cacheable = !o.params && !o.coeffs && !o.check_bounds && !o.use_exact_kernel && tmp.st;
+        if (cacheable) {
+            if (g_slots.size() >= 8) {
+                HostSlot &old = g_slots.front();
+                esn_plan_destroy(old.plan);
+                for (int d = 0; d < 3; ++d) dfree(old.dx[d]);
+                dfree(old.dc);
+                dfree(old.df);
+                if (old.st) cudaStreamDestroy(old.st);
+                g_slots.erase(g_slots.begin());
+            }
+            g_slots.push_back(tmp);
+            slot = &g_slots.back();
+        } else {
+            transient = true;
+            slot = &tmp;
+        }
+    }
+    esn_plan p = slot->plan;
+    cudaStream_t st = p->st;
+    const size_t cb = real_size(dtype) * 2;
+    int64_t nm = 1;
+    for (int d = 0; d < dim; ++d) nm *= nmodes[d];
+    int rc = ESN_SUCCESS;
+    if (M > slot->Mcap || !slot->dc) {
+        for (int d = 0; d < 3; ++d) { dfree(slot->dx[d]); slot->dx[d] = nullptr; }
+        dfree(slot->dc);
+        slot->dc = nullptr;
+        for (int d = 0; d < dim && !rc; ++d) rc = dmalloc(p, &slot->dx[d], sizeof(double) * M);
+        if (!rc) rc = dmalloc(p, &slot->dc, cb * M * ntransf);
+        slot->Mcap = M;
+    }
+    if (!rc && !slot->df) rc = dmalloc(p, &slot->df, cb * nm * ntransf);
+    if (!rc) {
+        for (int d = 0; d < dim && M > 0; ++d)
+            if (cudaMemcpyAsync(slot->dx[d], xs[d], sizeof(double) * M, cudaMemcpyHostToDevice, st) != cudaSuccess)
+                rc = fail(ESN_INTERNAL_ERROR, "H2D copy failed");
+        if (!rc && type == 1 && M > 0)
+            if (cudaMemcpyAsync(slot->dc, c, cb * M * ntransf, cudaMemcpyHostToDevice, st) != cudaSuccess)
+                rc = fail(ESN_INTERNAL_ERROR, "H2D copy failed");
+        if (!rc && type == 2)
+            if (cudaMemcpyAsync(slot->df, f, cb * nm * ntransf, cudaMemcpyHostToDevice, st) != cudaSuccess)
+                rc = fail(ESN_INTERNAL_ERROR, "H2D copy failed");
+    }
+    if (!rc) rc = esn_plan_setpts(p, M, ESN_F64, slot->dx[0], slot->dx[1], slot->dx[2]);
+    if (!rc) rc = esn_plan_execute(p, slot->dc, slot->df);
+    if (!rc) {
+        if (type == 1) {
+            if (cudaMemcpyAsync(f, slot->df, cb * nm * ntransf, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+                rc = fail(ESN_INTERNAL_ERROR, "D2H copy failed");
+        } else if (M > 0) {
+            if (cudaMemcpyAsync(c, slot->dc, cb * M * ntransf, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+                rc = fail(ESN_INTERNAL_ERROR, "D2H copy failed");
+        }
+    }
+    if (!rc) rc = esn_plan_check(p, nullptr);
+    if (transient) {
+        esn_plan_destroy(slot->plan);
+        for (int d = 0; d < 3; ++d) dfree(slot->dx[d]);
+        dfree(slot->dc);
+        dfree(slot->df);
+        if (slot->st) cudaStreamDestroy(slot->st);
+    }
+    return rc;
+}
+
+int esn_nufft1d1(int64_t M, const double *x, const void *c, int isign, double tol, int64_t N1, void *f,
+                 const esn_opts *opts) {
+    int64_t nm[1] = {N1};
+    return esn_nufft_host(1, 1, M, x, nullptr, nullptr, 1, (void *)c, isign, tol, nm, f, opts);
+}
+int esn_nufft2d1(int64_t M, const double *x, const double *y, const void *c, int isign, double tol, int64_t N1,
+                 int64_t N2, void *f, const esn_opts *opts) {
+    int64_t nm[2] = {N1, N2};
+    return esn_nufft_host(1, 2, M, x, y, nullptr, 1, (void *)c, isign, tol, nm, f, opts);
+}
+int esn_nufft3d1(int64_t M, const double *x, const double *y, const double *z, const void *c, int isign, double tol,
+                 int64_t N1, int64_t N2, int64_t N3, void *f, const esn_opts *opts) {
+    int64_t nm[3] = {N1, N2, N3};
+    return esn_nufft_host(1, 3, M, x, y, z, 1, (void *)c, isign, tol, nm, f, opts);
+}
+int esn_nufft1d2(int64_t M, const double *x, void *c, int isign, double tol, int64_t N1, const void *f,
+                 const esn_opts *opts) {
+    int64_t nm[1] = {N1};
+    return esn_nufft_host(2, 1, M, x, nullptr, nullptr, 1, c, isign, tol, nm, (void *)f, opts);
+}
+int esn_nufft2d2(int64_t M, const double *x, const double *y, void *c, int isign, double tol, int64_t N1, int64_t N2,
+                 const void *f, const esn_opts *opts) {
+    int64_t nm[2] = {N1, N2};
+    return esn_nufft_host(2, 2, M, x, y, nullptr, 1, c, isign, tol, nm, (void *)f, opts);
+}
+int esn_nufft3d2(int64_t M, const double *x, const double *y, const double *z, void *c, int isign, double tol,
+                 int64_t N1, int64_t N2, int64_t N3, const void *f, const esn_opts *opts) {
+    int64_t nm[3] = {N1, N2, N3};
+    return esn_nufft_host(2, 3, M, x, y, z, 1, c, isign, tol, nm, (void *)f, opts);
+}
+
+}  // extern "C"

@@ -1,0 +1,161 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's
+golden vectors and the CPU oracle on identical seeded inputs.
+
+Tolerances are written in each test:
+  * spread / interp with the reference's own Horner table: <= 1e-13 x
+    max|value| (float64; only the accumulation order and FMA contraction
+    differ);
+  * full transforms (product fits its own table, |dcoef| ~ 1e-15):
+    rel l2 <= 1e-3 x tol vs the reference output, and the north_star bar
+    rel l2 <= 10 x tol everywhere;
+  * fold / box keys: bit-exact.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import cases
+from make_golden import SPREAD_CASES, XFORM_CASES
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a = np.asarray(a).reshape(-1)
+    b = np.asarray(b).reshape(-1)
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.mark.parametrize("method", ["tile", "global"])
+def test_spread_matches_reference(esn, golden, method):
+    from paper_1808_06736_b200 import spreadinterp as SI
+    gk = golden("kernel")
+    gs = golden("spread")
+    for i, (dim, sizes, m, w, exact, seed) in enumerate(SPREAD_CASES):
+        r = np.random.default_rng(seed)
+        coords = [r.uniform(-np.pi, np.pi, m) for _ in range(dim)]
+        c = r.standard_normal(m) + 1j * r.standard_normal(m)
+        p = esn.params_for_width(w)
+        pts = SI.build_point_set(coords, sizes)
+        grid = SI.spread(pts, c, p, use_exact=exact, method=method, coeffs=gk[f"poly_{w}"])
+        ref = gs[f"sp_grid_{i}"]
+        err = np.abs(grid - ref).max() / np.abs(ref).max()
+        assert err <= 1e-13, (i, method, err)
+
+
+def test_interp_matches_reference(esn, golden):
+    from paper_1808_06736_b200 import spreadinterp as SI
+    gk = golden("kernel")
+    gs = golden("spread")
+    for i, (dim, sizes, m, w, exact, seed) in enumerate(SPREAD_CASES):
+        r = np.random.default_rng(seed)
+        coords = [r.uniform(-np.pi, np.pi, m) for _ in range(dim)]
+        r.standard_normal(m), r.standard_normal(m)
+        shape = tuple(reversed(sizes))
+        b = r.standard_normal(shape) + 1j * r.standard_normal(shape)
+        p = esn.params_for_width(w)
+        pts = SI.build_point_set(coords, sizes)
+        out = SI.interp(pts, b, p, use_exact=exact, coeffs=gk[f"poly_{w}"])
+        ref = gs[f"sp_interp_{i}"]
+        err = np.abs(out - ref).max() / np.abs(ref).max()
+        assert err <= 1e-13, (i, err)
+
+
+def test_fold_bit_exact(esn, golden):
+    from paper_1808_06736_b200 import grid as G
+    gg = golden("grid")
+    xs = gg["fold_x"]
+    for n in (20, 256, 2000, 20000, 1):
+        g = G.fold_coords(xs, n=n)
+        np.testing.assert_array_equal(g, gg[f"g_{n}"])
+
+
+def test_bin_sort_boxes_bit_exact(esn, golden):
+    from paper_1808_06736_b200 import grid as G
+    gg = golden("grid")
+    specs = [((64,), 1000, 1), ((100,), 5000, 2), ((128, 64), 20000, 3), ((50, 37), 3000, 4),
+             ((64, 32, 32), 5000, 5), ((30, 22, 17), 4000, 6), ((64,), 100, 7)]
+    for i, (sizes, m, seed) in enumerate(specs):
+        r = np.random.default_rng(seed)
+        coords = tuple(r.uniform(0, s, m) for s in sizes)
+        if i == 6:
+            coords = (np.full(m, 2.5),)
+        res = G.bin_sort(coords, sizes)
+        np.testing.assert_array_equal(res.boxes, gg[f"bs_boxes_{i}"])
+        np.testing.assert_array_equal(np.sort(res.perm), np.arange(m))
+        assert np.all(np.diff(res.boxes[res.perm]) >= 0)
+        # same bin membership as the reference's stable sort
+        ref = gg[f"bs_perm_{i}"]
+        kb = res.boxes[res.perm]
+        for b in np.unique(kb)[:200]:
+            np.testing.assert_array_equal(np.sort(res.perm[kb == b]), np.sort(ref[gg[f"bs_boxes_{i}"][ref] == b]))
+
+
+@pytest.mark.parametrize("i", range(len(XFORM_CASES)))
+def test_transforms_match_reference(esn, golden, i):
+    tt, dim, nm, m, tol, isign, sigma, exact, seed = XFORM_CASES[i]
+    gt = golden("transforms")
+    r = np.random.default_rng(seed)
+    coords = [r.uniform(-np.pi, np.pi, m) for _ in range(dim)]
+    opts = esn.TransformOptions(tolerance=tol, isign=isign, sigma=sigma, use_exact_kernel=exact)
+    if tt == 1:
+        c = r.standard_normal(m) + 1j * r.standard_normal(m)
+        out, t = esn.exec_type1(coords, c, nm, opts)
+    elif tt == 2:
+        shape = tuple(reversed(nm))
+        f = r.standard_normal(shape) + 1j * r.standard_normal(shape)
+        out, t = esn.exec_type2(coords, f, opts)
+    else:
+        c = r.standard_normal(m) + 1j * r.standard_normal(m)
+        targets = [r.uniform(-30, 30, 180) for _ in range(dim)]
+        out, t = esn.exec_type3(coords, c, targets, opts)
+    ref = gt[f"x_{i}"]
+    assert out.shape == ref.shape
+    e = rel(out, ref)
+    assert e <= max(1e-3 * tol, 1e-13), (i, e)
+    assert set(t) == {"sort", "spread", "fft", "correct"}
+
+
+def test_edge_cases(esn, golden):
+    gt = golden("transforms")
+    o = esn.TransformOptions(tolerance=1e-6)
+    out, _ = esn.exec_type1((np.zeros(0), np.zeros(0)), np.zeros(0, complex), (6, 4), o)
+    np.testing.assert_array_equal(out, gt["empty_t1"])
+    out, _ = esn.exec_type2((np.zeros(0),), np.ones(8, complex), o)
+    assert out.shape == (0,)
+    out, _ = esn.exec_type1((np.array([0.0]),), np.array([1.0 + 0j]), (8,),
+                            esn.TransformOptions(tolerance=1e-9))
+    assert rel(out, gt["origin_t1"]) <= 1e-12
+    np.testing.assert_allclose(out, np.ones(8), atol=1e-9)
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c3f", "c4", "c5"])
+def test_north_star_configs_golden(esn, golden, name):
+    """BASELINE configs at golden M vs the reference (run with all cores):
+    rel l2 <= 10 eps (north_star) and much tighter for float64."""
+    g = golden("northstar")
+    cfg = cases.CONFIGS[name]
+    T = cfg.get("ntransf_golden", 1)
+    coords, data, cfg = cases.make_inputs(name, M=cfg["M_golden"], ntransf=T)
+    opts = esn.TransformOptions(tolerance=cfg["tol"], isign=cfg["isign"], dtype=cfg["dtype"])
+    if cfg["dtype"] == "float32":
+        coords = [x.astype(np.float32) for x in coords]
+        data = data.astype(np.complex64)
+    if cfg["ttype"] == 1:
+        out, _ = esn.exec_type1(coords, data, cfg["nm"], opts)
+    else:
+        out, _ = esn.exec_type2(coords, data, opts)
+    out = np.asarray(out).reshape(T, -1)
+    if f"{name}_full" in g.files:
+        ref = g[f"{name}_full"].reshape(T, -1)
+        got = out
+    else:
+        idx = g[f"{name}_idx"]
+        ref = g[f"{name}_sample"]
+        got = out[:, idx]
+        np.testing.assert_allclose(np.linalg.norm(out, axis=1), g[f"{name}_norm"],
+                                   rtol=10 * cfg["tol"])
+    e = rel(got, ref)
+    bound = 10 * cfg["tol"] if cfg["dtype"] == "float32" else 1e-3 * cfg["tol"]
+    assert e <= bound, (name, e, bound)
