@@ -32,36 +32,8 @@ from esnufft import spreadinterp as rsi  # noqa: E402
 from esnufft.transforms import (TransformOptions, exec_type1, exec_type2,  # noqa: E402
                                 exec_type3)
 
-TOLS = [1e-1, 9e-2, 3e-2, 1e-2, 1e-3, 2e-4, 1e-4, 1e-5, 1e-6, 1e-7, 1e-8,
-        1e-9, 1e-10, 1e-11, 1e-12, 1e-13, 1e-14, 1e-15]
-FSERIES_CASES = [  # (w, sigma, n, N)
-    (7, 2.0, 20000, 10000), (6, 2.0, 2000, 1000), (7, 2.0, 256, 128),
-    (5, 2.0, 256, 128), (10, 2.0, 256, 128), (5, 2.0, 1024, 512),
-    (2, 2.0, 4, 1), (16, 2.0, 64, 31), (13, 2.0, 3000, 1499), (11, 1.25, 160, 128),
-    (3, 2.0, 6, 3), (8, 2.0, 2500, 2500),
-]
-SPREAD_CASES = [  # (dim, sizes, M, w, use_exact, seed)
-    (1, (48,), 200, 7, False, 1), (1, (600,), 3000, 7, True, 2),
-    (1, (20,), 50, 16, False, 3), (1, (8,), 40, 2, False, 4),
-    (2, (24, 20), 200, 7, False, 5), (2, (80, 64), 5000, 6, False, 6),
-    (2, (36, 30), 700, 13, True, 7), (2, (40, 50), 1500, 5, False, 8),
-    (3, (12, 16, 10), 200, 7, False, 9), (3, (32, 24, 20), 4000, 5, False, 10),
-    (3, (24, 24, 24), 3000, 10, False, 11), (3, (20, 18, 22), 500, 3, True, 12),
-    (3, (40, 40, 40), 25_000, 7, False, 13),
-]
-XFORM_CASES = [  # (ttype, dim, nm, M, tol, isign, sigma, exact, seed)
-    (1, 1, (50,), 300, 1e-9, 1, 2.0, False, 21), (1, 1, (64,), 500, 1e-6, -1, 2.0, False, 22),
-    (1, 2, (14, 10), 300, 1e-9, 1, 2.0, False, 23), (1, 2, (32, 24), 1000, 1e-5, -1, 2.0, False, 24),
-    (1, 3, (8, 6, 7), 300, 1e-9, -1, 2.0, False, 25), (1, 3, (16, 16, 16), 2000, 1e-4, 1, 2.0, False, 26),
-    (1, 2, (18, 12), 250, 1e-7, 1, 1.25, False, 27), (1, 2, (20, 16), 300, 1e-8, 1, 2.0, True, 28),
-    (1, 1, (1,), 30, 1e-3, 1, 2.0, False, 29), (1, 3, (9, 5, 4), 150, 1e-12, 1, 2.0, False, 30),
-    (2, 1, (40,), 200, 1e-9, 1, 2.0, False, 31), (2, 1, (129,), 800, 1e-6, -1, 2.0, False, 32),
-    (2, 2, (12, 9), 200, 1e-9, -1, 2.0, False, 33), (2, 2, (50, 40), 3000, 1e-5, 1, 2.0, False, 34),
-    (2, 3, (6, 5, 8), 200, 1e-9, 1, 2.0, False, 35), (2, 3, (16, 12, 10), 1500, 1e-3, -1, 2.0, False, 36),
-    (2, 2, (17, 11), 300, 1e-7, -1, 1.25, False, 37), (2, 3, (7, 7, 7), 100, 1e-14, 1, 2.0, False, 38),
-    (3, 1, None, 250, 1e-9, 1, 2.0, False, 41), (3, 2, None, 250, 1e-9, -1, 2.0, False, 42),
-    (3, 3, None, 250, 1e-6, 1, 2.0, False, 43), (3, 1, None, 400, 1e-4, -1, 2.0, False, 44),
-]
+from cases import FSERIES_CASES, SPREAD_CASES, TOLS, XFORM_CASES  # noqa: E402
+
 SAMPLE = 4096
 
 

@@ -16,7 +16,7 @@ import pytest
 import torch
 
 import cases
-from make_golden import SPREAD_CASES, XFORM_CASES
+from cases import SPREAD_CASES, XFORM_CASES
 
 pytestmark = pytest.mark.gpu
 
