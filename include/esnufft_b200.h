@@ -55,7 +55,7 @@ enum { ESN_COORD_GRID_UNITS = 0x10 };
 enum {
     ESN_METHOD_AUTO = 0,
     ESN_METHOD_GLOBAL = 1, /* point-parallel, direct global atomics        */
-    ESN_METHOD_TILE = 2    /* per-bin shared-memory tile + halo flush      */
+    ESN_METHOD_TILE = 2    /* per-bin register-resident row tiles + halo flush */
 };
 
 /* Library version (major*10000 + minor*100 + patch). */

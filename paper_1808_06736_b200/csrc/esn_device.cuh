@@ -2,13 +2,15 @@
 // kernel-row evaluation, spreaders, interpolator, deconvolution and mode
 // amplification.  Instantiated per precision by esn_inst_f64.cu / _f32.cu.
 //
-// Data layout in HBM (see DESIGN.md):
-//  * sorted grid coordinates gs[d][k] (plan dtype) and perm[k] (int32,
-//    sorted slot -> original index), produced by esn_setpts.cu;
+// Data layout in HBM (DESIGN.md section 3):
+//  * sorted point records rec[k] = {g_1, g_2, g_3, j} (grid coordinates in
+//    the plan dtype + original index), 32 B for float64 plans and 16 B for
+//    float32 plans -- one aligned sector-sized record per point, written once
+//    by setpts and read coalesced by the spreader / interpolator;
 //  * strengths c (ntransf, M) and fine grids (ntransf, n3, n2, n1) as
-//    interleaved complex of the plan dtype;
+//    interleaved complex of the plan dtype (C order, dimension 1 fastest);
 //  * bins are boxes of footprint origins i0 = floor(g - w/2 + 1) (wrapped
-//    into [0, n)), so a bin of bs cells owns a tile of bs + w - 1 cells.
+//    into [0, n)); a bin of bs cells owns a tile of bs + w - 1 cells.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -34,11 +36,13 @@ struct Cx<float> {
 // exp/sqrt.  The Horner table lives in the kernel parameter bank; with W a
 // compile-time constant every coefficient is a uniform constant operand.
 template <typename T, int W>
-__device__ __forceinline__ int kernel_row(T g, const KernelTab<T> &k, T *row) {
-    int i0 = (int)floor(g - (T)(0.5 * W) + (T)1);
+__device__ __forceinline__ int kernel_row(double g, const KernelTab<T> &k, T *row) {
+    // footprint origin and local coordinate in float64 exactly as the
+    // reference (spreadinterp.py:318, 329), then the plan dtype
+    const int i0 = (int)floor(g - 0.5 * W + 1.0);
     if (k.use_exact) {
         const T step = (T)2 / (T)W;
-        T z = step * ((T)i0 - g);
+        T z = (T)((2.0 / W) * ((double)i0 - g));
 #pragma unroll
         for (int m = 0; m < W; ++m) {
             T a = (T)1 - z * z;
@@ -47,7 +51,7 @@ __device__ __forceinline__ int kernel_row(T g, const KernelTab<T> &k, T *row) {
             z += step;
         }
     } else {
-        const T t = (T)2 * ((T)i0 - g) + (T)(W - 1);
+        const T t = (T)(2.0 * ((double)i0 - g) + (double)(W - 1));
 #pragma unroll
         for (int m = 0; m < W; ++m) {
             T v = k.coef[m * (W + 4)];
@@ -57,6 +61,39 @@ __device__ __forceinline__ int kernel_row(T g, const KernelTab<T> &k, T *row) {
         }
     }
     return i0;
+}
+
+// Lane-parallel row evaluation: a lane that always evaluates ordinate m
+// (runtime) keeps piece m's Horner coefficients in registers (loaded once per
+// kernel by kernel_col), then evaluates one ordinate per coordinate.
+template <typename T, int W>
+__device__ __forceinline__ void kernel_col(const KernelTab<T> &k, int m, T *cf) {
+#pragma unroll
+    for (int q = 0; q < W + 4; ++q) cf[q] = (T)0;
+#pragma unroll
+    for (int p = 0; p < W; ++p) {
+        if (p == m) {
+#pragma unroll
+            for (int q = 0; q < W + 4; ++q) cf[q] = k.coef[p * (W + 4) + q];
+        }
+    }
+}
+
+template <typename T, int W>
+__device__ __forceinline__ T kernel_one(double g, int m, const T *cf, const KernelTab<T> &k, int *i0out) {
+    const int i0 = (int)floor(g - 0.5 * W + 1.0);
+    *i0out = i0;
+    if (k.use_exact) {
+        const T z = (T)((2.0 / W) * ((double)(i0 + m) - g));
+        T a = (T)1 - z * z;
+        a = a < (T)0 ? (T)0 : a;
+        return exp(k.beta * (sqrt(a) - (T)1));
+    }
+    const T t = (T)(2.0 * ((double)i0 - g) + (double)(W - 1));
+    T v = cf[0];
+#pragma unroll
+    for (int q = 1; q < W + 4; ++q) v = fma(v, t, cf[q]);
+    return v;
 }
 
 __device__ __forceinline__ int wrap_once(int i, int n) {
@@ -80,28 +117,45 @@ __device__ __forceinline__ bool finite2(typename Cx<T>::type v) {
     return isfinite(v.x) && isfinite(v.y);
 }
 
+// One 256-bit read-only load per record (LDG.E.ENL2.256).
+__device__ __forceinline__ Rec load_rec(const Rec *r, int64_t k) {
+    unsigned long long a, b, c, d;
+    asm volatile("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(a), "=l"(b), "=l"(c), "=l"(d)
+                 : "l"(r + k));
+    Rec out;
+    out.g[0] = __longlong_as_double((long long)a);
+    out.g[1] = __longlong_as_double((long long)b);
+    out.g[2] = __longlong_as_double((long long)c);
+    out.j = (int)(d & 0xffffffffull);
+    out.pad = 0;
+    return out;
+}
+
 // ---------------------------------------------------------------------------
 // Global-atomic spreader: one thread per sorted point, w^d complex REDs
-// straight into the fine grid (rows reused across the ntransf batch).
+// straight into the fine grid (rows reused across the ntransf batch).  Used
+// for 1D (where a point's footprint is a single contiguous run).
 template <typename T, int DIM, int W>
 __global__ void __launch_bounds__(256) k_spread_global(SpreadArgs<T> a) {
     using C = typename Cx<T>::type;
     const int n1 = a.g.n[0], n2 = a.g.n[1], n3 = a.g.n[2];
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < a.M;
          k += (int64_t)gridDim.x * blockDim.x) {
-        const int j = a.perm[k];
+        const Rec rc = load_rec(a.rec, k);
+        const int j = rc.j;
         T r1[W], r2[W], r3[W];
         int ix1[W], ix2[W], ix3[W];
-        int i1 = kernel_row<T, W>(a.gs[0][k], a.k, r1);
+        int i1 = kernel_row<T, W>(rc.g[0], a.k, r1);
 #pragma unroll
         for (int m = 0; m < W; ++m) ix1[m] = wrap_once(i1 + m, n1);
         if (DIM > 1) {
-            int i2 = kernel_row<T, W>(a.gs[1][k], a.k, r2);
+            int i2 = kernel_row<T, W>(rc.g[1], a.k, r2);
 #pragma unroll
             for (int m = 0; m < W; ++m) ix2[m] = wrap_once(i2 + m, n2);
         }
         if (DIM > 2) {
-            int i3 = kernel_row<T, W>(a.gs[2][k], a.k, r3);
+            int i3 = kernel_row<T, W>(rc.g[2], a.k, r3);
 #pragma unroll
             for (int m = 0; m < W; ++m) ix3[m] = wrap_once(i3 + m, n3);
         }
@@ -124,10 +178,11 @@ __global__ void __launch_bounds__(256) k_spread_global(SpreadArgs<T> a) {
 #pragma unroll 1
                 for (int m3 = 0; m3 < W; ++m3) {
                     C v3{c.x * r3[m3], c.y * r3[m3]};
+                    const int iz = wrap_once(ix3[0] + m3, n3);
 #pragma unroll
                     for (int m2 = 0; m2 < W; ++m2) {
                         C v{v3.x * r2[m2], v3.y * r2[m2]};
-                        int64_t base = ((int64_t)ix3[m3] * n2 + ix2[m2]) * n1;
+                        int64_t base = ((int64_t)iz * n2 + ix2[m2]) * n1;
 #pragma unroll
                         for (int m1 = 0; m1 < W; ++m1)
                             red_add(grid + base + ix1[m1], C{v.x * r1[m1], v.y * r1[m1]});
@@ -139,34 +194,105 @@ __global__ void __launch_bounds__(256) k_spread_global(SpreadArgs<T> a) {
 }
 
 // ---------------------------------------------------------------------------
-// Tile spreader (one CTA per subproblem, persistent over a work queue): the
-// bin's tile of (bs + w - 1)^d cells is accumulated in shared memory, then
-// flushed to the periodic fine grid with one RED per tile cell.  Points are
-// staged in chunks: phase A evaluates kernel rows (one thread per point),
-// phase B lets each warp add one point at a time with lanes covering the
-// w^d footprint cells (distinct cells per lane).
+// Row spreader (2D / 3D).  One CTA per subproblem (persistent over a work
+// queue).  Every thread OWNS one x-row of the bin's tile (rows indexed by
+// (y, z) in the tile) and accumulates it in registers: acc[X] with
+// X = BX + W - 1.  For each staged point the warps whose row block meets the
+// point's w x w row footprint add c * r2[dy] * r3[dz] * r1[m] into
+// acc[ox + m]; the x offset ox is warp-uniform, so a switch over its BX values
+// gives static register indices.  No shared-memory atomics: the only atomics
+// are the final coalesced REDs of the tile (staged through shared memory)
+// into the periodic fine grid.
+//
+// Thread layout: 3D -- warps are 8 (y) x 4 (z) row blocks over a RY x RZ
+// row grid; 2D -- warps are 32 consecutive y rows.
 template <typename T, int DIM, int W>
-struct TileCfg {
-    static constexpr int CH = 64;  // points per staging chunk
-    static constexpr int NT = 256;
-};
+__device__ __forceinline__ void rows_accumulate(typename Cx<T>::type *acc, int ox,
+                                                typename Cx<T>::type v, const T *r1) {
+    constexpr int BX = RowsCfg<T, DIM, W>::BX;
+#define ESN_ROWS_CASE(OX)                                      \
+    case OX: {                                                 \
+        _Pragma("unroll") for (int m = 0; m < W; ++m) {        \
+            const T r = r1[m];                                 \
+            acc[OX + m].x = fma(v.x, r, acc[OX + m].x);        \
+            acc[OX + m].y = fma(v.y, r, acc[OX + m].y);        \
+        }                                                      \
+    } break;
+    switch (ox) {
+        ESN_ROWS_CASE(0)
+        ESN_ROWS_CASE(1)
+        ESN_ROWS_CASE(2)
+        ESN_ROWS_CASE(3)
+        ESN_ROWS_CASE(4)
+        ESN_ROWS_CASE(5)
+        ESN_ROWS_CASE(6)
+        ESN_ROWS_CASE(7)
+        default:
+            if constexpr (BX > 8) {
+                switch (ox) {
+                    ESN_ROWS_CASE(8)
+                    ESN_ROWS_CASE(9)
+                    ESN_ROWS_CASE(10)
+                    ESN_ROWS_CASE(11)
+                    ESN_ROWS_CASE(12)
+                    ESN_ROWS_CASE(13)
+                    ESN_ROWS_CASE(14)
+                    ESN_ROWS_CASE(15)
+                    default:
+                        if constexpr (BX > 16) {
+                            switch (ox) {
+                                ESN_ROWS_CASE(16)
+                                ESN_ROWS_CASE(17)
+                                ESN_ROWS_CASE(18)
+                                ESN_ROWS_CASE(19)
+                                ESN_ROWS_CASE(20)
+                                ESN_ROWS_CASE(21)
+                                ESN_ROWS_CASE(22)
+                                ESN_ROWS_CASE(23)
+                                ESN_ROWS_CASE(24)
+                                ESN_ROWS_CASE(25)
+                                ESN_ROWS_CASE(26)
+                                ESN_ROWS_CASE(27)
+                                ESN_ROWS_CASE(28)
+                                ESN_ROWS_CASE(29)
+                                ESN_ROWS_CASE(30)
+                                ESN_ROWS_CASE(31)
+                                default:
+                                    break;
+                            }
+                        }
+                        break;
+                }
+            }
+            break;
+    }
+#undef ESN_ROWS_CASE
+}
 
 template <typename T, int DIM, int W>
-__global__ void __launch_bounds__(256) k_spread_tile(SpreadArgs<T> a) {
+__global__ void __launch_bounds__(RowsCfg<T, DIM, W>::NT, RowsCfg<T, DIM, W>::MINB) k_spread_rows(SpreadArgs<T> a) {
     using C = typename Cx<T>::type;
-    constexpr int CH = TileCfg<T, DIM, W>::CH;
-    constexpr int FP = (DIM == 1 ? W : (DIM == 2 ? W * W : W * W * W));
+    using Cfg = RowsCfg<T, DIM, W>;
+    constexpr int X = Cfg::X, RY = Cfg::RY, RZ = Cfg::RZ, CH = Cfg::CH, NT = Cfg::NT;
+    constexpr int NW = NT / 32;                 // warps = row blocks
+    constexpr int WBY = DIM == 3 ? 8 : 32;      // row-block extent in y
+    constexpr int WBZ = DIM == 3 ? 4 : 1;       // row-block extent in z
+    constexpr int NWY = RY / WBY;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int T1 = a.g.bs[0] + W - 1;
-    const int T2 = DIM > 1 ? a.g.bs[1] + W - 1 : 1;
-    const int T3 = DIM > 2 ? a.g.bs[2] + W - 1 : 1;
-    const int ncell = T1 * T2 * T3;
-    C *tile = reinterpret_cast<C *>(smem_raw);
-    T *rows = reinterpret_cast<T *>(tile + ncell);            // CH x DIM x W
-    C *cs = reinterpret_cast<C *>(rows + CH * DIM * W);        // CH
-    int *offs = reinterpret_cast<int *>(cs + CH);              // CH x DIM
+    // staging: per point c, r1[W], r2[W], r3[W], offsets (ox, oy, oz); per
+    // warp the list of staged points whose row footprint meets its block
+    C *s_c = reinterpret_cast<C *>(smem_raw);
+    T *s_r = reinterpret_cast<T *>(s_c + CH);                 // CH x 3 x W
+    int *s_o = reinterpret_cast<int *>(s_r + CH * 3 * W);     // CH x 4
+    unsigned char *s_list = reinterpret_cast<unsigned char *>(s_o + CH * 4);  // NW x CH
+    C *s_tile = reinterpret_cast<C *>(smem_raw);              // reused for the flush: RY*RZ x X
     __shared__ int s_sub;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+    __shared__ int s_cnt[NW];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wy = warp % NWY, wz = warp / NWY;
+    const int ry = wy * WBY + (DIM == 3 ? (lane & 7) : lane);
+    const int rz = DIM == 3 ? wz * WBZ + (lane >> 3) : 0;
     const int n1 = a.g.n[0], n2 = a.g.n[1], n3 = a.g.n[2];
     const int nsub = *a.nsub;
     for (;;) {
@@ -178,159 +304,267 @@ __global__ void __launch_bounds__(256) k_spread_tile(SpreadArgs<T> a) {
         const int4 sp = a.subprob[s];
         const int bin = sp.x, start = sp.y, cnt = sp.z;
         const int b1 = bin % a.g.nb[0];
-        const int b2 = DIM > 1 ? (bin / a.g.nb[0]) % a.g.nb[1] : 0;
+        const int b2 = (bin / a.g.nb[0]) % a.g.nb[1];
         const int b3 = DIM > 2 ? bin / (a.g.nb[0] * a.g.nb[1]) : 0;
         const int lo1 = b1 * a.g.bs[0], lo2 = b2 * a.g.bs[1], lo3 = b3 * a.g.bs[2];
         for (int t = 0; t < a.ntransf; ++t) {
-            for (int i = tid; i < ncell; i += blockDim.x) tile[i] = C{(T)0, (T)0};
+            C acc[X];
+#pragma unroll
+            for (int x = 0; x < X; ++x) acc[x] = C{(T)0, (T)0};
             const C *cin = reinterpret_cast<const C *>(a.c) + (int64_t)t * a.M;
             for (int p0 = 0; p0 < cnt; p0 += CH) {
                 const int nch = min(CH, cnt - p0);
                 __syncthreads();
-                if (tid < nch) {
-                    const int k = start + p0 + tid;
-                    const int j = a.perm[k];
+                if (tid < NW) s_cnt[tid] = 0;
+                __syncthreads();
+                if (tid < nch) {  // phase A: one thread per staged point
+                    const Rec rc = load_rec(a.rec, start + p0 + tid);
                     T r[W];
-                    int i0 = kernel_row<T, W>(a.gs[0][k], a.k, r);
-                    offs[tid * DIM + 0] = (i0 < 0 ? i0 + n1 : i0) - lo1;
+                    int i0 = kernel_row<T, W>(rc.g[0], a.k, r);
+                    const int ox = (i0 < 0 ? i0 + n1 : i0) - lo1;
 #pragma unroll
-                    for (int m = 0; m < W; ++m) rows[(tid * DIM + 0) * W + m] = r[m];
-                    if (DIM > 1) {
-                        i0 = kernel_row<T, W>(a.gs[1][k], a.k, r);
-                        offs[tid * DIM + 1] = (i0 < 0 ? i0 + n2 : i0) - lo2;
+                    for (int m = 0; m < W; ++m) s_r[(tid * 3 + 0) * W + m] = r[m];
+                    i0 = kernel_row<T, W>(rc.g[1], a.k, r);
+                    const int oy = (i0 < 0 ? i0 + n2 : i0) - lo2;
 #pragma unroll
-                        for (int m = 0; m < W; ++m) rows[(tid * DIM + 1) * W + m] = r[m];
-                    }
+                    for (int m = 0; m < W; ++m) s_r[(tid * 3 + 1) * W + m] = r[m];
+                    int oz = 0;
                     if (DIM > 2) {
-                        i0 = kernel_row<T, W>(a.gs[2][k], a.k, r);
-                        offs[tid * DIM + 2] = (i0 < 0 ? i0 + n3 : i0) - lo3;
+                        i0 = kernel_row<T, W>(rc.g[2], a.k, r);
+                        oz = (i0 < 0 ? i0 + n3 : i0) - lo3;
 #pragma unroll
-                        for (int m = 0; m < W; ++m) rows[(tid * DIM + 2) * W + m] = r[m];
+                        for (int m = 0; m < W; ++m) s_r[(tid * 3 + 2) * W + m] = r[m];
                     }
-                    C c = cin[j];
-                    if (!finite2<T>(c)) flag_min(&a.flags[6], (unsigned long long)j);
-                    cs[tid] = c;
+                    *reinterpret_cast<int4 *>(s_o + tid * 4) = make_int4(ox, oy, oz, 0);
+                    C c = cin[rc.j];
+                    if (!finite2<T>(c)) flag_min(&a.flags[6], (unsigned long long)rc.j);
+                    s_c[tid] = c;
+                    // enqueue this point for every row block its w x w rows meet
+                    const int y0 = oy / WBY, y1 = (oy + W - 1) / WBY;
+                    const int z0 = oz / WBZ, z1 = (oz + W - 1) / WBZ;
+                    for (int zz = z0; zz <= z1; ++zz)
+                        for (int yy = y0; yy <= y1; ++yy) {
+                            const int wb = zz * NWY + yy;
+                            const int slot = atomicAdd(&s_cnt[wb], 1);
+                            s_list[wb * CH + slot] = (unsigned char)tid;
+                        }
                 }
                 __syncthreads();
-                for (int q = warp; q < nch; q += nwarp) {
-                    const C c = cs[q];
-                    const T *rq = rows + q * DIM * W;
-                    const int o1 = offs[q * DIM];
-                    const int o2 = DIM > 1 ? offs[q * DIM + 1] : 0;
-                    const int o3 = DIM > 2 ? offs[q * DIM + 2] : 0;
-                    for (int f = lane; f < FP; f += 32) {
-                        const int m1 = f % W;
-                        const int m2 = DIM > 1 ? (f / W) % W : 0;
-                        const int m3 = DIM > 2 ? f / (W * W) : 0;
-                        T v = rq[m1];
-                        if (DIM > 1) v *= rq[W + m2];
-                        if (DIM > 2) v *= rq[2 * W + m3];
-                        T *cell = reinterpret_cast<T *>(tile + ((o3 + m3) * T2 + (o2 + m2)) * T1 + (o1 + m1));
-                        atomicAdd(cell, c.x * v);
-                        atomicAdd(cell + 1, c.y * v);
-                    }
+                // phase B: the row owners of each block accumulate in registers
+                const int nq = s_cnt[warp];
+                for (int i = 0; i < nq; ++i) {
+                    const int q = s_list[warp * CH + i];
+                    const int4 o = *reinterpret_cast<const int4 *>(s_o + q * 4);
+                    const int dy = ry - o.y, dz = rz - o.z;
+                    const bool cov = dy >= 0 && dy < W && (DIM < 3 || (dz >= 0 && dz < W));
+                    const T *rq = s_r + q * 3 * W;
+                    T f = cov ? rq[W + (cov ? dy : 0)] : (T)0;
+                    if (DIM > 2) f *= cov ? rq[2 * W + (cov ? dz : 0)] : (T)0;
+                    const C cq = s_c[q];
+                    const C v{cq.x * f, cq.y * f};
+                    T r1[W];
+#pragma unroll
+                    for (int m = 0; m < W; ++m) r1[m] = rq[m];
+                    rows_accumulate<T, DIM, W>(acc, o.x, v, r1);
                 }
             }
+            // flush: stage the owned rows in shared memory, then coalesced REDs
+            __syncthreads();
+            const int nrow = RY * RZ;
+            const int myrow = rz * RY + ry;
+#pragma unroll
+            for (int x = 0; x < X; ++x) s_tile[myrow * X + x] = acc[x];
             __syncthreads();
             C *grid = reinterpret_cast<C *>(a.grid) + (int64_t)t * a.gstride;
-            for (int i = tid; i < ncell; i += blockDim.x) {
-                const C v = tile[i];
+            for (int i = tid; i < nrow * X; i += NT) {
+                const C v = s_tile[i];
                 if (v.x == (T)0 && v.y == (T)0) continue;
-                const int q1 = i % T1;
-                const int q2 = DIM > 1 ? (i / T1) % T2 : 0;
-                const int q3 = DIM > 2 ? i / (T1 * T2) : 0;
-                int g1 = lo1 + q1;
+                const int row = i / X, x = i - row * X;
+                const int yy = row % RY, zz = row / RY;
+                int g1 = lo1 + x;
                 while (g1 >= n1) g1 -= n1;
-                int64_t gi = g1;
-                if (DIM > 1) {
-                    int g2 = lo2 + q2;
-                    while (g2 >= n2) g2 -= n2;
-                    gi += (int64_t)g2 * n1;
-                }
+                int g2 = lo2 + yy;
+                while (g2 >= n2) g2 -= n2;
+                int64_t gi = (int64_t)g2 * n1 + g1;
                 if (DIM > 2) {
-                    int g3 = lo3 + q3;
+                    int g3 = lo3 + zz;
                     while (g3 >= n3) g3 -= n3;
                     gi += (int64_t)g3 * n2 * n1;
                 }
                 red_add(grid + gi, v);
             }
-            __syncthreads();
         }
     }
 }
 
 // ---------------------------------------------------------------------------
-// Interpolator (spreadinterp.py:442-507): one thread per sorted point,
-// separable weighted gather of the w^d patch (periodic indices), output in
-// ORIGINAL point order (out[perm[k]], spreadinterp.py:453).
-template <typename T, int DIM, int W>
-__global__ void __launch_bounds__(256) k_interp_thread(SpreadArgs<T> a, T *cout, const T *gridp) {
+// Batched 2D spreader (ntransf > 1): lanes are transforms.  A CTA owns one
+// bin tile (rows y of length X in registers) for 32 transforms at a time
+// (one warp per tile row, lane = transform); every staged point is applied by
+// the warps of its w rows with identical kernel values, so there is no lane
+// waste and the point data is a broadcast.
+template <typename T, int W>
+__global__ void __launch_bounds__(Batch2Cfg<T, W>::NT) k_spread_batch2d(SpreadArgs<T> a) {
     using C = typename Cx<T>::type;
+    using Cfg = Batch2Cfg<T, W>;
+    constexpr int X = Cfg::X, RY = Cfg::RY, CH = Cfg::CH;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C *s_c = reinterpret_cast<C *>(smem_raw);                 // CH x 32 strengths (point-major)
+    T *s_r = reinterpret_cast<T *>(s_c + CH * 32);            // CH x 2 x W
+    int *s_o = reinterpret_cast<int *>(s_r + CH * 2 * W);     // CH x 2
+    int *s_j = s_o + CH * 2;                                  // CH
+    __shared__ int s_sub;
+    const int tid = threadIdx.x, lane = tid & 31, row = tid >> 5;
+    const int n1 = a.g.n[0], n2 = a.g.n[1];
+    const int nsub = *a.nsub;
+    const int ngroups = (a.ntransf + 31) / 32;
+    for (;;) {
+        if (tid == 0) s_sub = atomicAdd(a.work, 1);
+        __syncthreads();
+        const int s = s_sub;
+        __syncthreads();
+        if (s >= nsub * ngroups) break;
+        const int4 sp = a.subprob[s / ngroups];
+        const int tg = s % ngroups;
+        const int bin = sp.x, start = sp.y, cnt = sp.z;
+        const int b1 = bin % a.g.nb[0], b2 = bin / a.g.nb[0];
+        const int lo1 = b1 * a.g.bs[0], lo2 = b2 * a.g.bs[1];
+        const int t = tg * 32 + lane;
+        const bool tok = t < a.ntransf;
+        C acc[X];
+#pragma unroll
+        for (int x = 0; x < X; ++x) acc[x] = C{(T)0, (T)0};
+        for (int p0 = 0; p0 < cnt; p0 += CH) {
+            const int nch = min(CH, cnt - p0);
+            __syncthreads();
+            if (tid < nch) {
+                const Rec rc = load_rec(a.rec, start + p0 + tid);
+                T r[W];
+                int i0 = kernel_row<T, W>(rc.g[0], a.k, r);
+                s_o[tid * 2 + 0] = (i0 < 0 ? i0 + n1 : i0) - lo1;
+#pragma unroll
+                for (int m = 0; m < W; ++m) s_r[(tid * 2 + 0) * W + m] = r[m];
+                i0 = kernel_row<T, W>(rc.g[1], a.k, r);
+                s_o[tid * 2 + 1] = (i0 < 0 ? i0 + n2 : i0) - lo2;
+#pragma unroll
+                for (int m = 0; m < W; ++m) s_r[(tid * 2 + 1) * W + m] = r[m];
+                s_j[tid] = rc.j;
+            }
+            __syncthreads();
+            // strengths of the chunk for this transform group: lane = transform
+            for (int q = row; q < nch; q += RY) {
+                const int j = s_j[q];
+                C c = tok ? reinterpret_cast<const C *>(a.c)[(int64_t)t * a.M + j] : C{(T)0, (T)0};
+                if (tok && !finite2<T>(c)) flag_min(&a.flags[6], (unsigned long long)j);
+                s_c[q * 32 + lane] = c;
+            }
+            __syncthreads();
+            for (int q = 0; q < nch; ++q) {
+                const int oy = s_o[q * 2 + 1];
+                const int dy = row - oy;
+                if (dy < 0 || dy >= W) continue;  // warp-uniform (one row per warp)
+                const T *rq = s_r + q * 2 * W;
+                const T f = rq[W + dy];
+                const C cq = s_c[q * 32 + lane];
+                const C v{cq.x * f, cq.y * f};
+                T r1[W];
+#pragma unroll
+                for (int m = 0; m < W; ++m) r1[m] = rq[m];
+                rows_accumulate<T, 2, W>(acc, s_o[q * 2], v, r1);
+            }
+        }
+        if (tok) {
+            C *grid = reinterpret_cast<C *>(a.grid) + (int64_t)t * a.gstride;
+            int g2 = lo2 + row;
+            while (g2 >= n2) g2 -= n2;
+#pragma unroll
+            for (int x = 0; x < X; ++x) {
+                if (acc[x].x == (T)0 && acc[x].y == (T)0) continue;
+                int g1 = lo1 + x;
+                while (g1 >= n1) g1 -= n1;
+                red_add(grid + (int64_t)g2 * n1 + g1, acc[x]);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Lane-group interpolator (spreadinterp.py:442-507).  A group of G lanes
+// (G = 8 for w <= 8, 16 for w <= 16) handles one sorted point: lane m owns
+// ordinate m along x, evaluates r1[m], r2[m], r3[m] itself, and walks the
+// w^(d-1) rows reading one contiguous run of w cells per row (coalesced
+// 128-byte segments instead of 32 scattered lanes).  Row weights come from
+// the owning lane by shuffle; a butterfly reduction finishes the sum, and
+// the result is written in ORIGINAL point order (spreadinterp.py:453).
+template <typename T, int DIM, int W>
+__global__ void __launch_bounds__(256) k_interp_group(SpreadArgs<T> a, T *cout, const T *gridp, int chunk) {
+    using C = typename Cx<T>::type;
+    constexpr int G = W <= 8 ? 8 : 16;
+    constexpr int PPW = 32 / G;  // points per warp per step
     const int n1 = a.g.n[0], n2 = a.g.n[1], n3 = a.g.n[2];
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < a.M;
-         k += (int64_t)gridDim.x * blockDim.x) {
-        const int j = a.perm[k];
-        T r1[W], r2[W], r3[W];
-        int ix1[W], ix2[W], ix3[W];
-        int i1 = kernel_row<T, W>(a.gs[0][k], a.k, r1);
-#pragma unroll
-        for (int m = 0; m < W; ++m) ix1[m] = wrap_once(i1 + m, n1);
-        if (DIM > 1) {
-            int i2 = kernel_row<T, W>(a.gs[1][k], a.k, r2);
-#pragma unroll
-            for (int m = 0; m < W; ++m) ix2[m] = wrap_once(i2 + m, n2);
-        }
-        if (DIM > 2) {
-            int i3 = kernel_row<T, W>(a.gs[2][k], a.k, r3);
-#pragma unroll
-            for (int m = 0; m < W; ++m) ix3[m] = wrap_once(i3 + m, n3);
-        }
-        for (int t = 0; t < a.ntransf; ++t) {
-            const C *grid = reinterpret_cast<const C *>(gridp) + (int64_t)t * a.gstride;
-            T are = 0, aim = 0;
-            if (DIM == 1) {
-#pragma unroll
-                for (int m1 = 0; m1 < W; ++m1) {
-                    C v = __ldg(grid + ix1[m1]);
-                    are = fma(r1[m1], v.x, are);
-                    aim = fma(r1[m1], v.y, aim);
-                }
-            } else if (DIM == 2) {
-#pragma unroll
-                for (int m2 = 0; m2 < W; ++m2) {
-                    const C *row = grid + (int64_t)ix2[m2] * n1;
-                    T pre = 0, pim = 0;
-#pragma unroll
-                    for (int m1 = 0; m1 < W; ++m1) {
-                        C v = __ldg(row + ix1[m1]);
-                        pre = fma(r1[m1], v.x, pre);
-                        pim = fma(r1[m1], v.y, pim);
-                    }
-                    are = fma(r2[m2], pre, are);
-                    aim = fma(r2[m2], pim, aim);
-                }
-            } else {
-#pragma unroll 1
-                for (int m3 = 0; m3 < W; ++m3) {
-                    T p3re = 0, p3im = 0;
+    const int lane = threadIdx.x & 31, gl = lane % G, gbase = lane - gl;
+    const int warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    const int mm = gl < W ? gl : W - 1;
+    T cf[W + 4];
+    kernel_col<T, W>(a.k, mm, cf);
+    // each CTA walks contiguous chunks of the sorted order so a bin's patch
+    // stays hot in L1 while all of its points are interpolated
+    for (int64_t c0 = (int64_t)blockIdx.x * chunk; c0 < a.M; c0 += (int64_t)gridDim.x * chunk) {
+        const int64_t c1 = min(c0 + chunk, a.M);
+        for (int64_t k0 = c0 + (int64_t)warp * PPW; k0 < c1; k0 += (int64_t)nwarp * PPW) {
+            const int64_t k = k0 + lane / G;
+            const bool live = k < c1;
+            const Rec rc = load_rec(a.rec, live ? k : c1 - 1);
+            int i1, i2 = 0, i3 = 0;
+            const T r1 = kernel_one<T, W>(rc.g[0], mm, cf, a.k, &i1);
+            T r2 = (T)1, r3 = (T)1;
+            if (DIM > 1) r2 = kernel_one<T, W>(rc.g[1], mm, cf, a.k, &i2);
+            if (DIM > 2) r3 = kernel_one<T, W>(rc.g[2], mm, cf, a.k, &i3);
+            const int x = wrap_once(i1 + mm, n1);
+            const T w1 = gl < W ? r1 : (T)0;
+            for (int t = 0; t < a.ntransf; ++t) {
+                const C *grid = reinterpret_cast<const C *>(gridp) + (int64_t)t * a.gstride;
+                T are = 0, aim = 0;
+                if (DIM == 1) {
+                    const C v = __ldg(grid + x);
+                    are = v.x;
+                    aim = v.y;
+                } else if (DIM == 2) {
 #pragma unroll
                     for (int m2 = 0; m2 < W; ++m2) {
-                        const C *row = grid + ((int64_t)ix3[m3] * n2 + ix2[m2]) * n1;
+                        const T w2 = __shfl_sync(0xffffffffu, r2, gbase + m2);
+                        const int y = wrap_once(i2 + m2, n2);
+                        const C v = __ldg(grid + (int64_t)y * n1 + x);
+                        are = fma(w2, v.x, are);
+                        aim = fma(w2, v.y, aim);
+                    }
+                } else {
+#pragma unroll 1
+                    for (int m3 = 0; m3 < W; ++m3) {
+                        const T w3 = __shfl_sync(0xffffffffu, r3, gbase + m3);
+                        const int z = wrap_once(i3 + m3, n3);
                         T pre = 0, pim = 0;
 #pragma unroll
-                        for (int m1 = 0; m1 < W; ++m1) {
-                            C v = __ldg(row + ix1[m1]);
-                            pre = fma(r1[m1], v.x, pre);
-                            pim = fma(r1[m1], v.y, pim);
+                        for (int m2 = 0; m2 < W; ++m2) {
+                            const T w2 = __shfl_sync(0xffffffffu, r2, gbase + m2);
+                            const int y = wrap_once(i2 + m2, n2);
+                            const C v = __ldg(grid + ((int64_t)z * n2 + y) * n1 + x);
+                            pre = fma(w2, v.x, pre);
+                            pim = fma(w2, v.y, pim);
                         }
-                        p3re = fma(r2[m2], pre, p3re);
-                        p3im = fma(r2[m2], pim, p3im);
+                        are = fma(w3, pre, are);
+                        aim = fma(w3, pim, aim);
                     }
-                    are = fma(r3[m3], p3re, are);
-                    aim = fma(r3[m3], p3im, aim);
                 }
+                are *= w1;
+                aim *= w1;
+#pragma unroll
+                for (int o = G / 2; o > 0; o >>= 1) {
+                    are += __shfl_xor_sync(0xffffffffu, are, o);
+                    aim += __shfl_xor_sync(0xffffffffu, aim, o);
+                }
+                if (gl == 0 && live) reinterpret_cast<C *>(cout)[(int64_t)t * a.M + rc.j] = C{are, aim};
             }
-            reinterpret_cast<C *>(cout)[(int64_t)t * a.M + j] = C{are, aim};
         }
     }
 }

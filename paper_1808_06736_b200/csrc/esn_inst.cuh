@@ -23,24 +23,61 @@ struct SpreadGlobalOp {
     }
 };
 
+template <typename K>
+static int persistent_launch(K kernel, int threads, size_t smem, cudaStream_t st, const void *args_dummy,
+                             int *grid_out) {
+    (void)args_dummy;
+    ESN_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ESN_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                      cudaSharedmemCarveoutMaxShared));
+    int occ = 0;
+    ESN_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem));
+    if (occ < 1) return fail(ESN_RESOURCE_ERROR, "spreader CTA (%d threads, %zu B smem) does not fit an SM", threads, smem);
+    *grid_out = device_sm_count() * occ;
+    return ESN_SUCCESS;
+}
+
 template <typename T, int D, int W>
-struct SpreadTileOp {
+struct SpreadRowsOp {
     static int run(const SpreadArgs<T> &a, cudaStream_t st) {
         if (a.M == 0) return ESN_SUCCESS;
-        const int dtype = sizeof(T) == 8 ? ESN_F64 : ESN_F32;
-        const size_t smem = tile_smem_bytes(D, W, a.g.bs, dtype);
-        static size_t configured = 0;
-        if (smem > configured) {
-            ESN_CUDA_TRY(cudaFuncSetAttribute(k_spread_tile<T, D, W>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            configured = smem;
+        if (D == 1) return SpreadGlobalOp<T, D, W>::run(a, st);
+        using Cfg = RowsCfg<T, (D < 2 ? 2 : D), W>;
+        using C = typename Cx<T>::type;
+        const size_t stage = Cfg::CH * sizeof(C) + Cfg::CH * 3 * W * sizeof(T) + Cfg::CH * 4 * sizeof(int) +
+                             (Cfg::NT / 32) * Cfg::CH;
+        const size_t tile = (size_t)Cfg::RY * Cfg::RZ * Cfg::X * sizeof(C);
+        const size_t smem = stage > tile ? stage : tile;
+        static int grid = 0;
+        if (grid == 0) {
+            int rc = persistent_launch(k_spread_rows<T, (D < 2 ? 2 : D), W>, Cfg::NT, smem, st, nullptr, &grid);
+            if (rc) return rc;
         }
-        int occ = 0;
-        ESN_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spread_tile<T, D, W>, 256, smem));
-        if (occ < 1) return fail(ESN_RESOURCE_ERROR, "spread tile of %zu bytes does not fit in shared memory", smem);
-        k_spread_tile<T, D, W><<<device_sm_count() * occ, 256, smem, st>>>(a);
+        k_spread_rows<T, (D < 2 ? 2 : D), W><<<grid, Cfg::NT, smem, st>>>(a);
         ESN_CUDA_TRY(cudaGetLastError());
         return ESN_SUCCESS;
+    }
+};
+
+template <typename T, int D, int W>
+struct SpreadBatchOp {
+    static int run(const SpreadArgs<T> &a, cudaStream_t st) {
+        if (a.M == 0) return ESN_SUCCESS;
+        if constexpr (D == 2 && sizeof(T) == 4 && W <= 10) {
+            using Cfg = Batch2Cfg<T, W>;
+            using C = typename Cx<T>::type;
+            const size_t smem = Cfg::CH * 32 * sizeof(C) + Cfg::CH * 2 * W * sizeof(T) + Cfg::CH * 3 * sizeof(int);
+            static int grid = 0;
+            if (grid == 0) {
+                int rc = persistent_launch(k_spread_batch2d<T, W>, Cfg::NT, smem, st, nullptr, &grid);
+                if (rc) return rc;
+            }
+            k_spread_batch2d<T, W><<<grid, Cfg::NT, smem, st>>>(a);
+            ESN_CUDA_TRY(cudaGetLastError());
+            return ESN_SUCCESS;
+        } else {
+            return SpreadRowsOp<T, D, W>::run(a, st);
+        }
     }
 };
 
@@ -48,7 +85,12 @@ template <typename T, int D, int W>
 struct InterpOp {
     static int run(const SpreadArgs<T> &a, T *cout, const T *grid, cudaStream_t st) {
         if (a.M == 0) return ESN_SUCCESS;
-        k_interp_thread<T, D, W><<<grid_for(a.M, 256), 256, 0, st>>>(a, cout, grid);
+        // contiguous chunks of the sorted order per CTA (L1 reuse of a bin's patch)
+        const int chunk = 1024;
+        int64_t blocks = (a.M + chunk - 1) / chunk;
+        const int64_t cap = (int64_t)device_sm_count() * 8;
+        if (blocks > cap) blocks = cap;
+        k_interp_group<T, D, W><<<(int)blocks, 256, 0, st>>>(a, cout, grid, chunk);
         ESN_CUDA_TRY(cudaGetLastError());
         return ESN_SUCCESS;
     }
@@ -57,9 +99,11 @@ struct InterpOp {
 template <>
 int launch_spread<ESN_T>(const SpreadArgs<ESN_T> &a, int method, int nbins, cudaStream_t st) {
     (void)nbins;
-    if (method == ESN_METHOD_GLOBAL)
+    if (method == ESN_METHOD_GLOBAL || a.g.dim == 1)
         return dispatch_dw<ESN_T, SpreadGlobalOp>(a.g.dim, a.g.w, a, st);
-    return dispatch_dw<ESN_T, SpreadTileOp>(a.g.dim, a.g.w, a, st);
+    if (a.ntransf > 1 && a.g.dim == 2 && sizeof(ESN_T) == 4 && a.g.w <= 10)
+        return dispatch_dw<ESN_T, SpreadBatchOp>(a.g.dim, a.g.w, a, st);
+    return dispatch_dw<ESN_T, SpreadRowsOp>(a.g.dim, a.g.w, a, st);
 }
 
 template <>

@@ -46,6 +46,18 @@ struct KernelTab {
     int use_exact;
 };
 
+// Sorted point record: float64 grid coordinates + original index, one
+// aligned 32-byte record per point for every plan dtype.  setpts writes it
+// with a single 256-bit store (STG.E.ENL2.256: a full L2 sector, so the
+// scattered writes need no read-modify-write) and the spreader /
+// interpolator read it coalesced with one 256-bit load.  float32 plans thus
+// keep float64 coordinates until the kernel row is formed.
+struct alignas(32) Rec {
+    double g[3];
+    int j;
+    int pad;
+};
+
 struct SetptsArgs {
     Geom g;
     int64_t M;
@@ -53,12 +65,10 @@ struct SetptsArgs {
     int grid_units;         // coordinates already in grid units [0, n) (no fold)
     const void *x[3];
     double scale[3];        // n_d / (2 pi), computed on the host (grid.py:167)
-    int *key;               // per original point: bin id
-    int *rank;              // per original point: rank inside its bin
     int *bin_count;         // nbins (zeroed before)
     int *bin_start;         // nbins + 1
-    int *perm;              // sorted position -> original index
-    void *gs[3];            // sorted grid coordinates (plan dtype)
+    int *cursor;            // nbins: running insert position (scatter pass)
+    Rec *rec;               // M sorted records
     unsigned long long *flags;  // [0..2] first non-finite per dim, [3..5] first |x|>3pi
     int check_bounds;
 };
@@ -69,8 +79,7 @@ struct SpreadArgs {
     KernelTab<T> k;
     int64_t M;
     int ntransf;
-    const T *gs[3];
-    const int *perm;
+    const Rec *rec;          // sorted point records
     const int *bin_start;
     const int4 *subprob;     // (bin, start, count, 0)
     const int *nsub;         // device count of subproblems
@@ -81,9 +90,38 @@ struct SpreadArgs {
     unsigned long long *flags;  // [6] first non-finite strength
 };
 
+// ---- compile-time geometry of the spreaders (shared with the host planner)
+template <typename T, int DIM, int W>
+struct RowsCfg {
+    static constexpr int BX = (sizeof(T) == 8) ? (W <= 8 ? 16 : 8) : (W <= 10 ? 32 : 16);
+    static constexpr int X = BX + W - 1;
+    static constexpr int RY = DIM == 3 ? 16 : 64;
+    static constexpr int RZ = DIM == 3 ? 16 : 1;
+    static constexpr int NT = RY * RZ;
+    static constexpr int BY = RY - W + 1;
+    static constexpr int BZ = DIM == 3 ? RZ - W + 1 : 1;
+    static constexpr int CH = 64;  // staged points per chunk
+    static constexpr int MINB = (sizeof(T) == 8 && DIM == 3) ? 2 : 1;
+};
+
+template <typename T, int W>
+struct Batch2Cfg {
+    static constexpr int BX = 16;
+    static constexpr int X = BX + W - 1;
+    static constexpr int BY = 16;
+    static constexpr int RY = BY + W - 1;  // rows (one warp each)
+    static constexpr int NT = RY * 32;
+    static constexpr int CH = 64;
+};
+
 // ---- launchers (esn_kernels.cu)
 int launch_setpts(const SetptsArgs &a, int dtype, int nbins, int max_subprob, int4 *subprob,
                   int *nsub, int *scan_aux, cudaStream_t st);
+int launch_sort_view(int dtype, const void *rec, const int *bin_start, int nbins, int64_t M, int *perm,
+                     int *keys, cudaStream_t st);
+// Bin geometry the chosen spreader needs: (bx, by, bz); returns 0 if the
+// method has no fixed geometry (global atomics).
+int spreader_bins(int method, int dtype, int dim, int w, int ntransf, int *bs);
 template <typename T>
 int launch_spread(const SpreadArgs<T> &a, int method, int nbins, cudaStream_t st);
 template <typename T>
@@ -95,7 +133,6 @@ template <typename T>
 int launch_amplify(int dim, int ntransf, const int *n, const int64_t *N, const T *f, const T *p1,
                    const T *p2, const T *p3, T *grid, unsigned long long *flag, cudaStream_t st);
 
-size_t tile_smem_bytes(int dim, int w, const int *bs, int dtype);
 int device_sm_count();
 
 }  // namespace esn

@@ -95,8 +95,8 @@ struct esn_plan_s {
     int64_t G = 1;
     // device state
     void *pk[3] = {nullptr, nullptr, nullptr};
-    void *gs[3] = {nullptr, nullptr, nullptr};
-    int *perm = nullptr, *key = nullptr, *rank = nullptr;
+    Rec *rec = nullptr;  // sorted point records
+    int *cursor = nullptr;
     int *bin_count = nullptr, *bin_start = nullptr, *subofs = nullptr, *nsub = nullptr, *work = nullptr;
     int4 *subprob = nullptr;
     unsigned long long *flags = nullptr;
@@ -125,31 +125,49 @@ static void dfree(void *ptr) {
     if (ptr) cudaFree(ptr);
 }
 
+template <int W>
+static void rows_bins(int dtype, int dim, int ntransf, int *bs) {
+    if (dim == 3) {
+        if (dtype == ESN_F64) {
+            bs[0] = RowsCfg<double, 3, W>::BX; bs[1] = RowsCfg<double, 3, W>::BY; bs[2] = RowsCfg<double, 3, W>::BZ;
+        } else {
+            bs[0] = RowsCfg<float, 3, W>::BX; bs[1] = RowsCfg<float, 3, W>::BY; bs[2] = RowsCfg<float, 3, W>::BZ;
+        }
+    } else if (dtype == ESN_F32 && ntransf > 1 && W <= 10) {
+        bs[0] = Batch2Cfg<float, W>::BX; bs[1] = Batch2Cfg<float, W>::BY; bs[2] = 1;
+    } else if (dtype == ESN_F64) {
+        bs[0] = RowsCfg<double, 2, W>::BX; bs[1] = RowsCfg<double, 2, W>::BY; bs[2] = 1;
+    } else {
+        bs[0] = RowsCfg<float, 2, W>::BX; bs[1] = RowsCfg<float, 2, W>::BY; bs[2] = 1;
+    }
+}
+
+int esn::spreader_bins(int method, int dtype, int dim, int w, int ntransf, int *bs) {
+    bs[0] = bs[1] = bs[2] = 1;
+    if (method == ESN_METHOD_GLOBAL || dim == 1) return 0;
+    switch (w) {
+#define ESN_BW(WW) case WW: rows_bins<WW>(dtype, dim, ntransf, bs); return 1;
+        ESN_BW(2) ESN_BW(3) ESN_BW(4) ESN_BW(5) ESN_BW(6) ESN_BW(7) ESN_BW(8) ESN_BW(9)
+        ESN_BW(10) ESN_BW(11) ESN_BW(12) ESN_BW(13) ESN_BW(14) ESN_BW(15) ESN_BW(16)
+#undef ESN_BW
+    }
+    return 0;
+}
+
 static void choose_bins(esn_plan p) {
     const int dim = p->dim, w = p->kp.w;
     int bs[3] = {1, 1, 1};
-    for (int d = 0; d < 3; ++d)
-        if (p->opts.bin_size[d] > 0) bs[d] = p->opts.bin_size[d];
-    bool user = p->opts.bin_size[0] > 0;
-    if (!user) {
+    if (!esn::spreader_bins(p->method, p->dtype, dim, w, p->ntransf, bs)) {
+        // global-atomic spreader / 1D: bins only order the points for locality
         if (dim == 1) {
             bs[0] = 1024;
         } else if (dim == 2) {
-            bs[0] = 32;
-            bs[1] = 32;
+            bs[0] = 32; bs[1] = 32;
         } else {
-            bs[0] = 16;
-            bs[1] = 8;
-            bs[2] = 8;
+            bs[0] = 16; bs[1] = 8; bs[2] = 8;
         }
-        // keep the shared-memory tile within ~100 KB (2 CTAs per SM)
-        while (tile_smem_bytes(dim, w, bs, p->dtype) > 100 * 1024) {
-            int big = 0;
-            for (int d = 1; d < dim; ++d)
-                if (bs[d] > bs[big]) big = d;
-            if (bs[big] <= 2) break;
-            bs[big] /= 2;
-        }
+        for (int d = 0; d < 3; ++d)
+            if (p->opts.bin_size[d] > 0) bs[d] = p->opts.bin_size[d];
     }
     p->nbins = 1;
     for (int d = 0; d < 3; ++d) {
@@ -185,13 +203,14 @@ static int plan_common_init(esn_plan p, const esn_opts *o) {
                     "fine grids need %lld complex values, over the cap of %lld; this regime is better "
                     "served by direct summation",
                     (long long)p->G, (long long)p->opts.max_grid_values);
-    choose_bins(p);
     p->method = p->opts.method;
     if (p->method == ESN_METHOD_AUTO) p->method = (p->dim == 1) ? ESN_METHOD_GLOBAL : ESN_METHOD_TILE;
+    choose_bins(p);
     p->maxsub = p->opts.max_subprob > 0 ? p->opts.max_subprob : 8192;
     int rc;
     if ((rc = dmalloc(p, &p->bin_count, sizeof(int) * p->nbins))) return rc;
     if ((rc = dmalloc(p, &p->bin_start, sizeof(int) * (p->nbins + 1)))) return rc;
+    if ((rc = dmalloc(p, &p->cursor, sizeof(int) * (p->nbins + 1)))) return rc;
     if ((rc = dmalloc(p, &p->subofs, sizeof(int) * (p->nbins + 1)))) return rc;
     if ((rc = dmalloc(p, &p->nsub, sizeof(int) * 2))) return rc;
     if ((rc = dmalloc(p, &p->work, sizeof(int) * 2))) return rc;
@@ -278,13 +297,9 @@ int esn_plan_destroy(esn_plan p) {
     if (!p) return ESN_SUCCESS;
     if (p->st) cudaStreamSynchronize(p->st);
     else cudaDeviceSynchronize();
-    for (int d = 0; d < 3; ++d) {
-        dfree(p->pk[d]);
-        dfree(p->gs[d]);
-    }
-    dfree(p->perm);
-    dfree(p->key);
-    dfree(p->rank);
+    for (int d = 0; d < 3; ++d) dfree(p->pk[d]);
+    dfree(p->rec);
+    dfree(p->cursor);
     dfree(p->bin_count);
     dfree(p->bin_start);
     dfree(p->subofs);
@@ -375,14 +390,10 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
         if (M > 0 && !xs[d]) return fail(ESN_SIZE_ERROR, "coordinate array %d missing", d + 1);
     int rc;
     if (M > p->Mcap) {
-        for (int d = 0; d < 3; ++d) { dfree(p->gs[d]); p->gs[d] = nullptr; }
-        dfree(p->perm); dfree(p->key); dfree(p->rank);
-        p->perm = p->key = p->rank = nullptr;
-        for (int d = 0; d < p->dim; ++d)
-            if ((rc = dmalloc(p, &p->gs[d], real_size(p->dtype) * M))) return rc;
-        if ((rc = dmalloc(p, &p->perm, sizeof(int) * M))) return rc;
-        if ((rc = dmalloc(p, &p->key, sizeof(int) * M))) return rc;
-        if ((rc = dmalloc(p, &p->rank, sizeof(int) * M))) return rc;
+        dfree(p->rec);
+        p->rec = nullptr;
+        if ((rc = dmalloc(p, &p->rec, sizeof(Rec) * M)))
+            return rc;
         p->Mcap = M;
     }
     const int64_t subneed = p->nbins + M / p->maxsub + 1;
@@ -404,13 +415,11 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
     for (int d = 0; d < 3; ++d) {
         a.x[d] = d < p->dim ? xs[d] : nullptr;
         a.scale[d] = (double)p->n[d] / (2.0 * M_PI);  // sizes[d] / TWO_PI (spreadinterp.py:99)
-        a.gs[d] = p->gs[d];
     }
-    a.key = p->key;
-    a.rank = p->rank;
     a.bin_count = p->bin_count;
     a.bin_start = p->bin_start;
-    a.perm = p->perm;
+    a.cursor = p->cursor;
+    a.rec = p->rec;
     a.flags = p->flags;
     a.check_bounds = p->opts.check_bounds;
     if ((rc = launch_setpts(a, p->dtype, p->nbins, p->maxsub, p->subprob, p->nsub, p->subofs, p->st))) return rc;
@@ -431,8 +440,7 @@ static SpreadArgs<T> make_spread_args(esn_plan p, const void *c, void *grid) {
     a.k.use_exact = p->opts.use_exact_kernel;
     a.M = p->M;
     a.ntransf = p->ntransf;
-    for (int d = 0; d < 3; ++d) a.gs[d] = (const T *)p->gs[d];
-    a.perm = p->perm;
+    a.rec = p->rec;
     a.bin_start = p->bin_start;
     a.subprob = p->subprob;
     a.nsub = p->nsub;
@@ -611,10 +619,8 @@ int esn_plan_bins(esn_plan p, int *nbins, int *bin_size, int *bins_per_dim) {
 
 int esn_plan_sort_view(esn_plan p, void *perm, void *keys, void *bin_start) {
     if (!p || !p->points_set) return fail(ESN_SIZE_ERROR, "plan has no points");
-    if (p->M > 0 && perm)
-        ESN_CUDA_TRY(cudaMemcpyAsync(perm, p->perm, sizeof(int) * p->M, cudaMemcpyDeviceToDevice, p->st));
-    if (p->M > 0 && keys)
-        ESN_CUDA_TRY(cudaMemcpyAsync(keys, p->key, sizeof(int) * p->M, cudaMemcpyDeviceToDevice, p->st));
+    int rc = launch_sort_view(p->dtype, p->rec, p->bin_start, p->nbins, p->M, (int *)perm, (int *)keys, p->st);
+    if (rc) return rc;
     if (bin_start)
         ESN_CUDA_TRY(cudaMemcpyAsync(bin_start, p->bin_start, sizeof(int) * (p->nbins + 1),
                                      cudaMemcpyDeviceToDevice, p->st));

@@ -51,14 +51,6 @@ int device_sm_count() {
     return cached[dev];
 }
 
-size_t tile_smem_bytes(int dim, int w, const int *bs, int dtype) {
-    const size_t real = dtype == ESN_F64 ? 8 : 4;
-    size_t cells = 1;
-    for (int d = 0; d < dim; ++d) cells *= (size_t)(bs[d] + w - 1);
-    const size_t CH = 64;
-    return cells * 2 * real + CH * dim * w * real + CH * 2 * real + CH * dim * sizeof(int) + 16;
-}
-
 // grid.py:152-168 + spreadinterp.py:99-100 in float64: np.mod(x, 2 pi)
 // (fmod plus 2 pi when the signs differ), exact 2 pi wraps to 0, scale by
 // n / 2 pi (host-computed), pull back g >= n.  Bit-identical to numpy.
@@ -79,13 +71,13 @@ __device__ __forceinline__ T to_plan(double g, int n) {
     return v;
 }
 
-template <typename XT, typename T>
-__device__ __forceinline__ int point_key(const SetptsArgs &a, int64_t i, T *gout, bool check) {
+template <typename T>
+__device__ __forceinline__ int point_key(const SetptsArgs &a, int64_t i, const double *xin, double *gout, bool check) {
     int key = 0, mul = 1;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
         if (d >= a.g.dim) break;
-        const double x = (double)reinterpret_cast<const XT *>(a.x[d])[i];
+        const double x = xin[d];
         double g = 0.0;
         if (!isfinite(x)) {
             if (check) atomicMin(&a.flags[d], (unsigned long long)i);
@@ -100,9 +92,8 @@ __device__ __forceinline__ int point_key(const SetptsArgs &a, int64_t i, T *gout
                 g = fold_scale(x, (double)a.g.n[d], a.scale[d]);
             }
         }
-        const T gt = to_plan<T>(g, a.g.n[d]);
-        gout[d] = gt;
-        int i0 = (int)floor(gt - (T)(0.5 * a.g.w) + (T)1);
+        gout[d] = g;
+        int i0 = (int)floor(g - 0.5 * a.g.w + 1.0);  // spreadinterp.py:117-120
         if (i0 < 0) i0 += a.g.n[d];
         key += (i0 / a.g.bs[d]) * mul;
         mul *= a.g.nb[d];
@@ -110,42 +101,74 @@ __device__ __forceinline__ int point_key(const SetptsArgs &a, int64_t i, T *gout
     return key;
 }
 
-template <typename XT, typename T>
-__global__ void __launch_bounds__(256) k_setpts_bin(SetptsArgs a) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.M;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        T g[3];
-        const int key = point_key<XT, T>(a, i, g, true);
-        // warp-aggregated histogram increment: one atomic per distinct bin
-        // in the warp (clustered inputs collapse to a single atomic)
-        const unsigned active = __activemask();
-        const unsigned peers = __match_any_sync(active, key);
-        const int lane = threadIdx.x & 31;
-        const int leader = __ffs(peers) - 1;
-        int base = 0;
-        if (lane == leader) base = atomicAdd(&a.bin_count[key], __popc(peers));
-        base = __shfl_sync(peers, base, leader);
-        a.key[i] = key;
-        a.rank[i] = base + __popc(peers & ((1u << lane) - 1));
+constexpr int kILP = 4;  // points in flight per thread (independent loads / atomics)
+
+template <typename XT>
+__device__ __forceinline__ void load_coords(const SetptsArgs &a, int64_t base, double (*x)[3]) {
+    // all loads first (independent, read-only), compute afterwards
+#pragma unroll
+    for (int u = 0; u < kILP; ++u) {
+        const int64_t i = base + (int64_t)u * blockDim.x;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            x[u][d] = 0.0;
+            if (d < a.g.dim && i < a.M) x[u][d] = (double)__ldg(reinterpret_cast<const XT *>(a.x[d]) + i);
+        }
     }
 }
 
+// Pass 1: bin histogram (fire-and-forget REDs, no return value needed) and
+// the finite / bounds flags.
+template <typename XT, typename T>
+__global__ void __launch_bounds__(256) k_setpts_count(SetptsArgs a) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * kILP;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x * kILP + threadIdx.x; base < a.M; base += stride) {
+        double x[kILP][3];
+        load_coords<XT>(a, base, x);
+#pragma unroll
+        for (int u = 0; u < kILP; ++u) {
+            const int64_t i = base + (int64_t)u * blockDim.x;
+            if (i >= a.M) continue;
+            double g[3];
+            atomicAdd(&a.bin_count[point_key<T>(a, i, x[u], g, true)], 1);
+        }
+    }
+}
+
+// Pass 2: claim a slot in the point's bin (atomic on the bin cursor) and
+// write its full record {g, j} there with one 256-bit store.
 template <typename XT, typename T>
 __global__ void __launch_bounds__(256) k_setpts_scatter(SetptsArgs a) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.M;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        T g[3];
-        point_key<XT, T>(a, i, g, false);
-        const int pos = a.bin_start[a.key[i]] + a.rank[i];
-        a.perm[pos] = (int)i;
-        for (int d = 0; d < a.g.dim; ++d) reinterpret_cast<T *>(a.gs[d])[pos] = g[d];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * kILP;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x * kILP + threadIdx.x; base < a.M; base += stride) {
+        double x[kILP][3];
+        load_coords<XT>(a, base, x);
+        int pos[kILP];
+#pragma unroll
+        for (int u = 0; u < kILP; ++u) {
+            const int64_t i = base + (int64_t)u * blockDim.x;
+            double g[3];
+            pos[u] = i < a.M ? atomicAdd(&a.cursor[point_key<T>(a, i, x[u], g, false)], 1) : -1;
+            x[u][0] = g[0];
+            x[u][1] = a.g.dim > 1 ? g[1] : 0.0;
+            x[u][2] = a.g.dim > 2 ? g[2] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kILP; ++u) {
+            if (pos[u] < 0) continue;
+            const unsigned long long j = (unsigned long long)(unsigned)(base + (int64_t)u * blockDim.x);
+            asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(a.rec + pos[u]),
+                         "l"(__double_as_longlong(x[u][0])), "l"(__double_as_longlong(x[u][1])),
+                         "l"(__double_as_longlong(x[u][2])), "l"(j)
+                         : "memory");
+        }
     }
 }
 
 // Single-CTA exclusive scan of the bin counts and of the per-bin subproblem
 // counts ceil(count / max_subprob); also publishes the subproblem total.
-__global__ void __launch_bounds__(1024) k_scan_bins(const int *count, int *start, int *subofs, int nbins,
-                                                    int maxsub, int *nsub_total) {
+__global__ void __launch_bounds__(1024) k_scan_bins(const int *count, int *start, int *cursor, int *subofs,
+                                                    int nbins, int maxsub, int *nsub_total) {
     __shared__ int wsum[2][32];
     __shared__ int carry[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -189,6 +212,7 @@ __global__ void __launch_bounds__(1024) k_scan_bins(const int *count, int *start
         const int offs = carry[1] + (warp ? wsum[1][warp - 1] : 0);
         if (i < nbins) {
             start[i] = offc + xc - c;
+            cursor[i] = offc + xc - c;
             subofs[i] = offs + xs - s;
         }
         __syncthreads();
@@ -219,15 +243,15 @@ template <typename XT, typename T>
 static int setpts_impl(const SetptsArgs &a, int nbins, int maxsub, int4 *subprob, int *nsub, int *scan_aux,
                        cudaStream_t st) {
     const int threads = 256;
-    int64_t blocks = (a.M + threads - 1) / threads;
-    const int64_t cap = (int64_t)device_sm_count() * 16;
+    int64_t blocks = (a.M + threads * kILP - 1) / (threads * kILP);
+    const int64_t cap = (int64_t)device_sm_count() * 8;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     if (a.M > 0) {
-        k_setpts_bin<XT, T><<<(int)blocks, threads, 0, st>>>(a);
+        k_setpts_count<XT, T><<<(int)blocks, threads, 0, st>>>(a);
         ESN_CUDA_TRY(cudaGetLastError());
     }
-    k_scan_bins<<<1, 1024, 0, st>>>(a.bin_count, a.bin_start, scan_aux, nbins, maxsub, nsub);
+    k_scan_bins<<<1, 1024, 0, st>>>(a.bin_count, a.bin_start, a.cursor, scan_aux, nbins, maxsub, nsub);
     ESN_CUDA_TRY(cudaGetLastError());
     if (a.M > 0) {
         k_setpts_scatter<XT, T><<<(int)blocks, threads, 0, st>>>(a);
@@ -237,6 +261,26 @@ static int setpts_impl(const SetptsArgs &a, int nbins, int maxsub, int4 *subprob
                                                          subprob);
         ESN_CUDA_TRY(cudaGetLastError());
     }
+    return ESN_SUCCESS;
+}
+
+__global__ void k_sort_view(const Rec *rec, const int *bin_start, int nbins, int *perm, int *keys) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nbins; b += gridDim.x * blockDim.x) {
+        for (int k = bin_start[b]; k < bin_start[b + 1]; ++k) {
+            const int j = rec[k].j;
+            if (perm) perm[k] = j;
+            if (keys) keys[j] = b;
+        }
+    }
+}
+
+int launch_sort_view(int dtype, const void *rec, const int *bin_start, int nbins, int64_t M, int *perm, int *keys,
+                     cudaStream_t st) {
+    if (M == 0) return ESN_SUCCESS;
+    int fb = (nbins + 127) / 128;
+    (void)dtype;
+    k_sort_view<<<fb, 128, 0, st>>>((const Rec *)rec, bin_start, nbins, perm, keys);
+    ESN_CUDA_TRY(cudaGetLastError());
     return ESN_SUCCESS;
 }
 

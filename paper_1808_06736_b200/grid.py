@@ -136,7 +136,7 @@ def bin_sort(grid_coords, sizes, threads: int = 1) -> BinSortPermutation:
     # w = 2 makes the footprint origin floor(g - 1 + 1) = floor(g): the
     # reference's box coordinate
     p = Plan(0, dim, nfine=tuple(sizes), device=dev, params=params_for_width(2, 2.0),
-             bin_size=box, timing=False)
+             bin_size=box, method="global", timing=False)
     xs = [D.as_real_1d(g, "g", dev).to(torch.float64) for g in grid_coords]
     p.setpts(xs, grid_units=True)
     perm, keys, _ = p.sort_view()
