@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(RowsCfg<T, DIM, W>::NT, RowsCfg<T, DIM, W>::MI
                     s_c[tid] = c;
                     // enqueue this point for every row block its w x w rows meet
                     const int y0 = oy / WBY, y1 = (oy + W - 1) / WBY;
-                    const int z0 = oz / WBZ, z1 = (oz + W - 1) / WBZ;
+                    const int z0 = DIM > 2 ? oz / WBZ : 0, z1 = DIM > 2 ? (oz + W - 1) / WBZ : 0;
                     for (int zz = z0; zz <= z1; ++zz)
                         for (int yy = y0; yy <= y1; ++yy) {
                             const int wb = zz * NWY + yy;
