@@ -278,14 +278,17 @@ __global__ void __launch_bounds__(RowsCfg<T, DIM, W>::NT, RowsCfg<T, DIM, W>::MI
     constexpr int WBY = DIM == 3 ? 8 : 32;      // row-block extent in y
     constexpr int WBZ = DIM == 3 ? 4 : 1;       // row-block extent in z
     constexpr int NWY = RY / WBY;
+    constexpr int NZ = DIM == 3 ? W : 1;        // entries of the (c * r3) table
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    // staging: per point c, r1[W], r2[W], r3[W], offsets (ox, oy, oz); per
-    // warp the list of staged points whose row footprint meets its block
-    C *s_c = reinterpret_cast<C *>(smem_raw);
-    T *s_r = reinterpret_cast<T *>(s_c + CH);                 // CH x 3 x W
-    int *s_o = reinterpret_cast<int *>(s_r + CH * 3 * W);     // CH x 4
+    // staging per point (one thread each): c * r3[m] (complex, NZ), r2[W],
+    // r1[W], offsets (ox, oy, oz); per warp the list of staged points whose
+    // row footprint meets its block
+    C *s_cz = reinterpret_cast<C *>(smem_raw);                    // CH x NZ
+    T *s_r2 = reinterpret_cast<T *>(s_cz + CH * NZ);              // CH x W
+    T *s_r1 = s_r2 + CH * W;                                      // CH x W
+    int *s_o = reinterpret_cast<int *>(s_r1 + CH * W);            // CH x 4
     unsigned char *s_list = reinterpret_cast<unsigned char *>(s_o + CH * 4);  // NW x CH
-    C *s_tile = reinterpret_cast<C *>(smem_raw);              // reused for the flush: RY*RZ x X
+    C *s_tile = reinterpret_cast<C *>(smem_raw);                  // reused for the flush: RY*RZ x X
     __shared__ int s_sub;
     __shared__ int s_cnt[NW];
 
@@ -312,33 +315,38 @@ __global__ void __launch_bounds__(RowsCfg<T, DIM, W>::NT, RowsCfg<T, DIM, W>::MI
 #pragma unroll
             for (int x = 0; x < X; ++x) acc[x] = C{(T)0, (T)0};
             const C *cin = reinterpret_cast<const C *>(a.c) + (int64_t)t * a.M;
-            for (int p0 = 0; p0 < cnt; p0 += CH) {
-                const int nch = min(CH, cnt - p0);
+            // chunk ci stages points ci, ci + nck, ... of the subproblem: the
+            // sort is fine (sub-cell order), so strided chunks sample the whole
+            // bin and keep every row block busy
+            const int nck = (cnt + CH - 1) / CH;
+            for (int ci = 0; ci < nck; ++ci) {
+                const int nch = (cnt - ci + nck - 1) / nck;
                 __syncthreads();
                 if (tid < NW) s_cnt[tid] = 0;
                 __syncthreads();
                 if (tid < nch) {  // phase A: one thread per staged point
-                    const Rec rc = load_rec(a.rec, start + p0 + tid);
+                    const Rec rc = load_rec(a.rec, start + ci + tid * nck);
+                    C c = cin[rc.j];
+                    if (!finite2<T>(c)) flag_min(&a.flags[6], (unsigned long long)rc.j);
                     T r[W];
                     int i0 = kernel_row<T, W>(rc.g[0], a.k, r);
                     const int ox = (i0 < 0 ? i0 + n1 : i0) - lo1;
 #pragma unroll
-                    for (int m = 0; m < W; ++m) s_r[(tid * 3 + 0) * W + m] = r[m];
+                    for (int m = 0; m < W; ++m) s_r1[tid * W + m] = r[m];
                     i0 = kernel_row<T, W>(rc.g[1], a.k, r);
                     const int oy = (i0 < 0 ? i0 + n2 : i0) - lo2;
 #pragma unroll
-                    for (int m = 0; m < W; ++m) s_r[(tid * 3 + 1) * W + m] = r[m];
+                    for (int m = 0; m < W; ++m) s_r2[tid * W + m] = r[m];
                     int oz = 0;
                     if (DIM > 2) {
                         i0 = kernel_row<T, W>(rc.g[2], a.k, r);
                         oz = (i0 < 0 ? i0 + n3 : i0) - lo3;
 #pragma unroll
-                        for (int m = 0; m < W; ++m) s_r[(tid * 3 + 2) * W + m] = r[m];
+                        for (int m = 0; m < W; ++m) s_cz[tid * NZ + m] = C{c.x * r[m], c.y * r[m]};
+                    } else {
+                        s_cz[tid] = c;
                     }
                     *reinterpret_cast<int4 *>(s_o + tid * 4) = make_int4(ox, oy, oz, 0);
-                    C c = cin[rc.j];
-                    if (!finite2<T>(c)) flag_min(&a.flags[6], (unsigned long long)rc.j);
-                    s_c[tid] = c;
                     // enqueue this point for every row block its w x w rows meet
                     const int y0 = oy / WBY, y1 = (oy + W - 1) / WBY;
                     const int z0 = DIM > 2 ? oz / WBZ : 0, z1 = DIM > 2 ? (oz + W - 1) / WBZ : 0;
@@ -357,14 +365,12 @@ __global__ void __launch_bounds__(RowsCfg<T, DIM, W>::NT, RowsCfg<T, DIM, W>::MI
                     const int4 o = *reinterpret_cast<const int4 *>(s_o + q * 4);
                     const int dy = ry - o.y, dz = rz - o.z;
                     const bool cov = dy >= 0 && dy < W && (DIM < 3 || (dz >= 0 && dz < W));
-                    const T *rq = s_r + q * 3 * W;
-                    T f = cov ? rq[W + (cov ? dy : 0)] : (T)0;
-                    if (DIM > 2) f *= cov ? rq[2 * W + (cov ? dz : 0)] : (T)0;
-                    const C cq = s_c[q];
-                    const C v{cq.x * f, cq.y * f};
+                    const T f = cov ? s_r2[q * W + dy] : (T)0;
+                    const C cz = s_cz[q * NZ + ((DIM > 2 && cov) ? dz : 0)];
+                    const C v{cz.x * f, cz.y * f};
                     T r1[W];
 #pragma unroll
-                    for (int m = 0; m < W; ++m) r1[m] = rq[m];
+                    for (int m = 0; m < W; ++m) r1[m] = s_r1[q * W + m];
                     rows_accumulate<T, DIM, W>(acc, o.x, v, r1);
                 }
             }
@@ -404,15 +410,13 @@ __global__ void __launch_bounds__(RowsCfg<T, DIM, W>::NT, RowsCfg<T, DIM, W>::MI
 // the warps of its w rows with identical kernel values, so there is no lane
 // waste and the point data is a broadcast.
 template <typename T, int W>
-__global__ void __launch_bounds__(Batch2Cfg<T, W>::NT) k_spread_batch2d(SpreadArgs<T> a) {
+__global__ void __launch_bounds__(Batch2Cfg<T, W>::NT) k_spread_batch2d(SpreadArgs<T> a, const T *cperm) {
     using C = typename Cx<T>::type;
     using Cfg = Batch2Cfg<T, W>;
     constexpr int X = Cfg::X, RY = Cfg::RY, CH = Cfg::CH;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    C *s_c = reinterpret_cast<C *>(smem_raw);                 // CH x 32 strengths (point-major)
-    T *s_r = reinterpret_cast<T *>(s_c + CH * 32);            // CH x 2 x W
+    T *s_r = reinterpret_cast<T *>(smem_raw);                 // CH x 2 x W
     int *s_o = reinterpret_cast<int *>(s_r + CH * 2 * W);     // CH x 2
-    int *s_j = s_o + CH * 2;                                  // CH
     __shared__ int s_sub;
     const int tid = threadIdx.x, lane = tid & 31, row = tid >> 5;
     const int n1 = a.g.n[0], n2 = a.g.n[1];
@@ -430,7 +434,8 @@ __global__ void __launch_bounds__(Batch2Cfg<T, W>::NT) k_spread_batch2d(SpreadAr
         const int b1 = bin % a.g.nb[0], b2 = bin / a.g.nb[0];
         const int lo1 = b1 * a.g.bs[0], lo2 = b2 * a.g.bs[1];
         const int t = tg * 32 + lane;
-        const bool tok = t < a.ntransf;
+        // strengths of this group in sorted order: 32 transforms per point
+        const C *cg = reinterpret_cast<const C *>(cperm) + (int64_t)tg * a.M * 32;
         C acc[X];
 #pragma unroll
         for (int x = 0; x < X; ++x) acc[x] = C{(T)0, (T)0};
@@ -448,15 +453,6 @@ __global__ void __launch_bounds__(Batch2Cfg<T, W>::NT) k_spread_batch2d(SpreadAr
                 s_o[tid * 2 + 1] = (i0 < 0 ? i0 + n2 : i0) - lo2;
 #pragma unroll
                 for (int m = 0; m < W; ++m) s_r[(tid * 2 + 1) * W + m] = r[m];
-                s_j[tid] = rc.j;
-            }
-            __syncthreads();
-            // strengths of the chunk for this transform group: lane = transform
-            for (int q = row; q < nch; q += RY) {
-                const int j = s_j[q];
-                C c = tok ? reinterpret_cast<const C *>(a.c)[(int64_t)t * a.M + j] : C{(T)0, (T)0};
-                if (tok && !finite2<T>(c)) flag_min(&a.flags[6], (unsigned long long)j);
-                s_c[q * 32 + lane] = c;
             }
             __syncthreads();
             for (int q = 0; q < nch; ++q) {
@@ -465,7 +461,7 @@ __global__ void __launch_bounds__(Batch2Cfg<T, W>::NT) k_spread_batch2d(SpreadAr
                 if (dy < 0 || dy >= W) continue;  // warp-uniform (one row per warp)
                 const T *rq = s_r + q * 2 * W;
                 const T f = rq[W + dy];
-                const C cq = s_c[q * 32 + lane];
+                const C cq = cg[(int64_t)(start + p0 + q) * 32 + lane];  // coalesced 32 transforms
                 const C v{cq.x * f, cq.y * f};
                 T r1[W];
 #pragma unroll
@@ -473,7 +469,7 @@ __global__ void __launch_bounds__(Batch2Cfg<T, W>::NT) k_spread_batch2d(SpreadAr
                 rows_accumulate<T, 2, W>(acc, s_o[q * 2], v, r1);
             }
         }
-        if (tok) {
+        if (t < a.ntransf) {
             C *grid = reinterpret_cast<C *>(a.grid) + (int64_t)t * a.gstride;
             int g2 = lo2 + row;
             while (g2 >= n2) g2 -= n2;
@@ -484,6 +480,236 @@ __global__ void __launch_bounds__(Batch2Cfg<T, W>::NT) k_spread_batch2d(SpreadAr
                 while (g1 >= n1) g1 -= n1;
                 red_add(grid + (int64_t)g2 * n1 + g1, acc[x]);
             }
+        }
+    }
+}
+
+// Batched strengths into sorted order, 32 transforms per point:
+// cperm[g][pos(j)][l] = c[32 g + l][j] with pos(j) = start[key[j]] + rank[j].
+// A 32 x 32 tile transpose through shared memory: coalesced reads along j,
+// one contiguous 32-transform record per point on the write side.  Also the
+// finiteness check of the strengths.
+template <typename T>
+__global__ void __launch_bounds__(1024) k_permute_strengths(SpreadArgs<T> a, const int *key, const int *rank,
+                                                            const int *kstart, T *cperm) {
+    using C = typename Cx<T>::type;
+    __shared__ C tile[32][33];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int ngroups = (a.ntransf + 31) / 32;
+    const int64_t jtiles = (a.M + 31) / 32;
+    for (int64_t b = blockIdx.x; b < jtiles * ngroups; b += gridDim.x) {
+        const int g = (int)(b % ngroups);
+        const int64_t j0 = (b / ngroups) * 32;
+        const int t = g * 32 + ty;
+        const int64_t j = j0 + tx;
+        C v{(T)0, (T)0};
+        if (t < a.ntransf && j < a.M) {
+            v = reinterpret_cast<const C *>(a.c)[(int64_t)t * a.M + j];
+            if (!finite2<T>(v)) flag_min(&a.flags[6], (unsigned long long)j);
+        }
+        tile[ty][tx] = v;
+        __syncthreads();
+        const int64_t jj = j0 + ty;
+        if (jj < a.M) {
+            const int pos = kstart[key[jj]] + rank[jj];
+            reinterpret_cast<C *>(cperm)[((int64_t)g * a.M + pos) * 32 + tx] = tile[tx][ty];
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Tile interpolator (spreadinterp.py:442-507).  One CTA per subproblem
+// (persistent work queue): the bin's periodic patch of (bs + w - 1)^d fine
+// cells is staged once in shared memory with coalesced loads, then each
+// thread interpolates sorted points from it (separable weighted sum, row
+// partial sums in registers).  Consecutive threads hold consecutive finely
+// sorted points, so the shared-memory gathers of a warp hit a few adjacent
+// cells (near-broadcast, conflict-light).  Output in ORIGINAL point order
+// (spreadinterp.py:453).
+template <typename T, int DIM, int W>
+__global__ void __launch_bounds__(256) k_interp_tile(SpreadArgs<T> a, T *cout, const T *gridp) {
+    using C = typename Cx<T>::type;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C *patch = reinterpret_cast<C *>(smem_raw);
+    __shared__ int s_sub;
+    const int tid = threadIdx.x;
+    const int n1 = a.g.n[0], n2 = a.g.n[1], n3 = a.g.n[2];
+    const int P1 = a.g.bs[0] + W - 1;
+    const int P2 = DIM > 1 ? a.g.bs[1] + W - 1 : 1;
+    const int P3 = DIM > 2 ? a.g.bs[2] + W - 1 : 1;
+    const int ncell = P1 * P2 * P3;
+    const int nsub = *a.nsub;
+    const int nwork = nsub * a.ntransf;
+    for (;;) {
+        if (tid == 0) s_sub = atomicAdd(a.work, 1);
+        __syncthreads();
+        const int s = s_sub;
+        if (s >= nwork) break;
+        const int t = s / nsub;
+        const int4 sp = a.subprob[s - t * nsub];
+        const int bin = sp.x, start = sp.y, cnt = sp.z;
+        const int b1 = bin % a.g.nb[0];
+        const int b2 = DIM > 1 ? (bin / a.g.nb[0]) % a.g.nb[1] : 0;
+        const int b3 = DIM > 2 ? bin / (a.g.nb[0] * a.g.nb[1]) : 0;
+        const int lo1 = b1 * a.g.bs[0], lo2 = b2 * a.g.bs[1], lo3 = b3 * a.g.bs[2];
+        const C *grid = reinterpret_cast<const C *>(gridp) + (int64_t)t * a.gstride;
+        for (int i = tid; i < ncell; i += blockDim.x) {
+            const int q1 = i % P1;
+            const int r = i / P1;
+            const int q2 = DIM > 1 ? r % P2 : 0;
+            const int q3 = DIM > 2 ? r / P2 : 0;
+            int g1 = lo1 + q1;
+            while (g1 >= n1) g1 -= n1;
+            int64_t gi = g1;
+            if (DIM > 1) {
+                int g2 = lo2 + q2;
+                while (g2 >= n2) g2 -= n2;
+                gi += (int64_t)g2 * n1;
+            }
+            if (DIM > 2) {
+                int g3 = lo3 + q3;
+                while (g3 >= n3) g3 -= n3;
+                gi += (int64_t)g3 * n2 * n1;
+            }
+            patch[i] = __ldg(grid + gi);
+        }
+        __syncthreads();
+        for (int k = tid; k < cnt; k += blockDim.x) {
+            const Rec rc = load_rec(a.rec, start + k);
+            T r1[W], r2[W], r3[W];
+            int i1 = kernel_row<T, W>(rc.g[0], a.k, r1);
+            const int o1 = (i1 < 0 ? i1 + n1 : i1) - lo1;
+            int o2 = 0, o3 = 0;
+            if (DIM > 1) {
+                const int i2 = kernel_row<T, W>(rc.g[1], a.k, r2);
+                o2 = (i2 < 0 ? i2 + n2 : i2) - lo2;
+            }
+            if (DIM > 2) {
+                const int i3 = kernel_row<T, W>(rc.g[2], a.k, r3);
+                o3 = (i3 < 0 ? i3 + n3 : i3) - lo3;
+            }
+            T are = 0, aim = 0;
+            if (DIM == 1) {
+#pragma unroll
+                for (int m1 = 0; m1 < W; ++m1) {
+                    const C v = patch[o1 + m1];
+                    are = fma(r1[m1], v.x, are);
+                    aim = fma(r1[m1], v.y, aim);
+                }
+            } else if (DIM == 2) {
+                const C *base = patch + o2 * P1 + o1;
+#pragma unroll
+                for (int m2 = 0; m2 < W; ++m2) {
+                    T pre = 0, pim = 0;
+#pragma unroll
+                    for (int m1 = 0; m1 < W; ++m1) {
+                        const C v = base[m2 * P1 + m1];
+                        pre = fma(r1[m1], v.x, pre);
+                        pim = fma(r1[m1], v.y, pim);
+                    }
+                    are = fma(r2[m2], pre, are);
+                    aim = fma(r2[m2], pim, aim);
+                }
+            } else {
+                const C *base = patch + (o3 * P2 + o2) * P1 + o1;
+#pragma unroll
+                for (int m3 = 0; m3 < W; ++m3) {
+                    T p3re = 0, p3im = 0;
+#pragma unroll
+                    for (int m2 = 0; m2 < W; ++m2) {
+                        T pre = 0, pim = 0;
+#pragma unroll
+                        for (int m1 = 0; m1 < W; ++m1) {
+                            const C v = base[(m3 * P2 + m2) * P1 + m1];
+                            pre = fma(r1[m1], v.x, pre);
+                            pim = fma(r1[m1], v.y, pim);
+                        }
+                        p3re = fma(r2[m2], pre, p3re);
+                        p3im = fma(r2[m2], pim, p3im);
+                    }
+                    are = fma(r3[m3], p3re, are);
+                    aim = fma(r3[m3], p3im, aim);
+                }
+            }
+            reinterpret_cast<C *>(cout)[(int64_t)t * a.M + rc.j] = C{are, aim};
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Thread-per-point interpolator (spreadinterp.py:442-507) over the finely
+// sorted records: the 32 lanes of a warp hold 32 consecutive points of the
+// same few sub-cells, so each of the w^d gathers is a near-broadcast of a
+// few cache lines; separable weighted sum in registers (w^(d-1) row partial
+// sums), output in ORIGINAL point order (spreadinterp.py:453).
+template <typename T, int DIM, int W>
+__global__ void __launch_bounds__(256, 3) k_interp_thread(SpreadArgs<T> a, T *cout, const T *gridp) {
+    using C = typename Cx<T>::type;
+    const int n1 = a.g.n[0], n2 = a.g.n[1], n3 = a.g.n[2];
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < a.M;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const Rec rc = load_rec(a.rec, k);
+        T r1[W], r2[W], r3[W];
+        int ix1[W];
+        const int i1 = kernel_row<T, W>(rc.g[0], a.k, r1);
+#pragma unroll
+        for (int m = 0; m < W; ++m) ix1[m] = wrap_once(i1 + m, n1);
+        int i2 = 0, i3 = 0;
+        if (DIM > 1) i2 = kernel_row<T, W>(rc.g[1], a.k, r2);
+        if (DIM > 2) i3 = kernel_row<T, W>(rc.g[2], a.k, r3);
+        for (int t = 0; t < a.ntransf; ++t) {
+            const C *grid = reinterpret_cast<const C *>(gridp) + (int64_t)t * a.gstride;
+            T are = 0, aim = 0;
+            if (DIM == 1) {
+#pragma unroll
+                for (int m1 = 0; m1 < W; ++m1) {
+                    const C v = __ldg(grid + ix1[m1]);
+                    are = fma(r1[m1], v.x, are);
+                    aim = fma(r1[m1], v.y, aim);
+                }
+            } else if (DIM == 2) {
+#pragma unroll
+                for (int m2 = 0; m2 < W; ++m2) {
+                    const C *row = grid + (int64_t)wrap_once(i2 + m2, n2) * n1;
+                    T pre = 0, pim = 0;
+#pragma unroll
+                    for (int m1 = 0; m1 < W; ++m1) {
+                        const C v = __ldg(row + ix1[m1]);
+                        pre = fma(r1[m1], v.x, pre);
+                        pim = fma(r1[m1], v.y, pim);
+                    }
+                    are = fma(r2[m2], pre, are);
+                    aim = fma(r2[m2], pim, aim);
+                }
+            } else {
+#pragma unroll 1
+                for (int m3 = 0; m3 < W; ++m3) {
+                    const C *plane = grid + (int64_t)wrap_once(i3 + m3, n3) * n2 * n1;
+                    T p3re = 0, p3im = 0;
+#pragma unroll
+                    for (int m2 = 0; m2 < W; ++m2) {
+                        const C *row = plane + (int64_t)wrap_once(i2 + m2, n2) * n1;
+                        T pre = 0, pim = 0;
+#pragma unroll
+                        for (int m1 = 0; m1 < W; ++m1) {
+                            const C v = __ldg(row + ix1[m1]);
+                            pre = fma(r1[m1], v.x, pre);
+                            pim = fma(r1[m1], v.y, pim);
+                        }
+                        p3re = fma(r2[m2], pre, p3re);
+                        p3im = fma(r2[m2], pim, p3im);
+                    }
+                    // r3 is indexed by the runtime m3: select from registers
+                    T w3 = r3[0];
+#pragma unroll
+                    for (int q = 1; q < W; ++q) w3 = (q == m3) ? r3[q] : w3;
+                    are = fma(w3, p3re, are);
+                    aim = fma(w3, p3im, aim);
+                }
+            }
+            reinterpret_cast<C *>(cout)[(int64_t)t * a.M + rc.j] = C{are, aim};
         }
     }
 }

@@ -2,6 +2,9 @@
 // and esn_inst_f32.cu so the two precisions compile in parallel).
 #pragma once
 
+#include <cstdlib>
+#include <string>
+
 #include "esn_device.cuh"
 
 namespace esn {
@@ -44,7 +47,8 @@ struct SpreadRowsOp {
         if (D == 1) return SpreadGlobalOp<T, D, W>::run(a, st);
         using Cfg = RowsCfg<T, (D < 2 ? 2 : D), W>;
         using C = typename Cx<T>::type;
-        const size_t stage = Cfg::CH * sizeof(C) + Cfg::CH * 3 * W * sizeof(T) + Cfg::CH * 4 * sizeof(int) +
+        constexpr int NZ = D == 3 ? W : 1;
+        const size_t stage = Cfg::CH * NZ * sizeof(C) + Cfg::CH * 2 * W * sizeof(T) + Cfg::CH * 4 * sizeof(int) +
                              (Cfg::NT / 32) * Cfg::CH;
         const size_t tile = (size_t)Cfg::RY * Cfg::RZ * Cfg::X * sizeof(C);
         const size_t smem = stage > tile ? stage : tile;
@@ -61,18 +65,23 @@ struct SpreadRowsOp {
 
 template <typename T, int D, int W>
 struct SpreadBatchOp {
-    static int run(const SpreadArgs<T> &a, cudaStream_t st) {
+    static int run(const SpreadArgs<T> &a, const int *key, const int *rank, const int *kstart, T *cperm,
+                   cudaStream_t st) {
         if (a.M == 0) return ESN_SUCCESS;
         if constexpr (D == 2 && sizeof(T) == 4 && W <= 10) {
             using Cfg = Batch2Cfg<T, W>;
-            using C = typename Cx<T>::type;
-            const size_t smem = Cfg::CH * 32 * sizeof(C) + Cfg::CH * 2 * W * sizeof(T) + Cfg::CH * 3 * sizeof(int);
+            const int ngroups = (a.ntransf + 31) / 32;
+            int64_t pb = ((a.M + 31) / 32) * ngroups;
+            if (pb > (int64_t)device_sm_count() * 16) pb = (int64_t)device_sm_count() * 16;
+            k_permute_strengths<T><<<(int)pb, 1024, 0, st>>>(a, key, rank, kstart, cperm);
+            ESN_CUDA_TRY(cudaGetLastError());
+            const size_t smem = Cfg::CH * 2 * W * sizeof(T) + Cfg::CH * 2 * sizeof(int);
             static int grid = 0;
             if (grid == 0) {
                 int rc = persistent_launch(k_spread_batch2d<T, W>, Cfg::NT, smem, st, nullptr, &grid);
                 if (rc) return rc;
             }
-            k_spread_batch2d<T, W><<<grid, Cfg::NT, smem, st>>>(a);
+            k_spread_batch2d<T, W><<<grid, Cfg::NT, smem, st>>>(a, cperm);
             ESN_CUDA_TRY(cudaGetLastError());
             return ESN_SUCCESS;
         } else {
@@ -85,24 +94,44 @@ template <typename T, int D, int W>
 struct InterpOp {
     static int run(const SpreadArgs<T> &a, T *cout, const T *grid, cudaStream_t st) {
         if (a.M == 0) return ESN_SUCCESS;
-        // contiguous chunks of the sorted order per CTA (L1 reuse of a bin's patch)
-        const int chunk = 1024;
-        int64_t blocks = (a.M + chunk - 1) / chunk;
-        const int64_t cap = (int64_t)device_sm_count() * 8;
-        if (blocks > cap) blocks = cap;
-        k_interp_group<T, D, W><<<(int)blocks, 256, 0, st>>>(a, cout, grid, chunk);
+        static const char *mode = getenv("ESN_INTERP");
+        if (mode && std::string(mode) == "thread") {
+            k_interp_thread<T, D, W><<<grid_for(a.M, 256), 256, 0, st>>>(a, cout, grid);
+            ESN_CUDA_TRY(cudaGetLastError());
+            return ESN_SUCCESS;
+        }
+        using C = typename Cx<T>::type;
+        size_t cells = 1;
+        for (int d = 0; d < D; ++d) cells *= (size_t)(a.g.bs[d] + W - 1);
+        const size_t smem = cells * sizeof(C);
+        if (smem > 200 * 1024) {  // patch too large for shared memory: L1 path
+            k_interp_thread<T, D, W><<<grid_for(a.M, 256), 256, 0, st>>>(a, cout, grid);
+            ESN_CUDA_TRY(cudaGetLastError());
+            return ESN_SUCCESS;
+        }
+        static size_t configured = 0;
+        if (smem > configured) {
+            ESN_CUDA_TRY(cudaFuncSetAttribute(k_interp_tile<T, D, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)smem));
+            configured = smem;
+        }
+        int occ = 0;
+        ESN_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_interp_tile<T, D, W>, 256, smem));
+        if (occ < 1) occ = 1;
+        k_interp_tile<T, D, W><<<device_sm_count() * occ, 256, smem, st>>>(a, cout, grid);
         ESN_CUDA_TRY(cudaGetLastError());
         return ESN_SUCCESS;
     }
 };
 
 template <>
-int launch_spread<ESN_T>(const SpreadArgs<ESN_T> &a, int method, int nbins, cudaStream_t st) {
+int launch_spread<ESN_T>(const SpreadArgs<ESN_T> &a, int method, int nbins, const int *key, const int *rank,
+                         const int *kstart, ESN_T *cperm, cudaStream_t st) {
     (void)nbins;
     if (method == ESN_METHOD_GLOBAL || a.g.dim == 1)
         return dispatch_dw<ESN_T, SpreadGlobalOp>(a.g.dim, a.g.w, a, st);
-    if (a.ntransf > 1 && a.g.dim == 2 && sizeof(ESN_T) == 4 && a.g.w <= 10)
-        return dispatch_dw<ESN_T, SpreadBatchOp>(a.g.dim, a.g.w, a, st);
+    if (batched_spread(sizeof(ESN_T) == 8 ? ESN_F64 : ESN_F32, a.g.dim, a.g.w, a.ntransf, method))
+        return dispatch_dw<ESN_T, SpreadBatchOp>(a.g.dim, a.g.w, a, key, rank, kstart, cperm, st);
     return dispatch_dw<ESN_T, SpreadRowsOp>(a.g.dim, a.g.w, a, st);
 }
 

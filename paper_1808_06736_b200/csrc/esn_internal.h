@@ -60,14 +60,21 @@ struct alignas(32) Rec {
 
 struct SetptsArgs {
     Geom g;
+    int sbl[3];             // log2 of the sub-bin size per dim (fine sort key)
+    int spb;                // sub-bins per bin
+    int nkeys;              // nbins * spb
+    double inv_bs[3];       // 1 / bs (fast division, corrected exactly)
     int64_t M;
     int coord_f32;          // input coordinates are float (else double)
     int grid_units;         // coordinates already in grid units [0, n) (no fold)
     const void *x[3];
     double scale[3];        // n_d / (2 pi), computed on the host (grid.py:167)
-    int *bin_count;         // nbins (zeroed before)
+    int *key_count;         // nkeys (zeroed before)
+    int *cursor;            // nkeys: exclusive scan of key_count (key start)
+    int *key;               // M: fine key of each point (original order)
+    int *rank;              // M: rank of the point inside its key
     int *bin_start;         // nbins + 1
-    int *cursor;            // nbins: running insert position (scatter pass)
+    int *block_sums;        // scan scratch
     Rec *rec;               // M sorted records
     unsigned long long *flags;  // [0..2] first non-finite per dim, [3..5] first |x|>3pi
     int check_bounds;
@@ -100,7 +107,7 @@ struct RowsCfg {
     static constexpr int NT = RY * RZ;
     static constexpr int BY = RY - W + 1;
     static constexpr int BZ = DIM == 3 ? RZ - W + 1 : 1;
-    static constexpr int CH = 64;  // staged points per chunk
+    static constexpr int CH = NT;  // staged points per chunk (one per thread)
     static constexpr int MINB = (sizeof(T) == 8 && DIM == 3) ? 2 : 1;
 };
 
@@ -115,15 +122,19 @@ struct Batch2Cfg {
 };
 
 // ---- launchers (esn_kernels.cu)
-int launch_setpts(const SetptsArgs &a, int dtype, int nbins, int max_subprob, int4 *subprob,
-                  int *nsub, int *scan_aux, cudaStream_t st);
+int launch_setpts(const SetptsArgs &a, int nbins, int max_subprob, int4 *subprob, int *nsub, int *subofs,
+                  cudaStream_t st);
+constexpr int kScanTile = 4096;  // keys per scan block
 int launch_sort_view(int dtype, const void *rec, const int *bin_start, int nbins, int64_t M, int *perm,
                      int *keys, cudaStream_t st);
 // Bin geometry the chosen spreader needs: (bx, by, bz); returns 0 if the
 // method has no fixed geometry (global atomics).
 int spreader_bins(int method, int dtype, int dim, int w, int ntransf, int *bs);
 template <typename T>
-int launch_spread(const SpreadArgs<T> &a, int method, int nbins, cudaStream_t st);
+int launch_spread(const SpreadArgs<T> &a, int method, int nbins, const int *key, const int *rank,
+                  const int *kstart, T *cperm, cudaStream_t st);
+// does the batched 2D path (needs a permuted-strength scratch) apply?
+bool batched_spread(int dtype, int dim, int w, int ntransf, int method);
 template <typename T>
 int launch_interp(const SpreadArgs<T> &a, T *cout, const T *grid, cudaStream_t st);
 template <typename T>

@@ -96,8 +96,12 @@ struct esn_plan_s {
     // device state
     void *pk[3] = {nullptr, nullptr, nullptr};
     Rec *rec = nullptr;  // sorted point records
-    int *cursor = nullptr;
-    int *bin_count = nullptr, *bin_start = nullptr, *subofs = nullptr, *nsub = nullptr, *work = nullptr;
+    int *pkey = nullptr, *prank = nullptr;  // per-point key / rank (setpts scratch)
+    void *cperm = nullptr;                  // batched strengths in sorted order
+    int64_t cperm_bytes = 0;
+    int *cursor = nullptr, *key_count = nullptr, *block_sums = nullptr;
+    int *bin_start = nullptr, *subofs = nullptr, *nsub = nullptr, *work = nullptr;
+    int sbl[3] = {0, 0, 0}, spb = 1, nkeys = 1;
     int4 *subprob = nullptr;
     unsigned long long *flags = nullptr;
     void *grid = nullptr;
@@ -133,7 +137,7 @@ static void rows_bins(int dtype, int dim, int ntransf, int *bs) {
         } else {
             bs[0] = RowsCfg<float, 3, W>::BX; bs[1] = RowsCfg<float, 3, W>::BY; bs[2] = RowsCfg<float, 3, W>::BZ;
         }
-    } else if (dtype == ESN_F32 && ntransf > 1 && W <= 10) {
+    } else if (esn::batched_spread(dtype, dim, W, ntransf, ESN_METHOD_TILE)) {
         bs[0] = Batch2Cfg<float, W>::BX; bs[1] = Batch2Cfg<float, W>::BY; bs[2] = 1;
     } else if (dtype == ESN_F64) {
         bs[0] = RowsCfg<double, 2, W>::BX; bs[1] = RowsCfg<double, 2, W>::BY; bs[2] = 1;
@@ -157,7 +161,30 @@ int esn::spreader_bins(int method, int dtype, int dim, int w, int ntransf, int *
 static void choose_bins(esn_plan p) {
     const int dim = p->dim, w = p->kp.w;
     int bs[3] = {1, 1, 1};
-    if (!esn::spreader_bins(p->method, p->dtype, dim, w, p->ntransf, bs)) {
+    if (p->type == 2 && dim > 1) {
+        // interpolation-only plan: bins sized for the shared-memory patch
+        const size_t cb = p->dtype == ESN_F64 ? 16 : 8;
+        if (dim == 2) {
+            bs[0] = 32;
+            bs[1] = 32;
+        } else {
+            bs[0] = 16;
+            bs[1] = 8;
+            bs[2] = 8;
+        }
+        auto patch = [&]() {
+            size_t c = cb;
+            for (int d = 0; d < dim; ++d) c *= (size_t)(bs[d] + w - 1);
+            return c;
+        };
+        while (patch() > 96 * 1024) {
+            int big = 0;
+            for (int d = 1; d < dim; ++d)
+                if (bs[d] > bs[big]) big = d;
+            if (bs[big] <= 2) break;
+            bs[big] /= 2;
+        }
+    } else if (!esn::spreader_bins(p->method, p->dtype, dim, w, p->ntransf, bs)) {
         // global-atomic spreader / 1D: bins only order the points for locality
         if (dim == 1) {
             bs[0] = 1024;
@@ -178,6 +205,28 @@ static void choose_bins(esn_plan p) {
     }
     p->geom.dim = dim;
     p->geom.w = w;
+    // fine sort key: sub-cells of 2^sbl cells inside each bin, coarsened
+    // (fastest dims first) until the key space is <= 8M entries
+    for (int d = 0; d < 3; ++d) p->sbl[d] = 0;
+    auto keys = [&]() {
+        int64_t k = p->nbins;
+        for (int d = 0; d < dim; ++d) k *= (p->geom.bs[d] >> p->sbl[d]);
+        return k;
+    };
+    for (int guard = 0; guard < 64 && keys() > (int64_t)8 << 20; ++guard) {
+        bool grew = false;
+        for (int d = 0; d < dim && keys() > (int64_t)8 << 20; ++d) {
+            const int s2 = 1 << (p->sbl[d] + 1);
+            if (p->geom.bs[d] % s2 == 0) {
+                p->sbl[d]++;
+                grew = true;
+            }
+        }
+        if (!grew) break;
+    }
+    p->spb = 1;
+    for (int d = 0; d < dim; ++d) p->spb *= p->geom.bs[d] >> p->sbl[d];
+    p->nkeys = (int)keys();
 }
 
 static int plan_common_init(esn_plan p, const esn_opts *o) {
@@ -208,9 +257,10 @@ static int plan_common_init(esn_plan p, const esn_opts *o) {
     choose_bins(p);
     p->maxsub = p->opts.max_subprob > 0 ? p->opts.max_subprob : 8192;
     int rc;
-    if ((rc = dmalloc(p, &p->bin_count, sizeof(int) * p->nbins))) return rc;
+    if ((rc = dmalloc(p, &p->key_count, sizeof(int) * p->nkeys))) return rc;
+    if ((rc = dmalloc(p, &p->cursor, sizeof(int) * p->nkeys))) return rc;
+    if ((rc = dmalloc(p, &p->block_sums, sizeof(int) * ((p->nkeys + kScanTile - 1) / kScanTile + 1)))) return rc;
     if ((rc = dmalloc(p, &p->bin_start, sizeof(int) * (p->nbins + 1)))) return rc;
-    if ((rc = dmalloc(p, &p->cursor, sizeof(int) * (p->nbins + 1)))) return rc;
     if ((rc = dmalloc(p, &p->subofs, sizeof(int) * (p->nbins + 1)))) return rc;
     if ((rc = dmalloc(p, &p->nsub, sizeof(int) * 2))) return rc;
     if ((rc = dmalloc(p, &p->work, sizeof(int) * 2))) return rc;
@@ -299,8 +349,12 @@ int esn_plan_destroy(esn_plan p) {
     else cudaDeviceSynchronize();
     for (int d = 0; d < 3; ++d) dfree(p->pk[d]);
     dfree(p->rec);
+    dfree(p->pkey);
+    dfree(p->prank);
+    dfree(p->cperm);
     dfree(p->cursor);
-    dfree(p->bin_count);
+    dfree(p->key_count);
+    dfree(p->block_sums);
     dfree(p->bin_start);
     dfree(p->subofs);
     dfree(p->nsub);
@@ -391,9 +445,13 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
     int rc;
     if (M > p->Mcap) {
         dfree(p->rec);
+        dfree(p->pkey);
+        dfree(p->prank);
         p->rec = nullptr;
-        if ((rc = dmalloc(p, &p->rec, sizeof(Rec) * M)))
-            return rc;
+        p->pkey = p->prank = nullptr;
+        if ((rc = dmalloc(p, &p->rec, sizeof(Rec) * M))) return rc;
+        if ((rc = dmalloc(p, &p->pkey, sizeof(int) * M))) return rc;
+        if ((rc = dmalloc(p, &p->prank, sizeof(int) * M))) return rc;
         p->Mcap = M;
     }
     const int64_t subneed = p->nbins + M / p->maxsub + 1;
@@ -405,7 +463,7 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
     }
     p->M = M;
     if (p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[0], p->st));
-    ESN_CUDA_TRY(cudaMemsetAsync(p->bin_count, 0, sizeof(int) * p->nbins, p->st));
+    ESN_CUDA_TRY(cudaMemsetAsync(p->key_count, 0, sizeof(int) * p->nkeys, p->st));
     ESN_CUDA_TRY(cudaMemsetAsync(p->flags, 0xff, sizeof(unsigned long long) * 8, p->st));
     SetptsArgs a{};
     a.g = p->geom;
@@ -416,13 +474,22 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
         a.x[d] = d < p->dim ? xs[d] : nullptr;
         a.scale[d] = (double)p->n[d] / (2.0 * M_PI);  // sizes[d] / TWO_PI (spreadinterp.py:99)
     }
-    a.bin_count = p->bin_count;
+    for (int d = 0; d < 3; ++d) {
+        a.sbl[d] = p->sbl[d];
+        a.inv_bs[d] = 1.0 / (double)p->geom.bs[d];
+    }
+    a.spb = p->spb;
+    a.nkeys = p->nkeys;
+    a.key_count = p->key_count;
+    a.block_sums = p->block_sums;
     a.bin_start = p->bin_start;
     a.cursor = p->cursor;
+    a.key = p->pkey;
+    a.rank = p->prank;
     a.rec = p->rec;
     a.flags = p->flags;
     a.check_bounds = p->opts.check_bounds;
-    if ((rc = launch_setpts(a, p->dtype, p->nbins, p->maxsub, p->subprob, p->nsub, p->subofs, p->st))) return rc;
+    if ((rc = launch_setpts(a, p->nbins, p->maxsub, p->subprob, p->nsub, p->subofs, p->st))) return rc;
     if (p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[1], p->st));
     p->points_set = true;
     return ESN_SUCCESS;
@@ -452,18 +519,35 @@ static SpreadArgs<T> make_spread_args(esn_plan p, const void *c, void *grid) {
     return a;
 }
 
+bool esn::batched_spread(int dtype, int dim, int w, int ntransf, int method) {
+    return method != ESN_METHOD_GLOBAL && dim == 2 && dtype == ESN_F32 && ntransf > 1 && w <= 10;
+}
+
 static int do_spread(esn_plan p, const void *c, void *grid) {
+    if (esn::batched_spread(p->dtype, p->dim, p->kp.w, p->ntransf, p->method)) {
+        const int64_t need = (int64_t)((p->ntransf + 31) / 32) * 32 * p->M * (int64_t)real_size(p->dtype) * 2;
+        if (need > p->cperm_bytes) {
+            dfree(p->cperm);
+            p->cperm = nullptr;
+            int rc = dmalloc(p, &p->cperm, (size_t)need);
+            if (rc) return rc;
+            p->cperm_bytes = need;
+        }
+    }
     ESN_CUDA_TRY(cudaMemsetAsync(grid, 0, real_size(p->dtype) * 2 * (size_t)p->G * p->ntransf, p->st));
     ESN_CUDA_TRY(cudaMemsetAsync(p->work, 0, sizeof(int), p->st));
     if (p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[6], p->st));
     int rc = p->dtype == ESN_F64
-                 ? launch_spread<double>(make_spread_args<double>(p, c, grid), p->method, p->nbins, p->st)
-                 : launch_spread<float>(make_spread_args<float>(p, c, grid), p->method, p->nbins, p->st);
+                 ? launch_spread<double>(make_spread_args<double>(p, c, grid), p->method, p->nbins, p->pkey,
+                                         p->prank, p->cursor, (double *)p->cperm, p->st)
+                 : launch_spread<float>(make_spread_args<float>(p, c, grid), p->method, p->nbins, p->pkey,
+                                        p->prank, p->cursor, (float *)p->cperm, p->st);
     if (!rc && p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[7], p->st));
     return rc;
 }
 
 static int do_interp(esn_plan p, const void *grid, void *c) {
+    ESN_CUDA_TRY(cudaMemsetAsync(p->work, 0, sizeof(int), p->st));
     if (p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[6], p->st));
     int rc = p->dtype == ESN_F64
                  ? launch_interp<double>(make_spread_args<double>(p, nullptr, nullptr), (double *)c,

@@ -1,7 +1,7 @@
-// esn_setpts.cu -- point preparation on sm_100a: fold + grid scale + bin key
-// (fused with the finite / bounds checks), bin counting sort (warp-aggregated
-// atomic histogram -> single-CTA exclusive scan -> scatter of the permutation
-// and of the sorted grid coordinates), and the subproblem table.
+// esn_setpts.cu -- point preparation on sm_100a: fold + grid scale + sort key
+// (fused with the finite / bounds checks), counting sort over fine keys
+// (RED histogram -> 3-phase exclusive scan -> atomic-cursor scatter of one
+// 256-bit record per point), and the subproblem table of the spreader.
 //
 // Replaces build_point_set / fold_coords / bin_sort / ensure_sorted /
 // partition_subproblems (spreadinterp.py:79-150, grid.py:152-254).  The
@@ -53,10 +53,12 @@ int device_sm_count() {
 
 // grid.py:152-168 + spreadinterp.py:99-100 in float64: np.mod(x, 2 pi)
 // (fmod plus 2 pi when the signs differ), exact 2 pi wraps to 0, scale by
-// n / 2 pi (host-computed), pull back g >= n.  Bit-identical to numpy.
+// n / 2 pi (host-computed), pull back g >= n.  Bit-identical to numpy; fmod
+// is skipped when |x| < 2 pi, where it is the identity.
 __device__ __forceinline__ double fold_scale(double x, double n, double scale) {
     const double two_pi = 6.283185307179586;
-    double r = fmod(x, two_pi);
+    double r = x;
+    if (!(fabs(x) < two_pi)) r = fmod(x, two_pi);
     if (r < 0.0) r += two_pi;
     if (r >= two_pi) r = 0.0;
     double g = r * scale;
@@ -64,16 +66,17 @@ __device__ __forceinline__ double fold_scale(double x, double n, double scale) {
     return g;
 }
 
-template <typename T>
-__device__ __forceinline__ T to_plan(double g, int n) {
-    T v = (T)g;
-    if (v >= (T)n) v -= (T)n;  // float rounding can land exactly on n
-    return v;
+// exact q = i / d for 0 <= i < 2^31 via a float64 reciprocal and one fix-up
+__device__ __forceinline__ int fast_div(int i, int d, double inv) {
+    int q = __double2int_rz((double)i * inv);
+    if (q * d > i) --q;
+    else if ((q + 1) * d <= i) ++q;
+    return q;
 }
 
-template <typename T>
+// Fine sort key of one point; g receives its grid coordinates.
 __device__ __forceinline__ int point_key(const SetptsArgs &a, int64_t i, const double *xin, double *gout, bool check) {
-    int key = 0, mul = 1;
+    int bin = 0, loc = 0, bmul = 1, lmul = 1;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
         if (d >= a.g.dim) break;
@@ -95,10 +98,14 @@ __device__ __forceinline__ int point_key(const SetptsArgs &a, int64_t i, const d
         gout[d] = g;
         int i0 = (int)floor(g - 0.5 * a.g.w + 1.0);  // spreadinterp.py:117-120
         if (i0 < 0) i0 += a.g.n[d];
-        key += (i0 / a.g.bs[d]) * mul;
-        mul *= a.g.nb[d];
+        const int bs = a.g.bs[d];
+        const int q = fast_div(i0, bs, a.inv_bs[d]);
+        bin += q * bmul;
+        bmul *= a.g.nb[d];
+        loc += ((i0 - q * bs) >> a.sbl[d]) * lmul;
+        lmul *= bs >> a.sbl[d];
     }
-    return key;
+    return bin * a.spb + loc;
 }
 
 constexpr int kILP = 4;  // points in flight per thread (independent loads / atomics)
@@ -117,130 +124,184 @@ __device__ __forceinline__ void load_coords(const SetptsArgs &a, int64_t base, d
     }
 }
 
-// Pass 1: bin histogram (fire-and-forget REDs, no return value needed) and
-// the finite / bounds flags.
-template <typename XT, typename T>
-__global__ void __launch_bounds__(256) k_setpts_count(SetptsArgs a) {
+// Pass 1: key histogram with ranks (atomic with return: the old count is the
+// point's rank inside its key) plus the finite / bounds flags.  Stores key
+// and rank (two coalesced 4-byte writes) so the scatter pass needs no atomics.
+template <typename XT>
+__global__ void __launch_bounds__(256, 4) k_setpts_count(SetptsArgs a) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * kILP;
     for (int64_t base = (int64_t)blockIdx.x * blockDim.x * kILP + threadIdx.x; base < a.M; base += stride) {
         double x[kILP][3];
         load_coords<XT>(a, base, x);
+        int key[kILP], rank[kILP];
 #pragma unroll
         for (int u = 0; u < kILP; ++u) {
             const int64_t i = base + (int64_t)u * blockDim.x;
-            if (i >= a.M) continue;
             double g[3];
-            atomicAdd(&a.bin_count[point_key<T>(a, i, x[u], g, true)], 1);
+            key[u] = i < a.M ? point_key(a, i, x[u], g, true) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < kILP; ++u) rank[u] = key[u] >= 0 ? atomicAdd(&a.key_count[key[u]], 1) : 0;
+#pragma unroll
+        for (int u = 0; u < kILP; ++u) {
+            const int64_t i = base + (int64_t)u * blockDim.x;
+            if (i < a.M) {
+                a.key[i] = key[u];
+                a.rank[i] = rank[u];
+            }
         }
     }
 }
 
-// Pass 2: claim a slot in the point's bin (atomic on the bin cursor) and
-// write its full record {g, j} there with one 256-bit store.
-template <typename XT, typename T>
+// Pass 2: pos = start[key] + rank; write the point's full record {g, j}
+// with one 256-bit store (a whole L2 sector).  No atomics.
+template <typename XT>
 __global__ void __launch_bounds__(256) k_setpts_scatter(SetptsArgs a) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * kILP;
     for (int64_t base = (int64_t)blockIdx.x * blockDim.x * kILP + threadIdx.x; base < a.M; base += stride) {
         double x[kILP][3];
         load_coords<XT>(a, base, x);
-        int pos[kILP];
+        int key[kILP], rank[kILP];
 #pragma unroll
         for (int u = 0; u < kILP; ++u) {
             const int64_t i = base + (int64_t)u * blockDim.x;
-            double g[3];
-            pos[u] = i < a.M ? atomicAdd(&a.cursor[point_key<T>(a, i, x[u], g, false)], 1) : -1;
-            x[u][0] = g[0];
-            x[u][1] = a.g.dim > 1 ? g[1] : 0.0;
-            x[u][2] = a.g.dim > 2 ? g[2] : 0.0;
+            key[u] = i < a.M ? __ldg(a.key + i) : -1;
+            rank[u] = i < a.M ? __ldg(a.rank + i) : 0;
         }
 #pragma unroll
         for (int u = 0; u < kILP; ++u) {
-            if (pos[u] < 0) continue;
-            const unsigned long long j = (unsigned long long)(unsigned)(base + (int64_t)u * blockDim.x);
-            asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(a.rec + pos[u]),
-                         "l"(__double_as_longlong(x[u][0])), "l"(__double_as_longlong(x[u][1])),
-                         "l"(__double_as_longlong(x[u][2])), "l"(j)
+            if (key[u] < 0) continue;
+            const int64_t i = base + (int64_t)u * blockDim.x;
+            double g[3] = {0.0, 0.0, 0.0};
+            point_key(a, i, x[u], g, false);
+            const int pos = __ldg(a.cursor + key[u]) + rank[u];
+            const unsigned long long j = (unsigned long long)(unsigned)i;
+            asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(a.rec + pos),
+                         "l"(__double_as_longlong(g[0])), "l"(__double_as_longlong(g[1])),
+                         "l"(__double_as_longlong(g[2])), "l"(j)
                          : "memory");
         }
     }
 }
 
-// Single-CTA exclusive scan of the bin counts and of the per-bin subproblem
-// counts ceil(count / max_subprob); also publishes the subproblem total.
-__global__ void __launch_bounds__(1024) k_scan_bins(const int *count, int *start, int *cursor, int *subofs,
-                                                    int nbins, int maxsub, int *nsub_total) {
-    __shared__ int wsum[2][32];
-    __shared__ int carry[2];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) carry[0] = carry[1] = 0;
+// ---- exclusive scan of the key histogram: block reduce -> top scan -> down
+__device__ __forceinline__ int block_scan_excl(int v, int *total, int *wsum) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
     __syncthreads();
-    for (int base = 0; base < nbins; base += 1024) {
-        const int i = base + tid;
-        const int c = i < nbins ? count[i] : 0;
-        const int s = i < nbins ? (c + maxsub - 1) / maxsub : 0;
-        int xc = c, xs = s;
+    if (warp == 0) {
+        int s = lane < nw ? wsum[lane] : 0;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            int yc = __shfl_up_sync(0xffffffffu, xc, o);
-            int ys = __shfl_up_sync(0xffffffffu, xs, o);
-            if (lane >= o) {
-                xc += yc;
-                xs += ys;
-            }
+            const int y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
         }
-        if (lane == 31) {
-            wsum[0][warp] = xc;
-            wsum[1][warp] = xs;
-        }
-        __syncthreads();
-        if (warp == 0) {
-            int vc = wsum[0][lane], vs = wsum[1][lane];
+        if (lane < nw) wsum[lane] = s;
+    }
+    __syncthreads();
+    const int off = warp ? wsum[warp - 1] : 0;
+    *total = wsum[nw - 1];
+    __syncthreads();
+    return off + x - v;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_reduce(const int *cnt, int n, int *block_sums) {
+    __shared__ int wsum[32];
+    const int base = blockIdx.x * kScanTile;
+    int v = 0;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                int yc = __shfl_up_sync(0xffffffffu, vc, o);
-                int ys = __shfl_up_sync(0xffffffffu, vs, o);
-                if (lane >= o) {
-                    vc += yc;
-                    vs += ys;
-                }
-            }
-            wsum[0][lane] = vc;
-            wsum[1][lane] = vs;
-        }
-        __syncthreads();
-        const int offc = carry[0] + (warp ? wsum[0][warp - 1] : 0);
-        const int offs = carry[1] + (warp ? wsum[1][warp - 1] : 0);
-        if (i < nbins) {
-            start[i] = offc + xc - c;
-            cursor[i] = offc + xc - c;
-            subofs[i] = offs + xs - s;
-        }
-        __syncthreads();
-        if (tid == 0) {
-            carry[0] += wsum[0][31];
-            carry[1] += wsum[1][31];
-        }
-        __syncthreads();
+    for (int u = 0; u < kScanTile / 1024; ++u) {
+        const int i = base + u * 1024 + threadIdx.x;
+        if (i < n) v += cnt[i];
     }
-    if (tid == 0) {
-        start[nbins] = carry[0];
-        subofs[nbins] = carry[1];
-        *nsub_total = carry[1];
-    }
+    int total;
+    block_scan_excl(v, &total, wsum);
+    if (threadIdx.x == 0) block_sums[blockIdx.x] = total;
 }
 
-__global__ void k_fill_subprob(const int *count, const int *start, const int *subofs, int nbins, int maxsub,
-                               int4 *table) {
+__global__ void __launch_bounds__(1024) k_scan_top(int *block_sums, int nblocks) {
+    __shared__ int wsum[32];
+    __shared__ int carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int b0 = 0; b0 < nblocks; b0 += 1024) {
+        const int i = b0 + threadIdx.x;
+        const int v = i < nblocks ? block_sums[i] : 0;
+        int total;
+        const int e = block_scan_excl(v, &total, wsum);
+        if (i < nblocks) block_sums[i] = carry + e;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) block_sums[nblocks] = carry;
+}
+
+// writes cursor[k] = exclusive prefix, and bin_start at every bin head
+__global__ void __launch_bounds__(1024) k_scan_down(const int *cnt, int n, const int *block_sums, int *cursor,
+                                                   int *bin_start, int spb, int nbins) {
+    __shared__ int wsum[32];
+    constexpr int U = kScanTile / 1024;
+    const int base = blockIdx.x * kScanTile + threadIdx.x * U;  // each thread owns U consecutive keys
+    int v[U], s = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        v[u] = base + u < n ? cnt[base + u] : 0;
+        s += v[u];
+    }
+    int total;
+    int e = block_scan_excl(s, &total, wsum) + block_sums[blockIdx.x];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int k = base + u;
+        if (k < n) {
+            cursor[k] = e;
+            if (k % spb == 0) bin_start[k / spb] = e;
+        }
+        e += v[u];
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) bin_start[nbins] = block_sums[gridDim.x];
+}
+
+// Subproblem counts per bin (ceil(count / max_subprob)) -> exclusive scan ->
+// total (single CTA over the bins).
+__global__ void __launch_bounds__(1024) k_scan_subprob(const int *bin_start, int nbins, int maxsub, int *subofs,
+                                                      int *nsub_total) {
+    __shared__ int wsum[32];
+    __shared__ int carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int b0 = 0; b0 < nbins; b0 += 1024) {
+        const int b = b0 + threadIdx.x;
+        const int c = b < nbins ? bin_start[b + 1] - bin_start[b] : 0;
+        const int v = (c + maxsub - 1) / maxsub;
+        int total;
+        const int e = block_scan_excl(v, &total, wsum);
+        if (b < nbins) subofs[b] = carry + e;
+        __syncthreads();
+        if (threadIdx.x == 0) carry += total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *nsub_total = carry;
+}
+
+__global__ void k_fill_subprob(const int *bin_start, const int *subofs, int nbins, int maxsub, int4 *table) {
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nbins; b += gridDim.x * blockDim.x) {
-        const int c = count[b];
-        int o = subofs[b];
+        const int c = bin_start[b + 1] - bin_start[b];
+        const int o = subofs[b];
         for (int s = 0; s * maxsub < c; ++s)
-            table[o + s] = make_int4(b, start[b] + s * maxsub, min(maxsub, c - s * maxsub), 0);
+            table[o + s] = make_int4(b, bin_start[b] + s * maxsub, min(maxsub, c - s * maxsub), 0);
     }
 }
 
-template <typename XT, typename T>
-static int setpts_impl(const SetptsArgs &a, int nbins, int maxsub, int4 *subprob, int *nsub, int *scan_aux,
+template <typename XT>
+static int setpts_impl(const SetptsArgs &a, int nbins, int maxsub, int4 *subprob, int *nsub, int *subofs,
                        cudaStream_t st) {
     const int threads = 256;
     int64_t blocks = (a.M + threads * kILP - 1) / (threads * kILP);
@@ -248,19 +309,22 @@ static int setpts_impl(const SetptsArgs &a, int nbins, int maxsub, int4 *subprob
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     if (a.M > 0) {
-        k_setpts_count<XT, T><<<(int)blocks, threads, 0, st>>>(a);
+        k_setpts_count<XT><<<(int)blocks, threads, 0, st>>>(a);
         ESN_CUDA_TRY(cudaGetLastError());
     }
-    k_scan_bins<<<1, 1024, 0, st>>>(a.bin_count, a.bin_start, a.cursor, scan_aux, nbins, maxsub, nsub);
+    const int nsb = (a.nkeys + kScanTile - 1) / kScanTile;
+    k_scan_reduce<<<nsb, 1024, 0, st>>>(a.key_count, a.nkeys, a.block_sums);
+    k_scan_top<<<1, 1024, 0, st>>>(a.block_sums, nsb);
+    k_scan_down<<<nsb, 1024, 0, st>>>(a.key_count, a.nkeys, a.block_sums, a.cursor, a.bin_start, a.spb, nbins);
     ESN_CUDA_TRY(cudaGetLastError());
     if (a.M > 0) {
-        k_setpts_scatter<XT, T><<<(int)blocks, threads, 0, st>>>(a);
-        ESN_CUDA_TRY(cudaGetLastError());
-        int fb = (nbins + 255) / 256;
-        k_fill_subprob<<<fb < 1 ? 1 : fb, 256, 0, st>>>(a.bin_count, a.bin_start, scan_aux, nbins, maxsub,
-                                                         subprob);
+        k_setpts_scatter<XT><<<(int)blocks, threads, 0, st>>>(a);
         ESN_CUDA_TRY(cudaGetLastError());
     }
+    k_scan_subprob<<<1, 1024, 0, st>>>(a.bin_start, nbins, maxsub, subofs, nsub);
+    int fb = (nbins + 255) / 256;
+    k_fill_subprob<<<fb < 1 ? 1 : fb, 256, 0, st>>>(a.bin_start, subofs, nbins, maxsub, subprob);
+    ESN_CUDA_TRY(cudaGetLastError());
     return ESN_SUCCESS;
 }
 
@@ -276,22 +340,18 @@ __global__ void k_sort_view(const Rec *rec, const int *bin_start, int nbins, int
 
 int launch_sort_view(int dtype, const void *rec, const int *bin_start, int nbins, int64_t M, int *perm, int *keys,
                      cudaStream_t st) {
+    (void)dtype;
     if (M == 0) return ESN_SUCCESS;
     int fb = (nbins + 127) / 128;
-    (void)dtype;
     k_sort_view<<<fb, 128, 0, st>>>((const Rec *)rec, bin_start, nbins, perm, keys);
     ESN_CUDA_TRY(cudaGetLastError());
     return ESN_SUCCESS;
 }
 
-int launch_setpts(const SetptsArgs &a, int dtype, int nbins, int max_subprob, int4 *subprob, int *nsub,
-                  int *scan_aux, cudaStream_t st) {
-    if (dtype == ESN_F64) {
-        return a.coord_f32 ? setpts_impl<float, double>(a, nbins, max_subprob, subprob, nsub, scan_aux, st)
-                           : setpts_impl<double, double>(a, nbins, max_subprob, subprob, nsub, scan_aux, st);
-    }
-    return a.coord_f32 ? setpts_impl<float, float>(a, nbins, max_subprob, subprob, nsub, scan_aux, st)
-                       : setpts_impl<double, float>(a, nbins, max_subprob, subprob, nsub, scan_aux, st);
+int launch_setpts(const SetptsArgs &a, int nbins, int max_subprob, int4 *subprob, int *nsub, int *subofs,
+                  cudaStream_t st) {
+    return a.coord_f32 ? setpts_impl<float>(a, nbins, max_subprob, subprob, nsub, subofs, st)
+                       : setpts_impl<double>(a, nbins, max_subprob, subprob, nsub, subofs, st);
 }
 
 }  // namespace esn

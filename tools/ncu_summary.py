@@ -51,6 +51,15 @@ if __name__ == '__main__':
         for k in KEYS:
             if k in h:
                 print(f'   {k:70s} {row[h.index(k)]} {u[h.index(k)]}')
+        items = []
+        for i, name in enumerate(h):
+            if name.startswith('smsp__pcsamp_warps_issue_stalled_') and not name.endswith('not_issued'):
+                try:
+                    items.append((float(row[i]), name.replace('smsp__pcsamp_warps_issue_stalled_', '')))
+                except ValueError:
+                    pass
+        tot = sum(v for v, _ in items) or 1
+        print('   stall reasons:', ', '.join(f'{n} {v / tot:.0%}' for v, n in sorted(items, reverse=True)[:7]))
     if len(sys.argv) > 2:
         for kern in sys.argv[2:]:
             print('-- stalls', kern)
