@@ -210,28 +210,57 @@ def gpu_run(args, rank, world, local_rank):
     name = args.config
     cfg = cases.CONFIGS[name]
     M, T = cfg["M_full"], cfg["ntransf"]
-    # every rank owns an independent shard (its own seed) of the full size
+    # multi-GPU mode: one large type 1 splits its points
+    # (NCCL reduce of the partial modes), a batch splits its transforms
+    # (all-gather of the results); type 2 / 1D run independent replicas
+    mode = "replica"
+    if world > 1 and cfg["ttype"] == 1 and T == 1 and cfg["dim"] == 3:
+        mode = "points"
+    elif world > 1 and T > 1:
+        mode = "transforms"
     coords, data, cfg = cases.make_inputs(name, M=M, ntransf=T)
-    if rank > 0:
+    from paper_1808_06736_b200.distributed import shard_range
+    Mr, Tr = M, T
+    if mode == "points":
+        lo, hi = shard_range(M, rank, world)
+        coords = [x[lo:hi] for x in coords]
+        data = data[lo:hi]
+        Mr = hi - lo
+    elif mode == "transforms":
+        lo, hi = shard_range(T, rank, world)
+        data = data[lo:hi]
+        Tr = hi - lo
+    elif rank > 0:
+        # replicas: every rank owns an independent shard (its own seed)
         rng = np.random.default_rng(cfg["seed"] + 7919 * rank)
         coords = [rng.uniform(cfg["lo"], cfg["hi"], M) for _ in range(cfg["dim"])]
     real = torch.float64 if cfg["dtype"] == "float64" else torch.float32
     cplx = torch.complex128 if cfg["dtype"] == "float64" else torch.complex64
     xs = [torch.from_numpy(x).to(dev, real).contiguous() for x in coords]
-    d = torch.from_numpy(data).to(dev, cplx).contiguous()
-    plan = Plan(cfg["ttype"], cfg["dim"], nmodes=cfg["nm"], isign=cfg["isign"], ntransf=T,
+    d = torch.from_numpy(np.ascontiguousarray(data)).to(dev, cplx).contiguous()
+    plan = Plan(cfg["ttype"], cfg["dim"], nmodes=cfg["nm"], isign=cfg["isign"], ntransf=Tr,
                 tol=cfg["tol"], device=dev, dtype=cfg["dtype"], method=args.method, timing=True)
     if cfg["ttype"] == 1:
-        out = torch.empty((T,) + tuple(reversed(cfg["nm"])), dtype=cplx, device=dev)
+        out = torch.empty(((Tr,) if T > 1 else ()) + tuple(reversed(cfg["nm"])), dtype=cplx, device=dev)
         cin, fout = d, out
     else:
-        out = torch.empty((T, M) if T > 1 else (M,), dtype=cplx, device=dev)
+        out = torch.empty((Tr, Mr) if T > 1 else (Mr,), dtype=cplx, device=dev)
         cin, fout = out, d
     stream = torch.cuda.current_stream(dev)
+    gathered = None
+    if mode == "transforms":
+        width = max(h - l for l, h in (shard_range(T, r, world) for r in range(world)))
+        gathered = [torch.empty((width,) + tuple(out.shape[1:]), dtype=cplx, device=dev) for _ in range(world)]
+        padded = torch.zeros_like(gathered[0])
 
     def step():
         plan.setpts(xs)
         plan.execute(cin, fout)
+        if mode == "points":
+            dist.reduce(torch.view_as_real(out), dst=0, op=dist.ReduceOp.SUM)
+        elif mode == "transforms":
+            padded[: out.shape[0]].copy_(out)
+            dist.all_gather([torch.view_as_real(g) for g in gathered], torch.view_as_real(padded))
 
     for _ in range(max(args.warmup, 0)):
         step()
@@ -267,12 +296,13 @@ def gpu_run(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     elapsed = float(t.item())
     Tn = T if cfg["ttype"] == 1 else 1
-    value = M * Tn * world * args.steps / elapsed
-    B, G = algorithmic_bytes(cfg, M, T)
+    total_units = M * Tn * (world if mode == "replica" else 1)
+    value = total_units * args.steps / elapsed
+    B, G = algorithmic_bytes(cfg, Mr, Tr)
     hot_s = statistics.mean(hot)
     peak, peak_kind = peaks()
     achieved = B / hot_s / 1e9
-    res = dict(value=value, elapsed=elapsed, hot_s=hot_s, achieved=achieved, peak=peak,
+    res = dict(value=value, elapsed=elapsed, hot_s=hot_s, achieved=achieved, peak=peak, mode=mode,
                peak_kind=peak_kind, B=B, G=G, clocks=clk.summary(),
                stages={k: v / args.steps for k, v in stages.items()})
     # e2e through the C ABI with pinned host buffers
@@ -282,6 +312,7 @@ def gpu_run(args, rank, world, local_rank):
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2["value"] = M * (T if cfg["ttype"] == 1 else 1) * world * e2.pop("calls") / float(te.item())
+        e2["note"] = "independent replica per rank" if world > 1 else "1 GPU"
         e2["ms_per_step"] = float(te.item()) / K_E2E * 1e3
         res["e2e"] = e2
     plan.close()
@@ -395,11 +426,18 @@ def main():
                 traffic = None
         kern = "interp" if cfg["ttype"] == 2 else "spread"
         n_launch = 4 + 2  # setpts: bin, scan, scatter, subproblem fill; + amplify/spread, deconv/interp
+        cb = config_block(args.config, world)
+        if res["mode"] == "points":
+            cb["parallelism"] = f"points split x{world}, NCCL reduce of the partial modes"
+            base["scaling"] = "strong"
+        elif res["mode"] == "transforms":
+            cb["parallelism"] = f"transforms split x{world}, all-gather of the results"
+            base["scaling"] = "strong"
         line = dict(base, value=res["value"], ms_per_step=res["elapsed"] / args.steps * 1e3,
-                    config=config_block(args.config, world),
+                    config=cb,
                     roofline={"bound": "hbm", "achieved": res["achieved"], "peak": res["peak"],
                               "unit": "GB/s", "frac": frac, "traffic": traffic,
-                              "kernel": f"{kern} (k_{'interp_thread' if kern == 'interp' else 'spread_tile'})",
+                              "kernel": f"{kern} (k_{'interp_tile' if kern == 'interp' else 'spread_rows / k_spread_batch2d'})",
                               "algorithmic_bytes": res["B"], "kernel_ms": res["hot_s"] * 1e3,
                               "peak_source": f"{res['peak_kind']} MEASURED_PEAKS.json hbm_gbs"},
                     stages_ms={k: v * 1e3 for k, v in res["stages"].items()},

@@ -35,21 +35,27 @@ struct Cx<float> {
 // by Horner on the piecewise polynomial (all pieces share t) or by exact
 // exp/sqrt.  The Horner table lives in the kernel parameter bank; with W a
 // compile-time constant every coefficient is a uniform constant operand.
+// Exact kernel row (spreadinterp.py:319-327), kept out of line: it is the
+// validation path (use_exact_kernel) and would otherwise bloat every kernel.
+template <typename T>
+__device__ __noinline__ void exact_row(double g, int i0, int W, T beta, T *row) {
+    const T step = (T)2 / (T)W;
+    T z = (T)((2.0 / W) * ((double)i0 - g));
+    for (int m = 0; m < W; ++m) {
+        T a = (T)1 - z * z;
+        a = a < (T)0 ? (T)0 : a;
+        row[m] = exp(beta * (sqrt(a) - (T)1));
+        z += step;
+    }
+}
+
 template <typename T, int W>
 __device__ __forceinline__ int kernel_row(double g, const KernelTab<T> &k, T *row) {
     // footprint origin and local coordinate in float64 exactly as the
     // reference (spreadinterp.py:318, 329), then the plan dtype
     const int i0 = (int)floor(g - 0.5 * W + 1.0);
     if (k.use_exact) {
-        const T step = (T)2 / (T)W;
-        T z = (T)((2.0 / W) * ((double)i0 - g));
-#pragma unroll
-        for (int m = 0; m < W; ++m) {
-            T a = (T)1 - z * z;
-            a = a < (T)0 ? (T)0 : a;
-            row[m] = exp(k.beta * (sqrt(a) - (T)1));
-            z += step;
-        }
+        exact_row<T>(g, i0, W, k.beta, row);
     } else {
         const T t = (T)(2.0 * ((double)i0 - g) + (double)(W - 1));
 #pragma unroll
@@ -409,78 +415,120 @@ __global__ void __launch_bounds__(RowsCfg<T, DIM, W>::NT, RowsCfg<T, DIM, W>::MI
 // (one warp per tile row, lane = transform); every staged point is applied by
 // the warps of its w rows with identical kernel values, so there is no lane
 // waste and the point data is a broadcast.
+// Per-point kernel rows for the batched 2D spreader: evaluated once per
+// point (not once per warp visit), 2W floats + the wrapped origins.
+template <int W>
+struct alignas(16) PtRows2 {
+    float r1[W];
+    float r2[W];
+    int i1, i2;
+};
+
 template <typename T, int W>
-__global__ void __launch_bounds__(Batch2Cfg<T, W>::NT) k_spread_batch2d(SpreadArgs<T> a, const T *cperm) {
+__global__ void __launch_bounds__(256) k_rows2d(SpreadArgs<T> a, PtRows2<W> *tab) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < a.M; k += (int64_t)gridDim.x * blockDim.x) {
+        const Rec rc = load_rec(a.rec, k);
+        PtRows2<W> e;
+        T r[W];
+        int i0 = kernel_row<T, W>(rc.g[0], a.k, r);
+        e.i1 = i0 < 0 ? i0 + a.g.n[0] : i0;
+#pragma unroll
+        for (int m = 0; m < W; ++m) e.r1[m] = (float)r[m];
+        i0 = kernel_row<T, W>(rc.g[1], a.k, r);
+        e.i2 = i0 < 0 ? i0 + a.g.n[1] : i0;
+#pragma unroll
+        for (int m = 0; m < W; ++m) e.r2[m] = (float)r[m];
+        tab[k] = e;
+    }
+}
+
+template <typename T, int W>
+__global__ void __launch_bounds__(128) k_spread_batch2d(SpreadArgs<T> a, const T *cperm, const PtRows2<W> *tab) {
+    // Warp-independent: a persistent warp takes work items (subproblem,
+    // transform group, tile row) from an atomic queue.  Lane = transform.
+    // The item's points are one contiguous run of the finely sorted bin
+    // (oy in [row - W + 1, row]); their kernel rows come precomputed
+    // (k_rows2d), their strengths as one coalesced 256-byte line per point.
+    // No block barriers, no shared memory; next point prefetched.
     using C = typename Cx<T>::type;
     using Cfg = Batch2Cfg<T, W>;
-    constexpr int X = Cfg::X, RY = Cfg::RY, CH = Cfg::CH;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T *s_r = reinterpret_cast<T *>(smem_raw);                 // CH x 2 x W
-    int *s_o = reinterpret_cast<int *>(s_r + CH * 2 * W);     // CH x 2
-    __shared__ int s_sub;
-    const int tid = threadIdx.x, lane = tid & 31, row = tid >> 5;
+    constexpr int X = Cfg::X, RY = Cfg::RY;
+    const int lane = threadIdx.x & 31;
     const int n1 = a.g.n[0], n2 = a.g.n[1];
     const int nsub = *a.nsub;
     const int ngroups = (a.ntransf + 31) / 32;
+    const int nitems = nsub * ngroups * RY;
+    const int kx = a.g.bs[0] >> a.sbl[0];
+    __shared__ C s_slab[4 * 32 * (X + 1)];  // one transposition slab per warp (128 threads)
     for (;;) {
-        if (tid == 0) s_sub = atomicAdd(a.work, 1);
-        __syncthreads();
-        const int s = s_sub;
-        __syncthreads();
-        if (s >= nsub * ngroups) break;
-        const int4 sp = a.subprob[s / ngroups];
-        const int tg = s % ngroups;
+        int item = 0;
+        if (lane == 0) item = atomicAdd(a.work, 1);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if (item >= nitems) break;
+        const int row = item % RY;
+        const int sg = item / RY;
+        const int tg = sg % ngroups;
+        const int4 sp = a.subprob[sg / ngroups];
         const int bin = sp.x, start = sp.y, cnt = sp.z;
         const int b1 = bin % a.g.nb[0], b2 = bin / a.g.nb[0];
         const int lo1 = b1 * a.g.bs[0], lo2 = b2 * a.g.bs[1];
+        const int ylo = max(0, row - W + 1), yhi = min(row, a.g.bs[1] - 1);
+        if (ylo > yhi) continue;
+        const int *ks = a.kstart + (int64_t)bin * a.spb;
+        const int k0 = max(start, ks[(ylo >> a.sbl[1]) * kx]);
+        const int r1k = (yhi >> a.sbl[1]) + 1;
+        const int k1 = min(start + cnt, r1k * kx < a.spb ? ks[r1k * kx] : 0x7fffffff);
+        if (k0 >= k1) continue;
         const int t = tg * 32 + lane;
-        // strengths of this group in sorted order: 32 transforms per point
-        const C *cg = reinterpret_cast<const C *>(cperm) + (int64_t)tg * a.M * 32;
+        const C *cg = reinterpret_cast<const C *>(cperm) + (int64_t)tg * a.M * 32 + lane;
         C acc[X];
 #pragma unroll
         for (int x = 0; x < X; ++x) acc[x] = C{(T)0, (T)0};
-        for (int p0 = 0; p0 < cnt; p0 += CH) {
-            const int nch = min(CH, cnt - p0);
-            __syncthreads();
-            if (tid < nch) {
-                const Rec rc = load_rec(a.rec, start + p0 + tid);
-                T r[W];
-                int i0 = kernel_row<T, W>(rc.g[0], a.k, r);
-                s_o[tid * 2 + 0] = (i0 < 0 ? i0 + n1 : i0) - lo1;
-#pragma unroll
-                for (int m = 0; m < W; ++m) s_r[(tid * 2 + 0) * W + m] = r[m];
-                i0 = kernel_row<T, W>(rc.g[1], a.k, r);
-                s_o[tid * 2 + 1] = (i0 < 0 ? i0 + n2 : i0) - lo2;
-#pragma unroll
-                for (int m = 0; m < W; ++m) s_r[(tid * 2 + 1) * W + m] = r[m];
+        PtRows2<W> e = tab[k0];
+        C cq = cg[(int64_t)k0 * 32];
+        for (int k = k0; k < k1; ++k) {
+            const PtRows2<W> cur = e;
+            const C ccur = cq;
+            if (k + 1 < k1) {  // prefetch the next point
+                e = tab[k + 1];
+                cq = cg[(int64_t)(k + 1) * 32];
             }
-            __syncthreads();
-            for (int q = 0; q < nch; ++q) {
-                const int oy = s_o[q * 2 + 1];
-                const int dy = row - oy;
-                if (dy < 0 || dy >= W) continue;  // warp-uniform (one row per warp)
-                const T *rq = s_r + q * 2 * W;
-                const T f = rq[W + dy];
-                const C cq = cg[(int64_t)(start + p0 + q) * 32 + lane];  // coalesced 32 transforms
-                const C v{cq.x * f, cq.y * f};
-                T r1[W];
+            const int dy = row - (cur.i2 - lo2);
+            if (dy < 0 || dy >= W) continue;  // warp-uniform (sub-cell edges)
+            T wy = (T)cur.r2[0];
 #pragma unroll
-                for (int m = 0; m < W; ++m) r1[m] = rq[m];
-                rows_accumulate<T, 2, W>(acc, s_o[q * 2], v, r1);
+            for (int m = 1; m < W; ++m) wy = (m == dy) ? (T)cur.r2[m] : wy;
+            const C v{ccur.x * wy, ccur.y * wy};
+            T r1[W];
+#pragma unroll
+            for (int m = 0; m < W; ++m) r1[m] = (T)cur.r1[m];
+            rows_accumulate<T, 2, W>(acc, cur.i1 - lo1, v, r1);
+        }
+        // flush: transpose the 32 transforms x X cells through this warp's
+        // shared-memory slab so each RED burst is one transform's contiguous
+        // row (lanes = x): lanes = transforms would scatter 32 planes apart,
+        // which runs at ~4e10 ops/s on B200 vs ~3.7e11 coalesced (measured)
+        (void)t;
+        C *slab = s_slab + (threadIdx.x >> 5) * 32 * (X + 1);
+        __syncwarp();
+#pragma unroll
+        for (int x = 0; x < X; ++x) slab[lane * (X + 1) + x] = acc[x];
+        __syncwarp();
+        int g2 = lo2 + row;
+        while (g2 >= n2) g2 -= n2;
+        int g1 = lo1 + lane;
+        while (g1 >= n1) g1 -= n1;
+        const int tmax = min(32, a.ntransf - tg * 32);
+        for (int tt = 0; tt < tmax; ++tt) {
+            if (lane < X) {
+                const C v = slab[tt * (X + 1) + lane];
+                if (v.x != (T)0 || v.y != (T)0)
+                    red_add(reinterpret_cast<C *>(a.grid) + (int64_t)(tg * 32 + tt) * a.gstride +
+                                (int64_t)g2 * n1 + g1,
+                            v);
             }
         }
-        if (t < a.ntransf) {
-            C *grid = reinterpret_cast<C *>(a.grid) + (int64_t)t * a.gstride;
-            int g2 = lo2 + row;
-            while (g2 >= n2) g2 -= n2;
-#pragma unroll
-            for (int x = 0; x < X; ++x) {
-                if (acc[x].x == (T)0 && acc[x].y == (T)0) continue;
-                int g1 = lo1 + x;
-                while (g1 >= n1) g1 -= n1;
-                red_add(grid + (int64_t)g2 * n1 + g1, acc[x]);
-            }
-        }
+        __syncwarp();
     }
 }
 
@@ -511,7 +559,9 @@ __global__ void __launch_bounds__(1024) k_permute_strengths(SpreadArgs<T> a, con
         __syncthreads();
         const int64_t jj = j0 + ty;
         if (jj < a.M) {
-            const int pos = kstart[key[jj]] + rank[jj];
+            const int pos = key[jj];  // setpts leaves each point's sorted position in key[]
+            (void)rank;
+            (void)kstart;
             reinterpret_cast<C *>(cperm)[((int64_t)g * a.M + pos) * 32 + tx] = tile[tx][ty];
         }
         __syncthreads();
@@ -554,6 +604,7 @@ __global__ void __launch_bounds__(256) k_interp_tile(SpreadArgs<T> a, T *cout, c
         const int b3 = DIM > 2 ? bin / (a.g.nb[0] * a.g.nb[1]) : 0;
         const int lo1 = b1 * a.g.bs[0], lo2 = b2 * a.g.bs[1], lo3 = b3 * a.g.bs[2];
         const C *grid = reinterpret_cast<const C *>(gridp) + (int64_t)t * a.gstride;
+#pragma unroll 4
         for (int i = tid; i < ncell; i += blockDim.x) {
             const int q1 = i % P1;
             const int r = i / P1;
@@ -575,8 +626,11 @@ __global__ void __launch_bounds__(256) k_interp_tile(SpreadArgs<T> a, T *cout, c
             patch[i] = __ldg(grid + gi);
         }
         __syncthreads();
+        // records are prefetched one iteration ahead (the loop body is long)
+        Rec nxt = load_rec(a.rec, start + min(tid, cnt - 1));
         for (int k = tid; k < cnt; k += blockDim.x) {
-            const Rec rc = load_rec(a.rec, start + k);
+            const Rec rc = nxt;
+            if (k + (int)blockDim.x < cnt) nxt = load_rec(a.rec, start + k + blockDim.x);
             T r1[W], r2[W], r3[W];
             int i1 = kernel_row<T, W>(rc.g[0], a.k, r1);
             const int o1 = (i1 < 0 ? i1 + n1 : i1) - lo1;
@@ -865,6 +919,29 @@ __global__ void k_amplify(int ntransf, int n1, int n2, int n3, int64_t N1, int64
 
 // ---------------------------------------------------------------------------
 // dispatch helpers
+template <typename T, int D, template <typename, int, int> class Op, typename... Args>
+int dispatch_w(int w, Args &&...args) {
+    switch (w) {
+// ESN_WMASK (bit w set = width w compiled) trims a development build
+#ifndef ESN_WMASK
+#define ESN_WMASK 0x1fffc
+#endif
+#define ESN_CASE_W(WW)                                   \
+    case WW:                                             \
+        if constexpr ((ESN_WMASK >> WW) & 1) {           \
+            return Op<T, D, WW>::run(args...);           \
+        } else {                                         \
+            return fail(ESN_INTERNAL_ERROR, "width %d not built (ESN_WMASK)", WW); \
+        }
+        ESN_CASE_W(2) ESN_CASE_W(3) ESN_CASE_W(4) ESN_CASE_W(5) ESN_CASE_W(6) ESN_CASE_W(7) ESN_CASE_W(8)
+        ESN_CASE_W(9) ESN_CASE_W(10) ESN_CASE_W(11) ESN_CASE_W(12) ESN_CASE_W(13) ESN_CASE_W(14)
+        ESN_CASE_W(15) ESN_CASE_W(16)
+#undef ESN_CASE_W
+        default:
+            return fail(ESN_INTERNAL_ERROR, "unsupported kernel width %d", w);
+    }
+}
+
 template <typename T, template <typename, int, int> class Op, typename... Args>
 int dispatch_dw(int dim, int w, Args &&...args) {
 #define ESN_CASE_W(D, WW) \

@@ -44,8 +44,10 @@ template <typename T, int D, int W>
 struct SpreadRowsOp {
     static int run(const SpreadArgs<T> &a, cudaStream_t st) {
         if (a.M == 0) return ESN_SUCCESS;
-        if (D == 1) return SpreadGlobalOp<T, D, W>::run(a, st);
-        using Cfg = RowsCfg<T, (D < 2 ? 2 : D), W>;
+        if constexpr (D == 1) {
+            return SpreadGlobalOp<T, D, W>::run(a, st);
+        } else {
+        using Cfg = RowsCfg<T, D, W>;
         using C = typename Cx<T>::type;
         constexpr int NZ = D == 3 ? W : 1;
         const size_t stage = Cfg::CH * NZ * sizeof(C) + Cfg::CH * 2 * W * sizeof(T) + Cfg::CH * 4 * sizeof(int) +
@@ -54,12 +56,13 @@ struct SpreadRowsOp {
         const size_t smem = stage > tile ? stage : tile;
         static int grid = 0;
         if (grid == 0) {
-            int rc = persistent_launch(k_spread_rows<T, (D < 2 ? 2 : D), W>, Cfg::NT, smem, st, nullptr, &grid);
+            int rc = persistent_launch(k_spread_rows<T, D, W>, Cfg::NT, smem, st, nullptr, &grid);
             if (rc) return rc;
         }
-        k_spread_rows<T, (D < 2 ? 2 : D), W><<<grid, Cfg::NT, smem, st>>>(a);
+        k_spread_rows<T, D, W><<<grid, Cfg::NT, smem, st>>>(a);
         ESN_CUDA_TRY(cudaGetLastError());
         return ESN_SUCCESS;
+        }
     }
 };
 
@@ -75,13 +78,16 @@ struct SpreadBatchOp {
             if (pb > (int64_t)device_sm_count() * 16) pb = (int64_t)device_sm_count() * 16;
             k_permute_strengths<T><<<(int)pb, 1024, 0, st>>>(a, key, rank, kstart, cperm);
             ESN_CUDA_TRY(cudaGetLastError());
-            const size_t smem = Cfg::CH * 2 * W * sizeof(T) + Cfg::CH * 2 * sizeof(int);
+            // per-point rows table lives behind the permuted strengths
+            PtRows2<W> *tab = reinterpret_cast<PtRows2<W> *>(
+                reinterpret_cast<char *>(cperm) + (size_t)ngroups * 32 * a.M * 2 * sizeof(T));
+            k_rows2d<T, W><<<grid_for(a.M, 256), 256, 0, st>>>(a, tab);
             static int grid = 0;
             if (grid == 0) {
-                int rc = persistent_launch(k_spread_batch2d<T, W>, Cfg::NT, smem, st, nullptr, &grid);
+                int rc = persistent_launch(k_spread_batch2d<T, W>, 128, 0, st, nullptr, &grid);
                 if (rc) return rc;
             }
-            k_spread_batch2d<T, W><<<grid, Cfg::NT, smem, st>>>(a, cperm);
+            k_spread_batch2d<T, W><<<grid, 128, 0, st>>>(a, cperm, tab);
             ESN_CUDA_TRY(cudaGetLastError());
             return ESN_SUCCESS;
         } else {
@@ -125,21 +131,20 @@ struct InterpOp {
 };
 
 template <>
-int launch_spread<ESN_T>(const SpreadArgs<ESN_T> &a, int method, int nbins, const int *key, const int *rank,
-                         const int *kstart, ESN_T *cperm, cudaStream_t st) {
-    (void)nbins;
-    if (method == ESN_METHOD_GLOBAL || a.g.dim == 1)
-        return dispatch_dw<ESN_T, SpreadGlobalOp>(a.g.dim, a.g.w, a, st);
-    if (batched_spread(sizeof(ESN_T) == 8 ? ESN_F64 : ESN_F32, a.g.dim, a.g.w, a.ntransf, method))
-        return dispatch_dw<ESN_T, SpreadBatchOp>(a.g.dim, a.g.w, a, key, rank, kstart, cperm, st);
-    return dispatch_dw<ESN_T, SpreadRowsOp>(a.g.dim, a.g.w, a, st);
+int launch_spread_d<ESN_T, ESN_D>(const SpreadArgs<ESN_T> &a, int method, const int *key, const int *rank,
+                                  const int *kstart, ESN_T *cperm, cudaStream_t st) {
+    if (method == ESN_METHOD_GLOBAL || ESN_D == 1) return dispatch_w<ESN_T, ESN_D, SpreadGlobalOp>(a.g.w, a, st);
+    if (batched_spread(sizeof(ESN_T) == 8 ? ESN_F64 : ESN_F32, ESN_D, a.g.w, a.ntransf, method))
+        return dispatch_w<ESN_T, ESN_D, SpreadBatchOp>(a.g.w, a, key, rank, kstart, cperm, st);
+    return dispatch_w<ESN_T, ESN_D, SpreadRowsOp>(a.g.w, a, st);
 }
 
 template <>
-int launch_interp<ESN_T>(const SpreadArgs<ESN_T> &a, ESN_T *cout, const ESN_T *grid, cudaStream_t st) {
-    return dispatch_dw<ESN_T, InterpOp>(a.g.dim, a.g.w, a, cout, grid, st);
+int launch_interp_d<ESN_T, ESN_D>(const SpreadArgs<ESN_T> &a, ESN_T *cout, const ESN_T *grid, cudaStream_t st) {
+    return dispatch_w<ESN_T, ESN_D, InterpOp>(a.g.w, a, cout, grid, st);
 }
 
+#if ESN_D == 1
 template <>
 int launch_deconv<ESN_T>(int dim, int ntransf, const int *n, const int64_t *N, const ESN_T *grid,
                          const ESN_T *p1, const ESN_T *p2, const ESN_T *p3, ESN_T *f, cudaStream_t st) {
@@ -164,5 +169,7 @@ int launch_amplify<ESN_T>(int dim, int ntransf, const int *n, const int64_t *N, 
     ESN_CUDA_TRY(cudaGetLastError());
     return ESN_SUCCESS;
 }
+
+#endif  // ESN_D == 1
 
 }  // namespace esn

@@ -89,6 +89,9 @@ struct SpreadArgs {
     const Rec *rec;          // sorted point records
     const int *bin_start;
     const int4 *subprob;     // (bin, start, count, 0)
+    const int *kstart;       // start of every fine sort key (bin-major, sub-cell minor)
+    int spb;                 // sub-cells per bin
+    int sbl[3];              // log2 sub-cell size per dim
     const int *nsub;         // device count of subproblems
     int *work;               // work-queue counter (zeroed before launch)
     const T *c;              // (ntransf, M) interleaved complex
@@ -137,6 +140,12 @@ int launch_spread(const SpreadArgs<T> &a, int method, int nbins, const int *key,
 bool batched_spread(int dtype, int dim, int w, int ntransf, int method);
 template <typename T>
 int launch_interp(const SpreadArgs<T> &a, T *cout, const T *grid, cudaStream_t st);
+// per-dimension instantiations (one translation unit per (dtype, dim))
+template <typename T, int D>
+int launch_spread_d(const SpreadArgs<T> &a, int method, const int *key, const int *rank, const int *kstart,
+                    T *cperm, cudaStream_t st);
+template <typename T, int D>
+int launch_interp_d(const SpreadArgs<T> &a, T *cout, const T *grid, cudaStream_t st);
 template <typename T>
 int launch_deconv(int dim, int ntransf, const int *n, const int64_t *N, const T *grid, const T *p1,
                   const T *p2, const T *p3, T *f, cudaStream_t st);

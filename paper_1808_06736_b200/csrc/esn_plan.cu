@@ -510,6 +510,9 @@ static SpreadArgs<T> make_spread_args(esn_plan p, const void *c, void *grid) {
     a.rec = p->rec;
     a.bin_start = p->bin_start;
     a.subprob = p->subprob;
+    a.kstart = p->cursor;
+    a.spb = p->spb;
+    for (int d = 0; d < 3; ++d) a.sbl[d] = p->sbl[d];
     a.nsub = p->nsub;
     a.work = p->work;
     a.c = (const T *)c;
@@ -525,7 +528,9 @@ bool esn::batched_spread(int dtype, int dim, int w, int ntransf, int method) {
 
 static int do_spread(esn_plan p, const void *c, void *grid) {
     if (esn::batched_spread(p->dtype, p->dim, p->kp.w, p->ntransf, p->method)) {
-        const int64_t need = (int64_t)((p->ntransf + 31) / 32) * 32 * p->M * (int64_t)real_size(p->dtype) * 2;
+        // permuted strengths + per-point rows table (<= 96 B per point)
+        const int64_t need = (int64_t)((p->ntransf + 31) / 32) * 32 * p->M * (int64_t)real_size(p->dtype) * 2 +
+                             96 * p->M + 256;
         if (need > p->cperm_bytes) {
             dfree(p->cperm);
             p->cperm = nullptr;

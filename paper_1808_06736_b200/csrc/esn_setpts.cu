@@ -153,30 +153,51 @@ __global__ void __launch_bounds__(256, 4) k_setpts_count(SetptsArgs a) {
     }
 }
 
-// Pass 2: pos = start[key] + rank; write the point's full record {g, j}
-// with one 256-bit store (a whole L2 sector).  No atomics.
+// Pass 2a: pos[i] = start[key[i]] + rank[i] -- a lean kernel (three 4-byte
+// streams and one L2-resident gather) so many lookups are in flight.
+__global__ void __launch_bounds__(256) k_setpts_pos(SetptsArgs a) {
+    constexpr int U = 8;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * U;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x * U + threadIdx.x; base < a.M; base += stride) {
+        int key[U], rank[U], st[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = base + (int64_t)u * blockDim.x;
+            key[u] = i < a.M ? a.key[i] : 0;
+            rank[u] = i < a.M ? a.rank[i] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) st[u] = __ldg(a.cursor + key[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = base + (int64_t)u * blockDim.x;
+            if (i < a.M) a.key[i] = st[u] + rank[u];  // key[] now holds the position
+        }
+    }
+}
+
+// Pass 2b: write the point's full record {g, j} at its position with one
+// 256-bit store (a whole L2 sector).  Streams x and pos; no dependent loads.
 template <typename XT>
 __global__ void __launch_bounds__(256) k_setpts_scatter(SetptsArgs a) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * kILP;
     for (int64_t base = (int64_t)blockIdx.x * blockDim.x * kILP + threadIdx.x; base < a.M; base += stride) {
         double x[kILP][3];
         load_coords<XT>(a, base, x);
-        int key[kILP], rank[kILP];
+        int pos[kILP];
 #pragma unroll
         for (int u = 0; u < kILP; ++u) {
             const int64_t i = base + (int64_t)u * blockDim.x;
-            key[u] = i < a.M ? __ldg(a.key + i) : -1;
-            rank[u] = i < a.M ? __ldg(a.rank + i) : 0;
+            pos[u] = i < a.M ? __ldg(a.key + i) : -1;
         }
 #pragma unroll
         for (int u = 0; u < kILP; ++u) {
-            if (key[u] < 0) continue;
+            if (pos[u] < 0) continue;
             const int64_t i = base + (int64_t)u * blockDim.x;
             double g[3] = {0.0, 0.0, 0.0};
             point_key(a, i, x[u], g, false);
-            const int pos = __ldg(a.cursor + key[u]) + rank[u];
             const unsigned long long j = (unsigned long long)(unsigned)i;
-            asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(a.rec + pos),
+            asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(a.rec + pos[u]),
                          "l"(__double_as_longlong(g[0])), "l"(__double_as_longlong(g[1])),
                          "l"(__double_as_longlong(g[2])), "l"(j)
                          : "memory");
@@ -318,6 +339,9 @@ static int setpts_impl(const SetptsArgs &a, int nbins, int maxsub, int4 *subprob
     k_scan_down<<<nsb, 1024, 0, st>>>(a.key_count, a.nkeys, a.block_sums, a.cursor, a.bin_start, a.spb, nbins);
     ESN_CUDA_TRY(cudaGetLastError());
     if (a.M > 0) {
+        int64_t pb = (a.M + threads * 8 - 1) / (threads * 8);
+        if (pb > cap) pb = cap;
+        k_setpts_pos<<<(int)pb, threads, 0, st>>>(a);
         k_setpts_scatter<XT><<<(int)blocks, threads, 0, st>>>(a);
         ESN_CUDA_TRY(cudaGetLastError());
     }

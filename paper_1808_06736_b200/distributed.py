@@ -1,0 +1,97 @@
+"""Multi-GPU execution (one process per GPU, torch.distributed over NCCL).
+
+SURVEY.md section 8(e):
+
+* one large type-1 transform (config c3) splits its POINTS across ranks;
+  each rank spreads its shard into its own fine grid, FFTs and
+  deconvolves, and the partial mode arrays are summed with one NCCL reduce
+  (exact by linearity of spreading, FFT and the diagonal correction; the
+  mode array is sigma^d = 8x smaller than the fine grid it replaces);
+* batched transforms (config c5) split their TRANSFORMS across ranks: every
+  rank sorts the shared point set itself and runs its slice of strength
+  vectors -- no data-path collective; the slices are gathered at the end;
+* type 2 and single-GPU configs run as independent replicas (each rank owns
+  its own targets; type-2 outputs are independent per point).
+
+``compute`` is injectable so the host-side sharding / reduction logic is
+testable on CPU with the gloo backend; production calls use the GPU
+transforms of this package.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous balanced shard [lo, hi) of ``total`` items for ``rank``."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank/world {rank}/{world}")
+    base, extra = divmod(int(total), world)
+    lo = rank * base + min(rank, extra)
+    hi = lo + base + (1 if rank < extra else 0)
+    return lo, hi
+
+
+def _world(group):
+    if not dist.is_available() or not dist.is_initialized():
+        return 0, 1
+    return dist.get_rank(group), dist.get_world_size(group)
+
+
+def _gpu_type1(coords, strengths, num_modes, opts):
+    from .transforms import exec_type1
+    return exec_type1(coords, strengths, num_modes, opts)[0]
+
+
+def _as_real_view(t: torch.Tensor) -> torch.Tensor:
+    return torch.view_as_real(t) if t.is_complex() else t
+
+
+def exec_type1_point_sharded(coords, strengths, num_modes, opts, *, group=None, dst: int | None = 0,
+                             compute=None):
+    """Type 1 over points distributed across ranks.
+
+    Every rank passes ITS shard of points / strengths (any split); the
+    result -- the transform of the union of all shards -- is returned on
+    ``dst`` (all ranks when ``dst`` is None, via all-reduce).  Other ranks
+    get their partial modes back (useful for overlap), or None when
+    ``dst`` is a different rank.
+    """
+    compute = compute or _gpu_type1
+    rank, world = _world(group)
+    part = compute(coords, strengths, num_modes, opts)
+    if world == 1:
+        return part
+    t = part if isinstance(part, torch.Tensor) else torch.as_tensor(part)
+    t = t.contiguous()
+    buf = _as_real_view(t)
+    if dst is None:
+        dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+        return t
+    dist.reduce(buf, dst=dst, op=dist.ReduceOp.SUM, group=group)
+    return t if rank == dst else None
+
+
+def exec_type1_transform_sharded(coords, strengths_all, num_modes, opts, *, group=None, compute=None):
+    """Batched type 1 (strengths (T, M)) with the T transforms split across
+    ranks; every rank returns the full (T, N_d..N_1) result (all-gather)."""
+    compute = compute or _gpu_type1
+    rank, world = _world(group)
+    T = strengths_all.shape[0]
+    lo, hi = shard_range(T, rank, world)
+    mine = strengths_all[lo:hi]
+    if hi <= lo:
+        raise ValueError(f"rank {rank} has no transforms (T={T} < world={world})")
+    part = compute(coords, mine, num_modes, opts)
+    if world == 1:
+        return part
+    shapes = [shard_range(T, r, world) for r in range(world)]
+    width = max(h - l for l, h in shapes)
+    ref = part if isinstance(part, torch.Tensor) else torch.as_tensor(part)
+    pad = torch.zeros((width,) + tuple(ref.shape[1:]), dtype=ref.dtype, device=ref.device)
+    pad[: ref.shape[0]] = ref
+    slabs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather([_as_real_view(s) for s in slabs], _as_real_view(pad), group=group)
+    return torch.cat([s[: h - l] for s, (l, h) in zip(slabs, shapes)], dim=0)
