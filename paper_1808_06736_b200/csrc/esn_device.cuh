@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(256) k_spread_global(SpreadArgs<T> a) {
         }
         for (int t = 0; t < a.ntransf; ++t) {
             C c = reinterpret_cast<const C *>(a.c)[(int64_t)t * a.M + j];
-            if (!finite2<T>(c)) flag_min(&a.flags[6], (unsigned long long)j);
+            if (!finite2<T>(c)) flag_min(&a.flags[6], (unsigned long long)(j + a.ibase));
             C *grid = reinterpret_cast<C *>(a.grid) + (int64_t)t * a.gstride;
             if (DIM == 1) {
 #pragma unroll
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(RowsCfg<T, DIM, W>::NT, RowsCfg<T, DIM, W>::MI
                 if (tid < nch) {  // phase A: one thread per staged point
                     const Rec rc = load_rec(a.rec, start + ci + tid * nck);
                     C c = cin[rc.j];
-                    if (!finite2<T>(c)) flag_min(&a.flags[6], (unsigned long long)rc.j);
+                    if (!finite2<T>(c)) flag_min(&a.flags[6], (unsigned long long)(rc.j + a.ibase));
                     T r[W];
                     int i0 = kernel_row<T, W>(rc.g[0], a.k, r);
                     const int ox = (i0 < 0 ? i0 + n1 : i0) - lo1;
@@ -553,7 +553,7 @@ __global__ void __launch_bounds__(1024) k_permute_strengths(SpreadArgs<T> a, con
         C v{(T)0, (T)0};
         if (t < a.ntransf && j < a.M) {
             v = reinterpret_cast<const C *>(a.c)[(int64_t)t * a.M + j];
-            if (!finite2<T>(v)) flag_min(&a.flags[6], (unsigned long long)j);
+            if (!finite2<T>(v)) flag_min(&a.flags[6], (unsigned long long)(j + a.ibase));
         }
         tile[ty][tx] = v;
         __syncthreads();

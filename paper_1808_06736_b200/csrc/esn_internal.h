@@ -76,6 +76,7 @@ struct SetptsArgs {
     int *bin_start;         // nbins + 1
     int *block_sums;        // scan scratch
     Rec *rec;               // M sorted records
+    int64_t ibase;          // index offset of this point chunk (error reports)
     unsigned long long *flags;  // [0..2] first non-finite per dim, [3..5] first |x|>3pi
     int check_bounds;
 };
@@ -97,6 +98,7 @@ struct SpreadArgs {
     const T *c;              // (ntransf, M) interleaved complex
     T *grid;                 // (ntransf, n3, n2, n1) interleaved complex
     int64_t gstride;         // complex cells per transform
+    int64_t ibase;           // index offset of this point chunk (error reports)
     unsigned long long *flags;  // [6] first non-finite strength
 };
 

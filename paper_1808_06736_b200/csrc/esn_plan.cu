@@ -110,6 +110,9 @@ struct esn_plan_s {
     cudaEvent_t ev[8] = {};
     bool have_events = false;
     bool points_set = false;
+    bool borrowed = false;    // pk[] and grid belong to another plan (pipeline helper)
+    bool keep_flags = false;  // setpts keeps accumulating error flags (chunked runs)
+    int64_t ibase = 0;        // original index of this plan's point 0 (chunked runs)
     float last_ms[4] = {0, 0, 0, 0};  // sort, spread, fft, correct
 };
 
@@ -347,7 +350,10 @@ int esn_plan_destroy(esn_plan p) {
     if (!p) return ESN_SUCCESS;
     if (p->st) cudaStreamSynchronize(p->st);
     else cudaDeviceSynchronize();
-    for (int d = 0; d < 3; ++d) dfree(p->pk[d]);
+    if (!p->borrowed) {
+        for (int d = 0; d < 3; ++d) dfree(p->pk[d]);
+        dfree(p->grid);
+    }
     dfree(p->rec);
     dfree(p->pkey);
     dfree(p->prank);
@@ -361,7 +367,6 @@ int esn_plan_destroy(esn_plan p) {
     dfree(p->work);
     dfree(p->subprob);
     dfree(p->flags);
-    dfree(p->grid);
     if (p->have_events)
         for (int i = 0; i < 8; ++i) cudaEventDestroy(p->ev[i]);
     delete p;
@@ -464,8 +469,9 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
     p->M = M;
     if (p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[0], p->st));
     ESN_CUDA_TRY(cudaMemsetAsync(p->key_count, 0, sizeof(int) * p->nkeys, p->st));
-    ESN_CUDA_TRY(cudaMemsetAsync(p->flags, 0xff, sizeof(unsigned long long) * 8, p->st));
+    if (!p->keep_flags) ESN_CUDA_TRY(cudaMemsetAsync(p->flags, 0xff, sizeof(unsigned long long) * 8, p->st));
     SetptsArgs a{};
+    a.ibase = p->ibase;
     a.g = p->geom;
     a.M = M;
     a.coord_f32 = (coord_dtype & 0xf) == ESN_F32;
@@ -518,6 +524,7 @@ static SpreadArgs<T> make_spread_args(esn_plan p, const void *c, void *grid) {
     a.c = (const T *)c;
     a.grid = (T *)grid;
     a.gstride = p->G;
+    a.ibase = p->ibase;
     a.flags = p->flags;
     return a;
 }
@@ -526,7 +533,7 @@ bool esn::batched_spread(int dtype, int dim, int w, int ntransf, int method) {
     return method != ESN_METHOD_GLOBAL && dim == 2 && dtype == ESN_F32 && ntransf > 1 && w <= 10;
 }
 
-static int do_spread(esn_plan p, const void *c, void *grid) {
+static int do_spread(esn_plan p, const void *c, void *grid, bool zero = true) {
     if (esn::batched_spread(p->dtype, p->dim, p->kp.w, p->ntransf, p->method)) {
         // permuted strengths + per-point rows table (<= 96 B per point)
         const int64_t need = (int64_t)((p->ntransf + 31) / 32) * 32 * p->M * (int64_t)real_size(p->dtype) * 2 +
@@ -539,7 +546,7 @@ static int do_spread(esn_plan p, const void *c, void *grid) {
             p->cperm_bytes = need;
         }
     }
-    ESN_CUDA_TRY(cudaMemsetAsync(grid, 0, real_size(p->dtype) * 2 * (size_t)p->G * p->ntransf, p->st));
+    if (zero) ESN_CUDA_TRY(cudaMemsetAsync(grid, 0, real_size(p->dtype) * 2 * (size_t)p->G * p->ntransf, p->st));
     ESN_CUDA_TRY(cudaMemsetAsync(p->work, 0, sizeof(int), p->st));
     if (p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[6], p->st));
     int rc = p->dtype == ESN_F64
@@ -731,7 +738,59 @@ int esn_fft(int dim, int dtype, int ntransf, const int64_t *nfine, void *data, i
 
 // ---------------------------------------------------------------------------
 // Host-buffer one-shot routines (esnufftpy analog).  A small cache keeps the
-// plan and device staging buffers for repeated calls of the same shape.
+// plan, two pipeline helper plans and device staging buffers for repeated
+// calls of the same shape.  With pinned host buffers and enough points the
+// transfer is pipelined: points are processed in chunks on two streams so
+// host->device copies of chunk i+1, the kernels of chunk i and the
+// device->host copy of chunk i-1 overlap (PCIe is full duplex); the fine
+// grid is shared (type 1: chunks spread into it; type 2: chunks interpolate
+// from it once amplify + FFT are done).
+
+// A plan that shares `main`'s kernel tables, corrections and fine grid but
+// owns its own point scratch and stream.
+static int clone_point_plan(esn_plan main, cudaStream_t st, esn_plan *out) {
+    esn_plan p = new esn_plan_s();
+    p->type = main->type;
+    p->dim = main->dim;
+    p->dtype = main->dtype;
+    p->isign = main->isign;
+    p->ntransf = main->ntransf;
+    for (int d = 0; d < 3; ++d) {
+        p->N[d] = main->N[d];
+        p->n[d] = main->n[d];
+        p->pk[d] = main->pk[d];
+        p->sbl[d] = main->sbl[d];
+    }
+    p->kp = main->kp;
+    p->coeffs = main->coeffs;
+    p->opts = main->opts;
+    p->opts.timing = 0;
+    p->opts.stream = st;
+    p->st = st;
+    p->geom = main->geom;
+    p->nbins = main->nbins;
+    p->maxsub = main->maxsub;
+    p->method = main->method;
+    p->G = main->G;
+    p->spb = main->spb;
+    p->nkeys = main->nkeys;
+    p->grid = main->grid;
+    p->borrowed = true;
+    int rc;
+    if ((rc = dmalloc(p, &p->key_count, sizeof(int) * p->nkeys)) ||
+        (rc = dmalloc(p, &p->cursor, sizeof(int) * p->nkeys)) ||
+        (rc = dmalloc(p, &p->block_sums, sizeof(int) * ((p->nkeys + kScanTile - 1) / kScanTile + 1))) ||
+        (rc = dmalloc(p, &p->bin_start, sizeof(int) * (p->nbins + 1))) ||
+        (rc = dmalloc(p, &p->subofs, sizeof(int) * (p->nbins + 1))) || (rc = dmalloc(p, &p->nsub, sizeof(int) * 2)) ||
+        (rc = dmalloc(p, &p->work, sizeof(int) * 2)) ||
+        (rc = dmalloc(p, &p->flags, sizeof(unsigned long long) * 8))) {
+        esn_plan_destroy(p);
+        return rc;
+    }
+    *out = p;
+    return ESN_SUCCESS;
+}
+
 namespace {
 struct HostSlot {
     int type, dim, isign, ntransf, dtype;
@@ -739,6 +798,10 @@ struct HostSlot {
     double tol, sigma;
     int method;
     esn_plan plan = nullptr;
+    static constexpr int NH = 4;  // pipeline helpers / streams
+    esn_plan helper[NH] = {};
+    cudaStream_t hst[NH] = {};
+    cudaEvent_t ev_grid = nullptr, ev_done[NH] = {};
     void *dx[3] = {nullptr, nullptr, nullptr};
     void *dc = nullptr, *df = nullptr;
     int64_t Mcap = 0;
@@ -746,7 +809,140 @@ struct HostSlot {
 };
 std::mutex g_host_mu;
 std::vector<HostSlot> g_slots;
+
+void free_slot(HostSlot &s) {
+    for (int h = 0; h < HostSlot::NH; ++h) {
+        if (s.helper[h]) esn_plan_destroy(s.helper[h]);
+        if (s.hst[h]) cudaStreamDestroy(s.hst[h]);
+        if (s.ev_done[h]) cudaEventDestroy(s.ev_done[h]);
+    }
+    if (s.ev_grid) cudaEventDestroy(s.ev_grid);
+    if (s.plan) esn_plan_destroy(s.plan);
+    for (int d = 0; d < 3; ++d) dfree(s.dx[d]);
+    dfree(s.dc);
+    dfree(s.df);
+    if (s.st) cudaStreamDestroy(s.st);
+}
+
+bool is_pinned(const void *ptr) {
+    if (!ptr) return true;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
 }  // namespace
+
+// strided (ntransf rows) H2D / D2H of point range [lo, hi) of a (T, M) array
+static int copy_rows(void *dst, const void *src, int64_t M_dst, int64_t M_src, int64_t lo_dst, int64_t lo_src,
+                     int64_t cnt, int T, size_t cb, cudaMemcpyKind kind, cudaStream_t st) {
+    if (cnt <= 0) return ESN_SUCCESS;
+    if (cudaMemcpy2DAsync((char *)dst + lo_dst * cb, M_dst * cb, (const char *)src + lo_src * cb, M_src * cb,
+                          cnt * cb, T, kind, st) != cudaSuccess)
+        return fail(ESN_INTERNAL_ERROR, "strided copy failed (%s)", cudaGetErrorString(cudaGetLastError()));
+    return ESN_SUCCESS;
+}
+
+static int pipelined(HostSlot *slot, int type, int dim, int64_t M, const double *const *xs, int T, void *c, void *f,
+                     int64_t nm, size_t cb) {
+    esn_plan p = slot->plan;
+    int rc;
+    constexpr int NH = HostSlot::NH;
+    for (int h = 0; h < NH; ++h) {
+        if (!slot->hst[h]) {
+            ESN_CUDA_TRY(cudaStreamCreateWithFlags(&slot->hst[h], cudaStreamNonBlocking));
+            ESN_CUDA_TRY(cudaEventCreateWithFlags(&slot->ev_done[h], cudaEventDisableTiming));
+        }
+        if (!slot->helper[h] && (rc = clone_point_plan(p, slot->hst[h], &slot->helper[h]))) return rc;
+    }
+    if (!slot->ev_grid) ESN_CUDA_TRY(cudaEventCreateWithFlags(&slot->ev_grid, cudaEventDisableTiming));
+    cudaStream_t st = p->st;
+    const int K = (int)std::min<int64_t>(16, (M + (1 << 19) - 1) >> 19);
+    const int64_t chunk = (M + K - 1) / K;
+    // main stream: error flags, then type 2: modes in + amplify + FFT;
+    // type 1: zero the shared grid
+    ESN_CUDA_TRY(cudaMemsetAsync(p->flags, 0xff, sizeof(unsigned long long) * 8, st));
+    for (int h = 0; h < NH; ++h) {
+        ESN_CUDA_TRY(cudaMemsetAsync(slot->helper[h]->flags, 0xff, sizeof(unsigned long long) * 8, slot->hst[h]));
+        slot->helper[h]->keep_flags = true;
+    }
+    if (type == 2) {
+        if (cudaMemcpyAsync(slot->df, f, cb * nm * T, cudaMemcpyHostToDevice, st) != cudaSuccess)
+            return fail(ESN_INTERNAL_ERROR, "H2D copy failed");
+        if (p->dtype == ESN_F64)
+            rc = launch_amplify<double>(p->dim, p->ntransf, p->n, p->N, (const double *)slot->df, (const double *)p->pk[0],
+                                        (const double *)p->pk[1], (const double *)p->pk[2], (double *)p->grid,
+                                        p->flags + 6, st);
+        else
+            rc = launch_amplify<float>(p->dim, p->ntransf, p->n, p->N, (const float *)slot->df, (const float *)p->pk[0],
+                                       (const float *)p->pk[1], (const float *)p->pk[2], (float *)p->grid, p->flags + 6,
+                                       st);
+        if (rc) return rc;
+        if ((rc = run_fft(p->dim, p->n, p->dtype, p->ntransf, p->grid, p->isign, st))) return rc;
+    } else {
+        ESN_CUDA_TRY(cudaMemsetAsync(p->grid, 0, real_size(p->dtype) * 2 * (size_t)p->G * p->ntransf, st));
+    }
+    ESN_CUDA_TRY(cudaEventRecord(slot->ev_grid, st));
+    for (int k = 0; k < K; ++k) {
+        const int h = k % NH;
+        esn_plan q = slot->helper[h];
+        cudaStream_t hs = slot->hst[h];
+        const int64_t lo = k * chunk, cnt = std::min(chunk, M - lo);
+        if (cnt <= 0) break;
+        // chunk k lands in staging slot lo (disjoint per chunk, so no reuse hazard)
+        for (int d = 0; d < dim; ++d)
+            if (cudaMemcpyAsync((double *)slot->dx[d] + lo, xs[d] + lo, sizeof(double) * cnt, cudaMemcpyHostToDevice,
+                                hs) != cudaSuccess)
+                return fail(ESN_INTERNAL_ERROR, "H2D copy failed");
+        // chunk views of the (T, M) strength / output arrays: the kernels
+        // index c[t * cnt + j], so T > 1 stages through a (T, cnt) block in
+        // the second half of the staging buffer (disjoint per chunk)
+        char *blk = (char *)slot->dc + (T > 1 ? (size_t)M * T * cb + (size_t)lo * T * cb : (size_t)lo * cb);
+        if (type == 1 && (rc = copy_rows(blk, c, cnt, M, 0, lo, cnt, T, cb, cudaMemcpyHostToDevice, hs))) return rc;
+        q->ibase = lo;
+        const void *cx[3] = {nullptr, nullptr, nullptr};
+        for (int d = 0; d < dim; ++d) cx[d] = (const double *)slot->dx[d] + lo;
+        if ((rc = esn_plan_setpts(q, cnt, ESN_F64, cx[0], cx[1], cx[2]))) return rc;
+        ESN_CUDA_TRY(cudaStreamWaitEvent(hs, slot->ev_grid, 0));
+        if (type == 1) {
+            if ((rc = do_spread(q, blk, p->grid, false))) return rc;
+        } else {
+            if ((rc = do_interp(q, p->grid, blk))) return rc;
+            if ((rc = copy_rows(c, blk, M, cnt, lo, 0, cnt, T, cb, cudaMemcpyDeviceToHost, hs))) return rc;
+        }
+        // (the helper's scratch is reused NH chunks later on the same stream)
+        ESN_CUDA_TRY(cudaEventRecord(slot->ev_done[h], hs));
+    }
+    for (int h = 0; h < NH; ++h) ESN_CUDA_TRY(cudaStreamWaitEvent(st, slot->ev_done[h], 0));
+    if (type == 1) {
+        if ((rc = run_fft(p->dim, p->n, p->dtype, p->ntransf, p->grid, p->isign, st))) return rc;
+        if (p->dtype == ESN_F64)
+            rc = launch_deconv<double>(p->dim, p->ntransf, p->n, p->N, (const double *)p->grid, (const double *)p->pk[0],
+                                       (const double *)p->pk[1], (const double *)p->pk[2], (double *)slot->df, st);
+        else
+            rc = launch_deconv<float>(p->dim, p->ntransf, p->n, p->N, (const float *)p->grid, (const float *)p->pk[0],
+                                      (const float *)p->pk[1], (const float *)p->pk[2], (float *)slot->df, st);
+        if (rc) return rc;
+        if (cudaMemcpyAsync(f, slot->df, cb * nm * T, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+            return fail(ESN_INTERNAL_ERROR, "D2H copy failed");
+    }
+    ESN_CUDA_TRY(cudaStreamSynchronize(st));
+    // merge the error flags: helpers hold the coordinate (and type-1
+    // strength) flags with global indices, the main plan the mode flags
+    unsigned long long h[NH + 1][8];
+    ESN_CUDA_TRY(cudaMemcpy(h[0], p->flags, sizeof(h[0]), cudaMemcpyDeviceToHost));
+    for (int k = 0; k < NH; ++k)
+        ESN_CUDA_TRY(cudaMemcpy(h[1 + k], slot->helper[k]->flags, sizeof(h[0]), cudaMemcpyDeviceToHost));
+    unsigned long long merged[8];
+    for (int i = 0; i < 8; ++i) {
+        merged[i] = h[0][i];
+        for (int k = 1; k <= NH; ++k) merged[i] = std::min(merged[i], h[k][i]);
+    }
+    ESN_CUDA_TRY(cudaMemcpy(p->flags, merged, sizeof(merged), cudaMemcpyHostToDevice));
+    return esn_plan_check(p, nullptr);
+}
 
 int esn_nufft_host(int type, int dim, int64_t M, const double *x, const double *y, const double *z, int ntransf,
                    void *c, int isign, double tol, const int64_t *nmodes, void *f, const esn_opts *opts) {
@@ -764,18 +960,21 @@ int esn_nufft_host(int type, int dim, int64_t M, const double *x, const double *
     if (opts) o = *opts; else esn_default_opts(&o);
     const int dtype = o.dtype == ESN_F32 ? ESN_F32 : ESN_F64;
     std::lock_guard<std::mutex> lk(g_host_mu);
+    const bool cacheable = !o.params && !o.coeffs && !o.check_bounds && !o.use_exact_kernel && !o.stream;
     HostSlot *slot = nullptr;
-    for (auto &s : g_slots) {
-        bool same = s.type == type && s.dim == dim && s.isign == isign && s.ntransf == ntransf && s.dtype == dtype &&
-                    s.tol == tol && s.sigma == o.sigma && s.method == o.method;
-        for (int d = 0; d < dim && same; ++d) same = s.N[d] == nmodes[d];
-        if (same && !o.params && !o.coeffs && !o.check_bounds && !o.use_exact_kernel && !o.stream) {
-            slot = &s;
-            break;
+    if (cacheable) {
+        for (auto &s : g_slots) {
+            bool same = s.type == type && s.dim == dim && s.isign == isign && s.ntransf == ntransf &&
+                        s.dtype == dtype && s.tol == tol && s.sigma == o.sigma && s.method == o.method;
+            for (int d = 0; d < dim && same; ++d) same = s.N[d] == nmodes[d];
+            if (same) {
+                slot = &s;
+                break;
+            }
         }
     }
-    bool transient = false;
     HostSlot tmp{};
+    bool transient = false;
     if (!slot) {
         tmp.type = type; tmp.dim = dim; tmp.isign = isign; tmp.ntransf = ntransf; tmp.dtype = dtype;
         tmp.tol = tol; tmp.sigma = o.sigma; tmp.method = o.method;
@@ -789,15 +988,9 @@ int esn_nufft_host(int type, int dim, int64_t M, const double *x, const double *
             if (tmp.st) cudaStreamDestroy(tmp.st);
             return rc;
         }
-        bool cacheable = !o.params && !o.coeffs && !o.check_bounds && !o.use_exact_kernel && tmp.st;
         if (cacheable) {
-            if (g_slots.size() >= 8) {
-                HostSlot &old = g_slots.front();
-                esn_plan_destroy(old.plan);
-                for (int d = 0; d < 3; ++d) dfree(old.dx[d]);
-                dfree(old.dc);
-                dfree(old.df);
-                if (old.st) cudaStreamDestroy(old.st);
+            if (g_slots.size() >= 4) {
+                free_slot(g_slots.front());
                 g_slots.erase(g_slots.begin());
             }
             g_slots.push_back(tmp);
@@ -817,11 +1010,21 @@ int esn_nufft_host(int type, int dim, int64_t M, const double *x, const double *
         for (int d = 0; d < 3; ++d) { dfree(slot->dx[d]); slot->dx[d] = nullptr; }
         dfree(slot->dc);
         slot->dc = nullptr;
-        for (int d = 0; d < dim && !rc; ++d) rc = dmalloc(p, &slot->dx[d], sizeof(double) * M);
-        if (!rc) rc = dmalloc(p, &slot->dc, cb * M * ntransf);
+        for (int d = 0; d < dim && !rc; ++d) rc = dmalloc(p, &slot->dx[d], sizeof(double) * (M > 0 ? M : 1));
+        // strengths / outputs plus a (T, chunk) staging block per chunk
+        if (!rc) rc = dmalloc(p, &slot->dc, cb * (M > 0 ? M : 1) * ntransf * 2);
         slot->Mcap = M;
     }
     if (!rc && !slot->df) rc = dmalloc(p, &slot->df, cb * nm * ntransf);
+    bool pipe = !rc && cacheable && M >= (int64_t)(2 << 20) && is_pinned(c) && is_pinned(f);
+    for (int d = 0; d < dim && pipe; ++d) pipe = is_pinned(xs[d]);
+    static const char *nopipe = getenv("ESN_NO_PIPELINE");
+    if (nopipe && nopipe[0] == '1') pipe = false;
+    if (pipe) {
+        rc = pipelined(slot, type, dim, M, xs, ntransf, c, f, nm, cb);
+        if (transient) free_slot(*slot);
+        return rc;
+    }
     if (!rc) {
         for (int d = 0; d < dim && M > 0; ++d)
             if (cudaMemcpyAsync(slot->dx[d], xs[d], sizeof(double) * M, cudaMemcpyHostToDevice, st) != cudaSuccess)
@@ -845,13 +1048,7 @@ int esn_nufft_host(int type, int dim, int64_t M, const double *x, const double *
         }
     }
     if (!rc) rc = esn_plan_check(p, nullptr);
-    if (transient) {
-        esn_plan_destroy(slot->plan);
-        for (int d = 0; d < 3; ++d) dfree(slot->dx[d]);
-        dfree(slot->dc);
-        dfree(slot->df);
-        if (slot->st) cudaStreamDestroy(slot->st);
-    }
+    if (transient) free_slot(*slot);
     return rc;
 }
 

@@ -83,10 +83,10 @@ __device__ __forceinline__ int point_key(const SetptsArgs &a, int64_t i, const d
         const double x = xin[d];
         double g = 0.0;
         if (!isfinite(x)) {
-            if (check) atomicMin(&a.flags[d], (unsigned long long)i);
+            if (check) atomicMin(&a.flags[d], (unsigned long long)(i + a.ibase));
         } else {
             if (check && a.check_bounds && fabs(x) > 3.0 * 3.141592653589793)
-                atomicMin(&a.flags[3 + d], (unsigned long long)i);
+                atomicMin(&a.flags[3 + d], (unsigned long long)(i + a.ibase));
             if (a.grid_units) {
                 g = x;  // caller already folded (bin_sort on grid coordinates, grid.py:202)
                 if (g >= (double)a.g.n[d]) g -= (double)a.g.n[d];

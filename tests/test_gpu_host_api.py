@@ -1,0 +1,76 @@
+"""The C ABI one-shot routines on HOST buffers (the esnufftpy convention):
+pipelined (pinned buffers, >= 2 Mi points: chunked H2D / compute / D2H on
+two streams) and plain paths against the CPU oracle and the device API."""
+
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+import cases
+
+pytestmark = pytest.mark.gpu
+
+
+def _call_host(ttype, coords, data, nm, tol, isign, dtype="float64", ntransf=1, pinned=True):
+    from paper_1808_06736_b200 import _lib
+    from paper_1808_06736_b200.plan import make_opts
+    cplx = torch.complex128 if dtype == "float64" else torch.complex64
+    M = len(coords[0])
+    hx = [torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)) for x in coords]
+    hd = torch.from_numpy(np.ascontiguousarray(data)).to(cplx)
+    if ttype == 1:
+        hout = torch.empty(((ntransf,) if ntransf > 1 else ()) + tuple(reversed(nm)), dtype=cplx)
+    else:
+        hout = torch.empty((ntransf, M) if ntransf > 1 else (M,), dtype=cplx)
+    if pinned:
+        hx = [x.pin_memory() for x in hx]
+        hd = hd.pin_memory()
+        hout = hout.pin_memory()
+    cptr, fptr = (hd, hout) if ttype == 1 else (hout, hd)
+    o, keep = make_opts(dtype=dtype, timing=False)
+    xp = [ctypes.c_void_p(x.data_ptr()) for x in hx] + [None] * (3 - len(hx))
+    st = _lib.lib.esn_nufft_host(ttype, len(coords), M, xp[0], xp[1], xp[2], ntransf,
+                                 ctypes.c_void_p(cptr.data_ptr()), isign, tol, _lib.i64_array(nm),
+                                 ctypes.c_void_p(fptr.data_ptr()), ctypes.byref(o))
+    return st, hout.numpy()
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_host_type2_pipelined_matches_device(esn, pinned):
+    coords, f, cfg = cases.make_inputs("c2", M=3_000_000)
+    st, out = _call_host(2, coords, f, cfg["nm"], cfg["tol"], cfg["isign"], pinned=pinned)
+    assert st == 0
+    ref, _ = esn.exec_type2(coords, f, esn.TransformOptions(tolerance=cfg["tol"], isign=cfg["isign"]))
+    assert np.linalg.norm(out - ref) <= 1e-13 * np.linalg.norm(ref)
+
+
+def test_host_type1_pipelined_matches_device(esn):
+    coords, c, cfg = cases.make_inputs("c3", M=2_500_000)
+    st, out = _call_host(1, coords, c, cfg["nm"], cfg["tol"], cfg["isign"])
+    assert st == 0
+    ref, _ = esn.exec_type1(coords, c, cfg["nm"], esn.TransformOptions(tolerance=cfg["tol"], isign=cfg["isign"]))
+    assert np.linalg.norm(out - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+def test_host_batched_pipelined_matches_device(esn):
+    coords, c, cfg = cases.make_inputs("c5", M=2_200_000, ntransf=5)
+    st, out = _call_host(1, coords, c, cfg["nm"], cfg["tol"], cfg["isign"], dtype="float32", ntransf=5)
+    assert st == 0
+    ref, _ = esn.exec_type1([x.astype(np.float32) for x in coords], c.astype(np.complex64), cfg["nm"],
+                            esn.TransformOptions(tolerance=cfg["tol"], isign=cfg["isign"], dtype="float32"))
+    assert np.linalg.norm(out - ref) <= 1e-5 * np.linalg.norm(ref)
+
+
+def test_host_status_codes(esn):
+    from paper_1808_06736_b200 import _lib
+    # argument misuse -> SIZE_ERROR (3) before any work (esnufftpy __init__.py:54-122)
+    st = _lib.lib.esn_nufft_host(3, 1, 10, None, None, None, 1, None, 1, 1e-6, None, None, None)
+    assert st == 3
+    x = np.array([0.5, np.nan])
+    st, _ = _call_host(1, [x], np.ones(2, complex), (8,), 1e-6, 1, pinned=False)
+    assert st == 5  # DATA_ERROR
+    st, _ = _call_host(1, [np.array([0.5])], np.ones(1, complex), (8,), 1e-20, 1, pinned=False)
+    assert st == 1  # BAD_TOLERANCE
+    assert "tolerance" in _lib.last_error()
