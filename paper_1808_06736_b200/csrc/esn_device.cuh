@@ -578,7 +578,7 @@ __global__ void __launch_bounds__(1024) k_permute_strengths(SpreadArgs<T> a, con
 // cells (near-broadcast, conflict-light).  Output in ORIGINAL point order
 // (spreadinterp.py:453).
 template <typename T, int DIM, int W>
-__global__ void __launch_bounds__(256) k_interp_tile(SpreadArgs<T> a, T *cout, const T *gridp) {
+__global__ void __launch_bounds__(256, 2) k_interp_tile(SpreadArgs<T> a, T *cout, const T *gridp) {
     using C = typename Cx<T>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     C *patch = reinterpret_cast<C *>(smem_raw);
@@ -604,33 +604,48 @@ __global__ void __launch_bounds__(256) k_interp_tile(SpreadArgs<T> a, T *cout, c
         const int b3 = DIM > 2 ? bin / (a.g.nb[0] * a.g.nb[1]) : 0;
         const int lo1 = b1 * a.g.bs[0], lo2 = b2 * a.g.bs[1], lo3 = b3 * a.g.bs[2];
         const C *grid = reinterpret_cast<const C *>(gridp) + (int64_t)t * a.gstride;
-#pragma unroll 4
-        for (int i = tid; i < ncell; i += blockDim.x) {
-            const int q1 = i % P1;
-            const int r = i / P1;
-            const int q2 = DIM > 1 ? r % P2 : 0;
-            const int q3 = DIM > 2 ? r / P2 : 0;
-            int g1 = lo1 + q1;
-            while (g1 >= n1) g1 -= n1;
-            int64_t gi = g1;
-            if (DIM > 1) {
-                int g2 = lo2 + q2;
-                while (g2 >= n2) g2 -= n2;
-                gi += (int64_t)g2 * n1;
+        // patch: 4 independent loads in flight per thread, then the stores
+        for (int i0 = tid; i0 < ncell; i0 += 4 * blockDim.x) {
+            C v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * blockDim.x;
+                if (i >= ncell) break;
+                const int q1 = i % P1;
+                const int r = i / P1;
+                const int q2 = DIM > 1 ? r % P2 : 0;
+                const int q3 = DIM > 2 ? r / P2 : 0;
+                int g1 = lo1 + q1;
+                while (g1 >= n1) g1 -= n1;
+                int64_t gi = g1;
+                if (DIM > 1) {
+                    int g2 = lo2 + q2;
+                    while (g2 >= n2) g2 -= n2;
+                    gi += (int64_t)g2 * n1;
+                }
+                if (DIM > 2) {
+                    int g3 = lo3 + q3;
+                    while (g3 >= n3) g3 -= n3;
+                    gi += (int64_t)g3 * n2 * n1;
+                }
+                v[u] = __ldg(grid + gi);
             }
-            if (DIM > 2) {
-                int g3 = lo3 + q3;
-                while (g3 >= n3) g3 -= n3;
-                gi += (int64_t)g3 * n2 * n1;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * blockDim.x;
+                if (i < ncell) patch[i] = v[u];
             }
-            patch[i] = __ldg(grid + gi);
         }
         __syncthreads();
-        // records are prefetched one iteration ahead (the loop body is long)
-        Rec nxt = load_rec(a.rec, start + min(tid, cnt - 1));
-        for (int k = tid; k < cnt; k += blockDim.x) {
-            const Rec rc = nxt;
-            if (k + (int)blockDim.x < cnt) nxt = load_rec(a.rec, start + k + blockDim.x);
+        // records are prefetched two iterations ahead (the body is long but
+        // a global load still outlasts one iteration at this occupancy)
+        const int NTB = blockDim.x;
+        Rec nx1 = load_rec(a.rec, start + min(tid, cnt - 1));
+        Rec nx2 = load_rec(a.rec, start + min(tid + NTB, cnt - 1));
+        for (int k = tid; k < cnt; k += NTB) {
+            const Rec rc = nx1;
+            nx1 = nx2;
+            if (k + 2 * NTB < cnt) nx2 = load_rec(a.rec, start + k + 2 * NTB);
             T r1[W], r2[W], r3[W];
             int i1 = kernel_row<T, W>(rc.g[0], a.k, r1);
             const int o1 = (i1 < 0 ? i1 + n1 : i1) - lo1;
