@@ -55,6 +55,19 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def hot_kernel_name(cfg):
+    """The kernel the plan dispatches for this config's hot stage
+    (esn_inst.cuh: SpreadGlobalOp / SpreadRowsOp / SpreadBatchOp / InterpOp)."""
+    f32 = cfg.get("dtype", "float64") == "float32"
+    if cfg["ttype"] == 2:
+        return "k_interp_tile" if f32 else "k_interp_bulk"
+    if cfg["dim"] == 1:
+        return "k_spread_global"
+    if cfg["dim"] == 2 and f32 and cfg.get("ntransf", 1) > 1:
+        return "k_spread_batch2d"
+    return "k_spread_rows"
+
+
 def algorithmic_bytes(cfg, M, T):
     """B = M d s_r + T M s_c + T G s_c for the spread/interp."""
     sr = 8 if cfg["dtype"] == "float64" else 4
@@ -437,7 +450,7 @@ def main():
                     config=cb,
                     roofline={"bound": "hbm", "achieved": res["achieved"], "peak": res["peak"],
                               "unit": "GB/s", "frac": frac, "traffic": traffic,
-                              "kernel": f"{kern} (k_{'interp_tile' if kern == 'interp' else 'spread_rows / k_spread_batch2d'})",
+                              "kernel": f"{kern} ({hot_kernel_name(cfg)})",
                               "algorithmic_bytes": res["B"], "kernel_ms": res["hot_s"] * 1e3,
                               "peak_source": f"{res['peak_kind']} MEASURED_PEAKS.json hbm_gbs"},
                     stages_ms={k: v * 1e3 for k, v in res["stages"].items()},

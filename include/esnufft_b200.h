@@ -166,6 +166,12 @@ int esn_plan_bins(esn_plan p, int *nbins, int *bin_size, int *bins_per_dim);
  * original point), bin_start (nbins + 1 int32).  Replaces the
  * BinSortPermutation of grid.py:171-182. */
 int esn_plan_sort_view(esn_plan p, void *perm, void *keys, void *bin_start);
+/* Target chunks of a type-2 plan's sort order (set by esn_plan_setpts): with
+ * nchunk > 1 the points are ordered by (chunk of original indices, bin,
+ * sub-cell) so that one chunk's scattered outputs stay L2-resident while
+ * it is interpolated; results are identical to the plain bin order.
+ * esn_plan_sort_view is unavailable (SIZE_ERROR) on such a plan. */
+int esn_plan_target_chunks(esn_plan p, int *nchunk);
 /* Device scratch bytes held by the plan. */
 int64_t esn_plan_device_bytes(esn_plan p);
 int esn_plan_destroy(esn_plan p);

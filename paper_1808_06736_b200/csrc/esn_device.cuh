@@ -55,7 +55,13 @@ __device__ __forceinline__ int kernel_row(double g, const KernelTab<T> &k, T *ro
     // reference (spreadinterp.py:318, 329), then the plan dtype
     const int i0 = (int)floor(g - 0.5 * W + 1.0);
     if (k.use_exact) {
-        exact_row<T>(g, i0, W, k.beta, row);
+        // the out-of-line call writes a private scratch row; copying it keeps
+        // the caller's row[] in registers (passing row itself would force it
+        // to the stack on the hot Horner path as well)
+        T tmp[W];
+        exact_row<T>(g, i0, W, k.beta, tmp);
+#pragma unroll
+        for (int m = 0; m < W; ++m) row[m] = tmp[m];
     } else {
         const T t = (T)(2.0 * ((double)i0 - g) + (double)(W - 1));
 #pragma unroll
@@ -568,6 +574,13 @@ __global__ void __launch_bounds__(1024) k_permute_strengths(SpreadArgs<T> a, con
     }
 }
 
+constexpr int kInterpSlice = 1024;  // point records staged per slice (32 KB)
+
+// CTAs per SM the interpolators are register-capped for: 3 (<= 80 registers)
+// only where the body fits without spilling (2D, w <= 7)
+template <int DIM, int W>
+constexpr int interp_minb() { return (DIM == 2 && W <= 7) ? 3 : 2; }
+
 // ---------------------------------------------------------------------------
 // Tile interpolator (spreadinterp.py:442-507).  One CTA per subproblem
 // (persistent work queue): the bin's periodic patch of (bs + w - 1)^d fine
@@ -578,10 +591,11 @@ __global__ void __launch_bounds__(1024) k_permute_strengths(SpreadArgs<T> a, con
 // cells (near-broadcast, conflict-light).  Output in ORIGINAL point order
 // (spreadinterp.py:453).
 template <typename T, int DIM, int W>
-__global__ void __launch_bounds__(256, 2) k_interp_tile(SpreadArgs<T> a, T *cout, const T *gridp) {
+__global__ void __launch_bounds__(256, interp_minb<DIM, W>()) k_interp_tile(SpreadArgs<T> a, T *cout, const T *gridp) {
     using C = typename Cx<T>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    C *patch = reinterpret_cast<C *>(smem_raw);
+    Rec *s_rec = reinterpret_cast<Rec *>(smem_raw);               // kInterpSlice records
+    C *patch = reinterpret_cast<C *>(s_rec + kInterpSlice);
     __shared__ int s_sub;
     const int tid = threadIdx.x;
     const int n1 = a.g.n[0], n2 = a.g.n[1], n3 = a.g.n[2];
@@ -598,7 +612,7 @@ __global__ void __launch_bounds__(256, 2) k_interp_tile(SpreadArgs<T> a, T *cout
         if (s >= nwork) break;
         const int t = s / nsub;
         const int4 sp = a.subprob[s - t * nsub];
-        const int bin = sp.x, start = sp.y, cnt = sp.z;
+        const int bin = sp.x % (a.g.nb[0] * a.g.nb[1] * a.g.nb[2]), start = sp.y, cnt = sp.z;  // geometric bin
         const int b1 = bin % a.g.nb[0];
         const int b2 = DIM > 1 ? (bin / a.g.nb[0]) % a.g.nb[1] : 0;
         const int b3 = DIM > 2 ? bin / (a.g.nb[0] * a.g.nb[1]) : 0;
@@ -637,15 +651,25 @@ __global__ void __launch_bounds__(256, 2) k_interp_tile(SpreadArgs<T> a, T *cout
             }
         }
         __syncthreads();
-        // records are prefetched two iterations ahead (the body is long but
-        // a global load still outlasts one iteration at this occupancy)
-        const int NTB = blockDim.x;
-        Rec nx1 = load_rec(a.rec, start + min(tid, cnt - 1));
-        Rec nx2 = load_rec(a.rec, start + min(tid + NTB, cnt - 1));
-        for (int k = tid; k < cnt; k += NTB) {
-            const Rec rc = nx1;
-            nx1 = nx2;
-            if (k + 2 * NTB < cnt) nx2 = load_rec(a.rec, start + k + 2 * NTB);
+        // point records are staged slice by slice into shared memory with
+        // all threads' loads in flight at once (a per-thread prefetch chain
+        // cannot cover the DRAM latency at this loop length)
+        for (int s0 = 0; s0 < cnt; s0 += kInterpSlice) {
+        const int sn = min(kInterpSlice, cnt - s0);
+        __syncthreads();
+        {
+            // four independent 256-bit loads per thread, then the stores
+            Rec tmp[4];
+            const int nt = blockDim.x;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) tmp[u] = load_rec(a.rec, start + s0 + min(tid + u * nt, sn - 1));
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (tid + u * nt < sn) s_rec[tid + u * nt] = tmp[u];
+        }
+        __syncthreads();
+        for (int kk = tid; kk < sn; kk += blockDim.x) {
+            const Rec rc = s_rec[kk];
             T r1[W], r2[W], r3[W];
             int i1 = kernel_row<T, W>(rc.g[0], a.k, r1);
             const int o1 = (i1 < 0 ? i1 + n1 : i1) - lo1;
@@ -668,7 +692,9 @@ __global__ void __launch_bounds__(256, 2) k_interp_tile(SpreadArgs<T> a, T *cout
                 }
             } else if (DIM == 2) {
                 const C *base = patch + o2 * P1 + o1;
-#pragma unroll
+                // rows not unrolled: keeps ~W row loads in flight instead of
+                // W^2 (register budget -> 3 CTAs per SM)
+#pragma unroll 1
                 for (int m2 = 0; m2 < W; ++m2) {
                     T pre = 0, pim = 0;
 #pragma unroll
@@ -677,12 +703,16 @@ __global__ void __launch_bounds__(256, 2) k_interp_tile(SpreadArgs<T> a, T *cout
                         pre = fma(r1[m1], v.x, pre);
                         pim = fma(r1[m1], v.y, pim);
                     }
-                    are = fma(r2[m2], pre, are);
-                    aim = fma(r2[m2], pim, aim);
+                    T w2 = r2[0];
+#pragma unroll
+                    for (int q = 1; q < W; ++q) w2 = (q == m2) ? r2[q] : w2;
+                    are = fma(w2, pre, are);
+                    aim = fma(w2, pim, aim);
                 }
             } else {
                 const C *base = patch + (o3 * P2 + o2) * P1 + o1;
-#pragma unroll
+                // planes not unrolled (W^2 body per plane; fits the registers)
+#pragma unroll 1
                 for (int m3 = 0; m3 < W; ++m3) {
                     T p3re = 0, p3im = 0;
 #pragma unroll
@@ -697,13 +727,266 @@ __global__ void __launch_bounds__(256, 2) k_interp_tile(SpreadArgs<T> a, T *cout
                         p3re = fma(r2[m2], pre, p3re);
                         p3im = fma(r2[m2], pim, p3im);
                     }
-                    are = fma(r3[m3], p3re, are);
-                    aim = fma(r3[m3], p3im, aim);
+                    T w3 = r3[0];
+#pragma unroll
+                    for (int q = 1; q < W; ++q) w3 = (q == m3) ? r3[q] : w3;
+                    are = fma(w3, p3re, are);
+                    aim = fma(w3, p3im, aim);
                 }
             }
             reinterpret_cast<C *>(cout)[(int64_t)t * a.M + rc.j] = C{are, aim};
         }
+        }
         __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Asynchronous bulk copies (cp.async.bulk, global -> shared) completing on an
+// mbarrier: the copy engine moves bytes without registers or LSU issue slots.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                              uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// 16-byte store that asks L2 to keep the line (scattered outputs of one
+// target chunk merge into whole sectors there before write-back)
+__device__ __forceinline__ void st_keep(double2 *p, double2 v, uint64_t policy) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(policy)
+                 : "memory");
+}
+__device__ __forceinline__ void st_keep(float2 *p, float2 v, uint64_t policy) {
+    asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(p), "f"(v.x), "f"(v.y), "l"(policy)
+                 : "memory");
+}
+
+// One unit of interpolation work: a slice of one subproblem's point records.
+struct InterpUnit {
+    int valid, t, start, n;   // transform, first record, records in the slice
+    int lo1, lo2, lo3, pb;    // patch origin and the patch buffer holding it
+};
+
+// Pipelined tile interpolator (same arithmetic and output as k_interp_tile).
+// Work streams through a CTA as units (subproblem slices) in a two-slot
+// ring.  Warp 0 also produces: it queues unit i+1's records -- and, on a new
+// subproblem, its periodic patch row by row -- as bulk copies into the other
+// slot ("full" mbarrier, transaction-counted) once every warp has released
+// that slot ("empty" mbarrier, one arrival per warp).  No block-wide barrier:
+// a warp that finishes its share of a unit moves on to the next one, and
+// DRAM latency overlaps the fp64 work.  Records are fetched with an
+// evict-first L2 policy and outputs stored evict-last, so the scattered
+// outputs of one target chunk (see the plan's chunked sort key) merge into
+// whole sectors in L2.  Requires complex128 cells (16-byte rows) and
+// P_d <= n_d (each patch row wraps at most once).
+template <typename T, int DIM, int W>
+__global__ void __launch_bounds__(256, interp_minb<DIM, W>())
+    k_interp_bulk(SpreadArgs<T> a, T *cout, const T *gridp, int slice) {
+    using C = typename Cx<T>::type;
+    extern __shared__ __align__(16) unsigned char bulk_smem[];
+    __shared__ uint64_t s_full[2], s_empty[2];
+    __shared__ InterpUnit s_unit[2];
+    // producer state, touched by lane 0 of warp 0 only (kept in shared
+    // memory so it costs the compute threads no registers)
+    __shared__ int s_prod[8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nwarps = blockDim.x >> 5;
+    const int n1 = a.g.n[0], n2 = a.g.n[1], n3 = a.g.n[2];
+    const int P1 = a.g.bs[0] + W - 1;
+    const int P2 = DIM > 1 ? a.g.bs[1] + W - 1 : 1;
+    const int P3 = DIM > 2 ? a.g.bs[2] + W - 1 : 1;
+    const int ncell = P1 * P2 * P3;
+    Rec *const rec0 = reinterpret_cast<Rec *>(bulk_smem);              // 2 x slice records
+    C *const patch0 = reinterpret_cast<C *>(rec0 + 2 * slice);         // 2 x ncell cells
+    const int nsub = *a.nsub;
+    const int nwork = nsub * a.ntransf;
+    const int nbins_geo = a.g.nb[0] * a.g.nb[1] * a.g.nb[2];
+    const C *gridc = reinterpret_cast<const C *>(gridp);
+    int &p_start = s_prod[0], &p_cnt = s_prod[1], &p_off = s_prod[2], &p_pb = s_prod[3];
+    int &p_t = s_prod[4], &p_lo1 = s_prod[5], &p_lo2 = s_prod[6], &p_lo3 = s_prod[7];
+    int p_next = 0;  // (lane 0 of warp 0) work index claimed one subproblem ahead
+
+    // warp 0: choose unit k and queue its copies into slot k & 1
+    auto produce = [&](int k) -> int {
+        const int rb = k & 1;
+        if (k >= 2) mbar_wait(&s_empty[rb], ((k >> 1) - 1) & 1);  // every warp released unit k - 2
+        int fresh = 0, valid = 0;
+        InterpUnit u;
+        if (lane == 0) {
+            while (p_off >= p_cnt) {
+                const int s = p_next;
+                if (s >= nwork) { p_cnt = -1; break; }
+                p_next = atomicAdd(a.work, 1);
+                p_t = s / nsub;
+                const int4 sp = a.subprob[s - p_t * nsub];
+                const int bin = sp.x % nbins_geo;  // geometric bin (key major part = target chunk)
+                p_start = sp.y; p_cnt = sp.z; p_off = 0; fresh = 1;
+                const int b1 = bin % a.g.nb[0];
+                const int b2 = DIM > 1 ? (bin / a.g.nb[0]) % a.g.nb[1] : 0;
+                const int b3 = DIM > 2 ? bin / (a.g.nb[0] * a.g.nb[1]) : 0;
+                p_lo1 = b1 * a.g.bs[0]; p_lo2 = b2 * a.g.bs[1]; p_lo3 = b3 * a.g.bs[2];
+            }
+            if (p_cnt < 0) {
+                u.valid = 0;
+                p_cnt = 0; p_off = 0; fresh = 0;
+            } else {
+                if (fresh) p_pb ^= 1;  // the patch slot the previous subproblem did not use
+                u.valid = 1; u.t = p_t; u.start = p_start + p_off; u.n = min(slice, p_cnt - p_off);
+                u.lo1 = p_lo1; u.lo2 = p_lo2; u.lo3 = p_lo3; u.pb = p_pb;
+                p_off += slice;
+            }
+            valid = u.valid;
+            s_unit[rb] = u;
+            // arrival (release) publishes s_unit[rb]; the phase completes when
+            // the copies' bytes have landed
+            mbar_expect_tx(&s_full[rb], valid ? (uint32_t)u.n * sizeof(Rec) + (fresh ? (uint32_t)ncell * sizeof(C) : 0u)
+                                              : 0u);
+        }
+        fresh = __shfl_sync(0xffffffffu, fresh, 0);
+        valid = __shfl_sync(0xffffffffu, valid, 0);
+        if (!valid) return 0;
+        if (lane == 0)
+            bulk_g2s_hint(rec0 + rb * slice, a.rec + u.start, (uint32_t)u.n * sizeof(Rec), &s_full[rb],
+                          policy_evict_first());  // records stream through once
+        if (fresh) {
+            __syncwarp();
+            const int t = p_t, lo1 = p_lo1, lo2 = p_lo2, lo3 = p_lo3, pb = p_pb;
+            const C *grid = gridc + (int64_t)t * a.gstride;
+            const int head = min(P1, n1 - lo1);  // cells before the x wrap
+            for (int r = lane; r < P2 * P3; r += 32) {
+                const int q2 = DIM > 1 ? r % P2 : 0;
+                const int q3 = DIM > 2 ? r / P2 : 0;
+                int g2 = lo2 + q2, g3 = lo3 + q3;
+                if (g2 >= n2) g2 -= n2;
+                if (g3 >= n3) g3 -= n3;
+                const C *row = grid + ((int64_t)g3 * n2 + g2) * n1;
+                C *dst = patch0 + pb * ncell + r * P1;
+                bulk_g2s(dst, row + lo1, (uint32_t)head * sizeof(C), &s_full[rb]);
+                if (head < P1) bulk_g2s(dst + head, row, (uint32_t)(P1 - head) * sizeof(C), &s_full[rb]);
+            }
+        }
+        return 1;
+    };
+
+    if (tid == 0) {
+        p_start = p_cnt = p_off = p_t = p_lo1 = p_lo2 = p_lo3 = 0;
+        p_pb = 1;
+        mbar_init(&s_full[0], 1);
+        mbar_init(&s_full[1], 1);
+        mbar_init(&s_empty[0], nwarps);
+        mbar_init(&s_empty[1], nwarps);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (tid == 0) p_next = atomicAdd(a.work, 1);
+    __syncthreads();
+    int producing = warp == 0 ? produce(0) : 0;
+    const uint64_t keep = policy_evict_last();
+    for (int k = 0;; ++k) {
+        const int rb = k & 1;
+        if (producing) producing = produce(k + 1);
+        mbar_wait(&s_full[rb], (k >> 1) & 1);
+        const InterpUnit u = s_unit[rb];
+        if (!u.valid) break;
+        const Rec *recs = rec0 + rb * slice;
+        const C *patch = patch0 + u.pb * ncell;
+        for (int kk = tid; kk < u.n; kk += blockDim.x) {
+            const Rec rc = recs[kk];
+            T r1[W], r2[W], r3[W];
+            const int i1 = kernel_row<T, W>(rc.g[0], a.k, r1);
+            const int o1 = (i1 < 0 ? i1 + n1 : i1) - u.lo1;
+            int o2 = 0, o3 = 0;
+            if (DIM > 1) {
+                const int i2 = kernel_row<T, W>(rc.g[1], a.k, r2);
+                o2 = (i2 < 0 ? i2 + n2 : i2) - u.lo2;
+            }
+            if (DIM > 2) {
+                const int i3 = kernel_row<T, W>(rc.g[2], a.k, r3);
+                o3 = (i3 < 0 ? i3 + n3 : i3) - u.lo3;
+            }
+            T are = 0, aim = 0;
+            const C *base = patch + (o3 * P2 + o2) * P1 + o1;
+#pragma unroll 1
+            for (int m3 = 0; m3 < (DIM > 2 ? W : 1); ++m3) {
+                T p3re = 0, p3im = 0;
+#pragma unroll 1
+                for (int m2 = 0; m2 < (DIM > 1 ? W : 1); ++m2) {
+                    T pre = 0, pim = 0;
+#pragma unroll
+                    for (int m1 = 0; m1 < W; ++m1) {
+                        const C v = base[(m3 * P2 + m2) * P1 + m1];
+                        pre = fma(r1[m1], v.x, pre);
+                        pim = fma(r1[m1], v.y, pim);
+                    }
+                    if (DIM > 1) {
+                        T w2 = r2[0];
+#pragma unroll
+                        for (int q = 1; q < W; ++q) w2 = (q == m2) ? r2[q] : w2;
+                        p3re = fma(w2, pre, p3re);
+                        p3im = fma(w2, pim, p3im);
+                    } else {
+                        p3re = pre;
+                        p3im = pim;
+                    }
+                }
+                if (DIM > 2) {
+                    T w3 = r3[0];
+#pragma unroll
+                    for (int q = 1; q < W; ++q) w3 = (q == m3) ? r3[q] : w3;
+                    are = fma(w3, p3re, are);
+                    aim = fma(w3, p3im, aim);
+                } else {
+                    are = p3re;
+                    aim = p3im;
+                }
+            }
+            st_keep(reinterpret_cast<C *>(cout) + (int64_t)u.t * a.M + rc.j, C{are, aim}, keep);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[rb]);
     }
 }
 
@@ -714,7 +997,7 @@ __global__ void __launch_bounds__(256, 2) k_interp_tile(SpreadArgs<T> a, T *cout
 // few cache lines; separable weighted sum in registers (w^(d-1) row partial
 // sums), output in ORIGINAL point order (spreadinterp.py:453).
 template <typename T, int DIM, int W>
-__global__ void __launch_bounds__(256, 3) k_interp_thread(SpreadArgs<T> a, T *cout, const T *gridp) {
+__global__ void __launch_bounds__(256, 2) k_interp_thread(SpreadArgs<T> a, T *cout, const T *gridp) {
     using C = typename Cx<T>::type;
     const int n1 = a.g.n[0], n2 = a.g.n[1], n3 = a.g.n[2];
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < a.M;

@@ -108,8 +108,31 @@ struct InterpOp {
         }
         using C = typename Cx<T>::type;
         size_t cells = 1;
-        for (int d = 0; d < D; ++d) cells *= (size_t)(a.g.bs[d] + W - 1);
-        const size_t smem = cells * sizeof(C);
+        bool fits = true;  // every patch row wraps at most once
+        for (int d = 0; d < D; ++d) {
+            cells *= (size_t)(a.g.bs[d] + W - 1);
+            fits = fits && a.g.bs[d] + W - 1 <= a.g.n[d];
+        }
+        if constexpr (sizeof(C) == 16) if (fits && !(mode && std::string(mode) == "tile")) {
+            static const char *sl = getenv("ESN_INTERP_SLICE");
+            const int slice = sl ? atoi(sl) : 512;
+            const size_t bsmem = 2 * cells * sizeof(C) + 2 * (size_t)slice * sizeof(Rec);
+            if (bsmem <= 112 * 1024) {
+                static size_t bconfigured = 0;
+                if (bsmem > bconfigured) {
+                    ESN_CUDA_TRY(cudaFuncSetAttribute(k_interp_bulk<T, D, W>,
+                                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem));
+                    bconfigured = bsmem;
+                }
+                int occ = 0;
+                ESN_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_interp_bulk<T, D, W>, 256, bsmem));
+                if (occ < 1) occ = 1;
+                k_interp_bulk<T, D, W><<<device_sm_count() * occ, 256, bsmem, st>>>(a, cout, grid, slice);
+                ESN_CUDA_TRY(cudaGetLastError());
+                return ESN_SUCCESS;
+            }
+        }
+        const size_t smem = cells * sizeof(C) + kInterpSlice * sizeof(Rec);
         if (smem > 200 * 1024) {  // patch too large for shared memory: L1 path
             k_interp_thread<T, D, W><<<grid_for(a.M, 256), 256, 0, st>>>(a, cout, grid);
             ESN_CUDA_TRY(cudaGetLastError());

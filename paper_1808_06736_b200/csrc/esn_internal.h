@@ -62,7 +62,9 @@ struct SetptsArgs {
     Geom g;
     int sbl[3];             // log2 of the sub-bin size per dim (fine sort key)
     int spb;                // sub-bins per bin
-    int nkeys;              // nbins * spb
+    int nkeys;              // nchunk * nbins * spb
+    int nbins_geo;          // geometric bins
+    int64_t chunk_len;      // > 0: points per target chunk (key major part)
     double inv_bs[3];       // 1 / bs (fast division, corrected exactly)
     int64_t M;
     int coord_f32;          // input coordinates are float (else double)
@@ -113,7 +115,7 @@ struct RowsCfg {
     static constexpr int BY = RY - W + 1;
     static constexpr int BZ = DIM == 3 ? RZ - W + 1 : 1;
     static constexpr int CH = NT;  // staged points per chunk (one per thread)
-    static constexpr int MINB = (sizeof(T) == 8 && DIM == 3) ? 2 : 1;
+    static constexpr int MINB = DIM == 3 ? 2 : 1;  // two CTAs per SM (<= 128 registers)
 };
 
 template <typename T, int W>

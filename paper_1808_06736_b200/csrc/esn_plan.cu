@@ -102,6 +102,12 @@ struct esn_plan_s {
     int *cursor = nullptr, *key_count = nullptr, *block_sums = nullptr;
     int *bin_start = nullptr, *subofs = nullptr, *nsub = nullptr, *work = nullptr;
     int sbl[3] = {0, 0, 0}, spb = 1, nkeys = 1;
+    // type-2 target chunks: the sort key is (chunk of original indices, bin,
+    // sub-cell), so the interpolator's scattered output writes of one chunk
+    // land in an L2-sized window and merge into whole sectors there
+    int nchunk = 1, nbk = 1;          // chunks; sort bins = nchunk * nbins
+    int64_t chunk_len = 0;            // points per chunk (0: unchunked)
+    int keycap = 0, bincap = 0;       // allocated key / sort-bin capacity
     int4 *subprob = nullptr;
     unsigned long long *flags = nullptr;
     void *grid = nullptr;
@@ -132,6 +138,30 @@ static void dfree(void *ptr) {
     if (ptr) cudaFree(ptr);
 }
 
+// (re)allocate the key-space arrays when the key space / sort-bin count grew
+static int ensure_key_space(esn_plan p) {
+    int rc;
+    if (p->nkeys > p->keycap) {
+        dfree(p->key_count);
+        dfree(p->cursor);
+        dfree(p->block_sums);
+        p->key_count = p->cursor = p->block_sums = nullptr;
+        if ((rc = dmalloc(p, &p->key_count, sizeof(int) * p->nkeys))) return rc;
+        if ((rc = dmalloc(p, &p->cursor, sizeof(int) * p->nkeys))) return rc;
+        if ((rc = dmalloc(p, &p->block_sums, sizeof(int) * ((p->nkeys + kScanTile - 1) / kScanTile + 1)))) return rc;
+        p->keycap = p->nkeys;
+    }
+    if (p->nbk > p->bincap) {
+        dfree(p->bin_start);
+        dfree(p->subofs);
+        p->bin_start = p->subofs = nullptr;
+        if ((rc = dmalloc(p, &p->bin_start, sizeof(int) * (p->nbk + 1)))) return rc;
+        if ((rc = dmalloc(p, &p->subofs, sizeof(int) * (p->nbk + 1)))) return rc;
+        p->bincap = p->nbk;
+    }
+    return ESN_SUCCESS;
+}
+
 template <int W>
 static void rows_bins(int dtype, int dim, int ntransf, int *bs) {
     if (dim == 3) {
@@ -160,6 +190,8 @@ int esn::spreader_bins(int method, int dtype, int dim, int w, int ntransf, int *
     }
     return 0;
 }
+
+static void set_key_space(esn_plan p, int nchunk);
 
 static void choose_bins(esn_plan p) {
     const int dim = p->dim, w = p->kp.w;
@@ -208,11 +240,19 @@ static void choose_bins(esn_plan p) {
     }
     p->geom.dim = dim;
     p->geom.w = w;
-    // fine sort key: sub-cells of 2^sbl cells inside each bin, coarsened
-    // (fastest dims first) until the key space is <= 8M entries
+    set_key_space(p, 1);
+}
+
+// fine sort key: sub-cells of 2^sbl cells inside each bin, coarsened
+// (fastest dims first) until the key space (nchunk * nbins * sub-cells) is
+// <= 8M entries
+static void set_key_space(esn_plan p, int nchunk) {
+    const int dim = p->dim;
+    p->nchunk = nchunk;
+    p->nbk = p->nbins * nchunk;
     for (int d = 0; d < 3; ++d) p->sbl[d] = 0;
     auto keys = [&]() {
-        int64_t k = p->nbins;
+        int64_t k = p->nbk;
         for (int d = 0; d < dim; ++d) k *= (p->geom.bs[d] >> p->sbl[d]);
         return k;
     };
@@ -260,11 +300,7 @@ static int plan_common_init(esn_plan p, const esn_opts *o) {
     choose_bins(p);
     p->maxsub = p->opts.max_subprob > 0 ? p->opts.max_subprob : 8192;
     int rc;
-    if ((rc = dmalloc(p, &p->key_count, sizeof(int) * p->nkeys))) return rc;
-    if ((rc = dmalloc(p, &p->cursor, sizeof(int) * p->nkeys))) return rc;
-    if ((rc = dmalloc(p, &p->block_sums, sizeof(int) * ((p->nkeys + kScanTile - 1) / kScanTile + 1)))) return rc;
-    if ((rc = dmalloc(p, &p->bin_start, sizeof(int) * (p->nbins + 1)))) return rc;
-    if ((rc = dmalloc(p, &p->subofs, sizeof(int) * (p->nbins + 1)))) return rc;
+    if ((rc = ensure_key_space(p))) return rc;
     if ((rc = dmalloc(p, &p->nsub, sizeof(int) * 2))) return rc;
     if ((rc = dmalloc(p, &p->work, sizeof(int) * 2))) return rc;
     if ((rc = dmalloc(p, &p->flags, sizeof(unsigned long long) * 8))) return rc;
@@ -459,7 +495,27 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
         if ((rc = dmalloc(p, &p->prank, sizeof(int) * M))) return rc;
         p->Mcap = M;
     }
-    const int64_t subneed = p->nbins + M / p->maxsub + 1;
+    if (p->type == 2) {
+        // target chunks sized so one chunk's outputs (all transforms) stay
+        // well inside L2 while it is being interpolated
+        static const char *env = getenv("ESN_OUT_CHUNK_MB");
+        static const double l2mb = [] {
+            int dev = 0, l2 = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+            return l2 > 0 ? 0.75 * l2 / 1048576.0 : 64.0;
+        }();
+        const double mb = env ? atof(env) : l2mb;
+        const double out_bytes = (double)M * real_size(p->dtype) * 2;
+        int h = mb > 0 ? (int)std::ceil(out_bytes / (mb * 1048576.0)) : 1;
+        h = std::max(1, std::min({h, 64, std::max(1, (8 << 20) / p->nbins)}));
+        if (h != p->nchunk) {
+            set_key_space(p, h);
+            if ((rc = ensure_key_space(p))) return rc;
+        }
+        p->chunk_len = h > 1 ? (M + h - 1) / h : 0;
+    }
+    const int64_t subneed = p->nbk + M / p->maxsub + 1;
     if (subneed > p->subcap) {
         dfree(p->subprob);
         p->subprob = nullptr;
@@ -486,6 +542,8 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
     }
     a.spb = p->spb;
     a.nkeys = p->nkeys;
+    a.nbins_geo = p->nbins;
+    a.chunk_len = p->chunk_len;
     a.key_count = p->key_count;
     a.block_sums = p->block_sums;
     a.bin_start = p->bin_start;
@@ -495,7 +553,7 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
     a.rec = p->rec;
     a.flags = p->flags;
     a.check_bounds = p->opts.check_bounds;
-    if ((rc = launch_setpts(a, p->nbins, p->maxsub, p->subprob, p->nsub, p->subofs, p->st))) return rc;
+    if ((rc = launch_setpts(a, p->nbk, p->maxsub, p->subprob, p->nsub, p->subofs, p->st))) return rc;
     if (p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[1], p->st));
     p->points_set = true;
     return ESN_SUCCESS;
@@ -534,7 +592,12 @@ bool esn::batched_spread(int dtype, int dim, int w, int ntransf, int method) {
 }
 
 static int do_spread(esn_plan p, const void *c, void *grid, bool zero = true) {
-    if (esn::batched_spread(p->dtype, p->dim, p->kp.w, p->ntransf, p->method)) {
+    // the bin-structured spreaders need their own bin geometry and the
+    // geometric sort; a type-2 plan (interpolation bins, possibly a
+    // target-chunked order) spreads its adjoint with the order-agnostic
+    // spreader
+    const int method = p->type == 2 ? ESN_METHOD_GLOBAL : p->method;
+    if (esn::batched_spread(p->dtype, p->dim, p->kp.w, p->ntransf, method)) {
         // permuted strengths + per-point rows table (<= 96 B per point)
         const int64_t need = (int64_t)((p->ntransf + 31) / 32) * 32 * p->M * (int64_t)real_size(p->dtype) * 2 +
                              96 * p->M + 256;
@@ -550,9 +613,9 @@ static int do_spread(esn_plan p, const void *c, void *grid, bool zero = true) {
     ESN_CUDA_TRY(cudaMemsetAsync(p->work, 0, sizeof(int), p->st));
     if (p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[6], p->st));
     int rc = p->dtype == ESN_F64
-                 ? launch_spread<double>(make_spread_args<double>(p, c, grid), p->method, p->nbins, p->pkey,
+                 ? launch_spread<double>(make_spread_args<double>(p, c, grid), method, p->nbins, p->pkey,
                                          p->prank, p->cursor, (double *)p->cperm, p->st)
-                 : launch_spread<float>(make_spread_args<float>(p, c, grid), p->method, p->nbins, p->pkey,
+                 : launch_spread<float>(make_spread_args<float>(p, c, grid), method, p->nbins, p->pkey,
                                         p->prank, p->cursor, (float *)p->cperm, p->st);
     if (!rc && p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[7], p->st));
     return rc;
@@ -715,11 +778,18 @@ int esn_plan_bins(esn_plan p, int *nbins, int *bin_size, int *bins_per_dim) {
 
 int esn_plan_sort_view(esn_plan p, void *perm, void *keys, void *bin_start) {
     if (!p || !p->points_set) return fail(ESN_SIZE_ERROR, "plan has no points");
+    if (p->nchunk > 1) return fail(ESN_SIZE_ERROR, "sort view needs a spreader plan (this plan's order is target-chunked)");
     int rc = launch_sort_view(p->dtype, p->rec, p->bin_start, p->nbins, p->M, (int *)perm, (int *)keys, p->st);
     if (rc) return rc;
     if (bin_start)
         ESN_CUDA_TRY(cudaMemcpyAsync(bin_start, p->bin_start, sizeof(int) * (p->nbins + 1),
                                      cudaMemcpyDeviceToDevice, p->st));
+    return ESN_SUCCESS;
+}
+
+int esn_plan_target_chunks(esn_plan p, int *nchunk) {
+    if (!p) return fail(ESN_SIZE_ERROR, "null plan");
+    if (nchunk) *nchunk = p->nchunk;
     return ESN_SUCCESS;
 }
 
@@ -777,11 +847,9 @@ static int clone_point_plan(esn_plan main, cudaStream_t st, esn_plan *out) {
     p->grid = main->grid;
     p->borrowed = true;
     int rc;
-    if ((rc = dmalloc(p, &p->key_count, sizeof(int) * p->nkeys)) ||
-        (rc = dmalloc(p, &p->cursor, sizeof(int) * p->nkeys)) ||
-        (rc = dmalloc(p, &p->block_sums, sizeof(int) * ((p->nkeys + kScanTile - 1) / kScanTile + 1))) ||
-        (rc = dmalloc(p, &p->bin_start, sizeof(int) * (p->nbins + 1))) ||
-        (rc = dmalloc(p, &p->subofs, sizeof(int) * (p->nbins + 1))) || (rc = dmalloc(p, &p->nsub, sizeof(int) * 2)) ||
+    p->nchunk = main->nchunk;
+    p->nbk = main->nbk;
+    if ((rc = ensure_key_space(p)) || (rc = dmalloc(p, &p->nsub, sizeof(int) * 2)) ||
         (rc = dmalloc(p, &p->work, sizeof(int) * 2)) ||
         (rc = dmalloc(p, &p->flags, sizeof(unsigned long long) * 8))) {
         esn_plan_destroy(p);

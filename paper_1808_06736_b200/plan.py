@@ -170,6 +170,12 @@ class Plan:
         _lib.check(_lib.lib.esn_plan_sort_view(self.h, _ptr(perm), _ptr(keys), _ptr(start)))
         return perm, keys, start
 
+    def target_chunks(self) -> int:
+        """Target chunks of a type-2 plan's sort order (1 = plain bin order)."""
+        n = ctypes.c_int()
+        _lib.check(_lib.lib.esn_plan_target_chunks(self.h, ctypes.byref(n)))
+        return int(n.value)
+
     def device_bytes(self) -> int:
         return int(_lib.lib.esn_plan_device_bytes(self.h))
 
