@@ -438,7 +438,11 @@ def main():
             except Exception:
                 traffic = None
         kern = "interp" if cfg["ttype"] == 2 else "spread"
-        n_launch = 4 + 2  # setpts: bin, scan, scatter, subproblem fill; + amplify/spread, deconv/interp
+        # our kernels per step: setpts = count, scan x3, pos, scatter, subproblem
+        # scan + fill (8); type 2: amplify + interp; type 1: spread (batched:
+        # permute + row table + spread) + deconv.  cuFFT's own kernels excluded.
+        hk = hot_kernel_name(cfg)
+        n_launch = 8 + (2 if cfg["ttype"] == 2 else (3 if hk == "k_spread_batch2d" else 1) + 1)
         cb = config_block(args.config, world)
         if res["mode"] == "points":
             cb["parallelism"] = f"points split x{world}, NCCL reduce of the partial modes"

@@ -15,6 +15,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <chrono>
 #include <tuple>
 #include <vector>
 
@@ -108,6 +109,7 @@ struct esn_plan_s {
     int nchunk = 1, nbk = 1;          // chunks; sort bins = nchunk * nbins
     int64_t chunk_len = 0;            // points per chunk (0: unchunked)
     int keycap = 0, bincap = 0;       // allocated key / sort-bin capacity
+    int64_t keycap_req = (int64_t)8 << 20;  // key-space limit the current sbl was chosen for
     int4 *subprob = nullptr;
     unsigned long long *flags = nullptr;
     void *grid = nullptr;
@@ -191,7 +193,7 @@ int esn::spreader_bins(int method, int dtype, int dim, int w, int ntransf, int *
     return 0;
 }
 
-static void set_key_space(esn_plan p, int nchunk);
+static void set_key_space(esn_plan p, int nchunk, int64_t maxkeys = (int64_t)8 << 20);
 
 static void choose_bins(esn_plan p) {
     const int dim = p->dim, w = p->kp.w;
@@ -246,7 +248,7 @@ static void choose_bins(esn_plan p) {
 // fine sort key: sub-cells of 2^sbl cells inside each bin, coarsened
 // (fastest dims first) until the key space (nchunk * nbins * sub-cells) is
 // <= 8M entries
-static void set_key_space(esn_plan p, int nchunk) {
+static void set_key_space(esn_plan p, int nchunk, int64_t maxkeys) {
     const int dim = p->dim;
     p->nchunk = nchunk;
     p->nbk = p->nbins * nchunk;
@@ -256,9 +258,9 @@ static void set_key_space(esn_plan p, int nchunk) {
         for (int d = 0; d < dim; ++d) k *= (p->geom.bs[d] >> p->sbl[d]);
         return k;
     };
-    for (int guard = 0; guard < 64 && keys() > (int64_t)8 << 20; ++guard) {
+    for (int guard = 0; guard < 64 && keys() > maxkeys; ++guard) {
         bool grew = false;
-        for (int d = 0; d < dim && keys() > (int64_t)8 << 20; ++d) {
+        for (int d = 0; d < dim && keys() > maxkeys; ++d) {
             const int s2 = 1 << (p->sbl[d] + 1);
             if (p->geom.bs[d] % s2 == 0) {
                 p->sbl[d]++;
@@ -509,8 +511,12 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
         const double out_bytes = (double)M * real_size(p->dtype) * 2;
         int h = mb > 0 ? (int)std::ceil(out_bytes / (mb * 1048576.0)) : 1;
         h = std::max(1, std::min({h, 64, std::max(1, (8 << 20) / p->nbins)}));
-        if (h != p->nchunk) {
-            set_key_space(p, h);
+        // the interpolator only needs bins; sub-cells beyond ~2 keys per
+        // point cost key-space work (memset + scans) for nothing
+        const int64_t maxkeys = std::min<int64_t>((int64_t)8 << 20, std::max<int64_t>(2 * M, 1 << 16));
+        if (h != p->nchunk || maxkeys != p->keycap_req) {
+            set_key_space(p, h, maxkeys);
+            p->keycap_req = maxkeys;
             if ((rc = ensure_key_space(p))) return rc;
         }
         p->chunk_len = h > 1 ? (M + h - 1) / h : 0;
@@ -866,10 +872,16 @@ struct HostSlot {
     double tol, sigma;
     int method;
     esn_plan plan = nullptr;
-    static constexpr int NH = 4;  // pipeline helpers / streams
+    static constexpr int NH = 8;  // pipeline helpers / streams (capacity)
     esn_plan helper[NH] = {};
     cudaStream_t hst[NH] = {};
     cudaEvent_t ev_grid = nullptr, ev_done[NH] = {};
+    // transfer streams: every H2D goes through `up` (back to back, in chunk
+    // order), every D2H through `down`; per-chunk events link them to the
+    // compute streams so neither copy engine waits behind kernels
+    static constexpr int KC = 64;  // chunk capacity
+    cudaStream_t up = nullptr, down = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_up[KC] = {}, ev_comp[KC] = {}, ev_down = nullptr;
     void *dx[3] = {nullptr, nullptr, nullptr};
     void *dc = nullptr, *df = nullptr;
     int64_t Mcap = 0;
@@ -885,6 +897,14 @@ void free_slot(HostSlot &s) {
         if (s.ev_done[h]) cudaEventDestroy(s.ev_done[h]);
     }
     if (s.ev_grid) cudaEventDestroy(s.ev_grid);
+    for (int k = 0; k < HostSlot::KC; ++k) {
+        if (s.ev_up[k]) cudaEventDestroy(s.ev_up[k]);
+        if (s.ev_comp[k]) cudaEventDestroy(s.ev_comp[k]);
+    }
+    if (s.ev_in) cudaEventDestroy(s.ev_in);
+    if (s.ev_down) cudaEventDestroy(s.ev_down);
+    if (s.up) cudaStreamDestroy(s.up);
+    if (s.down) cudaStreamDestroy(s.down);
     if (s.plan) esn_plan_destroy(s.plan);
     for (int d = 0; d < 3; ++d) dfree(s.dx[d]);
     dfree(s.dc);
@@ -907,6 +927,12 @@ bool is_pinned(const void *ptr) {
 static int copy_rows(void *dst, const void *src, int64_t M_dst, int64_t M_src, int64_t lo_dst, int64_t lo_src,
                      int64_t cnt, int T, size_t cb, cudaMemcpyKind kind, cudaStream_t st) {
     if (cnt <= 0) return ESN_SUCCESS;
+    if (T == 1) {
+        if (cudaMemcpyAsync((char *)dst + lo_dst * cb, (const char *)src + lo_src * cb, cnt * cb, kind, st) !=
+            cudaSuccess)
+            return fail(ESN_INTERNAL_ERROR, "copy failed (%s)", cudaGetErrorString(cudaGetLastError()));
+        return ESN_SUCCESS;
+    }
     if (cudaMemcpy2DAsync((char *)dst + lo_dst * cb, M_dst * cb, (const char *)src + lo_src * cb, M_src * cb,
                           cnt * cb, T, kind, st) != cudaSuccess)
         return fail(ESN_INTERNAL_ERROR, "strided copy failed (%s)", cudaGetErrorString(cudaGetLastError()));
@@ -915,9 +941,18 @@ static int copy_rows(void *dst, const void *src, int64_t M_dst, int64_t M_src, i
 
 static int pipelined(HostSlot *slot, int type, int dim, int64_t M, const double *const *xs, int T, void *c, void *f,
                      int64_t nm, size_t cb) {
+    const auto t_start = std::chrono::steady_clock::now();
     esn_plan p = slot->plan;
     int rc;
-    constexpr int NH = HostSlot::NH;
+    static const int NH = [] {  // helpers / compute streams in use
+        const char *e = getenv("ESN_PIPE_STREAMS");
+        const int v = e ? atoi(e) : 4;
+        return std::max(1, std::min(v, HostSlot::NH));
+    }();
+    static const int KMAX = [] {
+        const char *e = getenv("ESN_PIPE_CHUNKS");
+        return std::max(1, std::min(e ? atoi(e) : 12, HostSlot::KC));
+    }();
     for (int h = 0; h < NH; ++h) {
         if (!slot->hst[h]) {
             ESN_CUDA_TRY(cudaStreamCreateWithFlags(&slot->hst[h], cudaStreamNonBlocking));
@@ -925,10 +960,47 @@ static int pipelined(HostSlot *slot, int type, int dim, int64_t M, const double 
         }
         if (!slot->helper[h] && (rc = clone_point_plan(p, slot->hst[h], &slot->helper[h]))) return rc;
     }
-    if (!slot->ev_grid) ESN_CUDA_TRY(cudaEventCreateWithFlags(&slot->ev_grid, cudaEventDisableTiming));
-    cudaStream_t st = p->st;
-    const int K = (int)std::min<int64_t>(16, (M + (1 << 19) - 1) >> 19);
-    const int64_t chunk = (M + K - 1) / K;
+    if (!slot->up) {
+        ESN_CUDA_TRY(cudaStreamCreateWithFlags(&slot->up, cudaStreamNonBlocking));
+        ESN_CUDA_TRY(cudaStreamCreateWithFlags(&slot->down, cudaStreamNonBlocking));
+        ESN_CUDA_TRY(cudaEventCreateWithFlags(&slot->ev_grid, cudaEventDisableTiming));
+        ESN_CUDA_TRY(cudaEventCreateWithFlags(&slot->ev_in, cudaEventDisableTiming));
+        ESN_CUDA_TRY(cudaEventCreateWithFlags(&slot->ev_down, cudaEventDisableTiming));
+        for (int k = 0; k < HostSlot::KC; ++k) {
+            ESN_CUDA_TRY(cudaEventCreateWithFlags(&slot->ev_up[k], cudaEventDisableTiming));
+            ESN_CUDA_TRY(cudaEventCreateWithFlags(&slot->ev_comp[k], cudaEventDisableTiming));
+        }
+    }
+    cudaStream_t st = p->st, up = slot->up, down = slot->down;
+    static const bool trace = getenv("ESN_TRACE") != nullptr;
+    static cudaEvent_t tev[4][HostSlot::KC + 1];  // start, up, comp, down
+    static bool tev_init = false;
+    if (trace && !tev_init) {
+        for (auto &row : tev)
+            for (auto &e : row) cudaEventCreate(&e);
+        tev_init = true;
+    }
+    if (trace) cudaEventRecord(tev[0][0], st);
+    const int K = (int)std::min<int64_t>(KMAX, (M + (1 << 19) - 1) >> 19);
+    // chunk boundaries: short first chunks (compute and the download start
+    // early) and geometrically shrinking last ones (short tail after the
+    // final upload); equal chunks in between
+    int64_t bound[HostSlot::KC + 1];
+    {
+        double w[HostSlot::KC], wsum = 0;
+        for (int k = 0; k < K; ++k) w[k] = 1.0;
+        if (K >= 6) {
+            w[0] = 0.25; w[1] = 0.5;
+            w[K - 3] = 0.5; w[K - 2] = 0.25; w[K - 1] = 0.125;
+        }
+        for (int k = 0; k < K; ++k) wsum += w[k];
+        double acc = 0;
+        bound[0] = 0;
+        for (int k = 0; k < K; ++k) {
+            acc += w[k];
+            bound[k + 1] = k == K - 1 ? M : std::min<int64_t>(M, (int64_t)std::llround(M * (acc / wsum)));
+        }
+    }
     // main stream: error flags, then type 2: modes in + amplify + FFT;
     // type 1: zero the shared grid
     ESN_CUDA_TRY(cudaMemsetAsync(p->flags, 0xff, sizeof(unsigned long long) * 8, st));
@@ -936,9 +1008,15 @@ static int pipelined(HostSlot *slot, int type, int dim, int64_t M, const double 
         ESN_CUDA_TRY(cudaMemsetAsync(slot->helper[h]->flags, 0xff, sizeof(unsigned long long) * 8, slot->hst[h]));
         slot->helper[h]->keep_flags = true;
     }
+    // the transfer streams start after everything queued before this call
+    ESN_CUDA_TRY(cudaEventRecord(slot->ev_in, st));
+    ESN_CUDA_TRY(cudaStreamWaitEvent(up, slot->ev_in, 0));
+    ESN_CUDA_TRY(cudaStreamWaitEvent(down, slot->ev_in, 0));
     if (type == 2) {
-        if (cudaMemcpyAsync(slot->df, f, cb * nm * T, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        if (cudaMemcpyAsync(slot->df, f, cb * nm * T, cudaMemcpyHostToDevice, up) != cudaSuccess)
             return fail(ESN_INTERNAL_ERROR, "H2D copy failed");
+        ESN_CUDA_TRY(cudaEventRecord(slot->ev_in, up));
+        ESN_CUDA_TRY(cudaStreamWaitEvent(st, slot->ev_in, 0));
         if (p->dtype == ESN_F64)
             rc = launch_amplify<double>(p->dim, p->ntransf, p->n, p->N, (const double *)slot->df, (const double *)p->pk[0],
                                         (const double *)p->pk[1], (const double *)p->pk[2], (double *)p->grid,
@@ -953,22 +1031,34 @@ static int pipelined(HostSlot *slot, int type, int dim, int64_t M, const double 
         ESN_CUDA_TRY(cudaMemsetAsync(p->grid, 0, real_size(p->dtype) * 2 * (size_t)p->G * p->ntransf, st));
     }
     ESN_CUDA_TRY(cudaEventRecord(slot->ev_grid, st));
+    // all uploads back to back (chunk k lands in staging slot lo: disjoint
+    // per chunk, so no reuse hazard)
+    auto block = [&](int64_t lo) {  // (T, cnt) staging block of chunk at lo
+        return (char *)slot->dc + (T > 1 ? (size_t)M * T * cb + (size_t)lo * T * cb : (size_t)lo * cb);
+    };
+    for (int k = 0; k < K; ++k) {
+        const int64_t lo = bound[k], cnt = bound[k + 1] - lo;
+        if (cnt <= 0) continue;
+        for (int d = 0; d < dim; ++d)
+            if (cudaMemcpyAsync((double *)slot->dx[d] + lo, xs[d] + lo, sizeof(double) * cnt, cudaMemcpyHostToDevice,
+                                up) != cudaSuccess)
+                return fail(ESN_INTERNAL_ERROR, "H2D copy failed");
+        if (type == 1 && (rc = copy_rows(block(lo), c, cnt, M, 0, lo, cnt, T, cb, cudaMemcpyHostToDevice, up)))
+            return rc;
+        ESN_CUDA_TRY(cudaEventRecord(slot->ev_up[k], up));
+        if (trace) cudaEventRecord(tev[1][k], up);
+    }
     for (int k = 0; k < K; ++k) {
         const int h = k % NH;
         esn_plan q = slot->helper[h];
         cudaStream_t hs = slot->hst[h];
-        const int64_t lo = k * chunk, cnt = std::min(chunk, M - lo);
-        if (cnt <= 0) break;
-        // chunk k lands in staging slot lo (disjoint per chunk, so no reuse hazard)
-        for (int d = 0; d < dim; ++d)
-            if (cudaMemcpyAsync((double *)slot->dx[d] + lo, xs[d] + lo, sizeof(double) * cnt, cudaMemcpyHostToDevice,
-                                hs) != cudaSuccess)
-                return fail(ESN_INTERNAL_ERROR, "H2D copy failed");
+        const int64_t lo = bound[k], cnt = bound[k + 1] - lo;
+        if (cnt <= 0) continue;
         // chunk views of the (T, M) strength / output arrays: the kernels
         // index c[t * cnt + j], so T > 1 stages through a (T, cnt) block in
         // the second half of the staging buffer (disjoint per chunk)
-        char *blk = (char *)slot->dc + (T > 1 ? (size_t)M * T * cb + (size_t)lo * T * cb : (size_t)lo * cb);
-        if (type == 1 && (rc = copy_rows(blk, c, cnt, M, 0, lo, cnt, T, cb, cudaMemcpyHostToDevice, hs))) return rc;
+        char *blk = block(lo);
+        ESN_CUDA_TRY(cudaStreamWaitEvent(hs, slot->ev_up[k], 0));
         q->ibase = lo;
         const void *cx[3] = {nullptr, nullptr, nullptr};
         for (int d = 0; d < dim; ++d) cx[d] = (const double *)slot->dx[d] + lo;
@@ -978,12 +1068,20 @@ static int pipelined(HostSlot *slot, int type, int dim, int64_t M, const double 
             if ((rc = do_spread(q, blk, p->grid, false))) return rc;
         } else {
             if ((rc = do_interp(q, p->grid, blk))) return rc;
-            if ((rc = copy_rows(c, blk, M, cnt, lo, 0, cnt, T, cb, cudaMemcpyDeviceToHost, hs))) return rc;
+            ESN_CUDA_TRY(cudaEventRecord(slot->ev_comp[k], hs));
+            ESN_CUDA_TRY(cudaStreamWaitEvent(down, slot->ev_comp[k], 0));
+            if ((rc = copy_rows(c, blk, M, cnt, lo, 0, cnt, T, cb, cudaMemcpyDeviceToHost, down))) return rc;
+            if (trace) {
+                cudaEventRecord(tev[2][k], hs);
+                cudaEventRecord(tev[3][k], down);
+            }
         }
         // (the helper's scratch is reused NH chunks later on the same stream)
         ESN_CUDA_TRY(cudaEventRecord(slot->ev_done[h], hs));
     }
     for (int h = 0; h < NH; ++h) ESN_CUDA_TRY(cudaStreamWaitEvent(st, slot->ev_done[h], 0));
+    ESN_CUDA_TRY(cudaEventRecord(slot->ev_down, down));
+    ESN_CUDA_TRY(cudaStreamWaitEvent(st, slot->ev_down, 0));
     if (type == 1) {
         if ((rc = run_fft(p->dim, p->n, p->dtype, p->ntransf, p->grid, p->isign, st))) return rc;
         if (p->dtype == ESN_F64)
@@ -996,10 +1094,26 @@ static int pipelined(HostSlot *slot, int type, int dim, int64_t M, const double 
         if (cudaMemcpyAsync(f, slot->df, cb * nm * T, cudaMemcpyDeviceToHost, st) != cudaSuccess)
             return fail(ESN_INTERNAL_ERROR, "D2H copy failed");
     }
+    const auto t_enq = std::chrono::steady_clock::now();
     ESN_CUDA_TRY(cudaStreamSynchronize(st));
+    if (trace) {
+        fprintf(stderr, "[esn] pipelined K=%d NH=%d: enqueue %.3f ms, wait %.3f ms\n", K, NH,
+                std::chrono::duration<double, std::milli>(t_enq - t_start).count(),
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_enq).count());
+        cudaDeviceSynchronize();
+        for (int k = 0; k < K && type == 2; ++k) {
+            float a = 0, b = 0, d = 0;
+            cudaEventElapsedTime(&a, tev[0][0], tev[1][k]);
+            cudaEventElapsedTime(&b, tev[0][0], tev[2][k]);
+            cudaEventElapsedTime(&d, tev[0][0], tev[3][k]);
+            fprintf(stderr, "[esn]   chunk %2d: up %.3f  comp %.3f  down %.3f ms\n", k, a, b, d);
+        }
+        cudaGetLastError();  // (events a transfer-only probe never recorded)
+    }
+    const auto t_sync = std::chrono::steady_clock::now();
     // merge the error flags: helpers hold the coordinate (and type-1
     // strength) flags with global indices, the main plan the mode flags
-    unsigned long long h[NH + 1][8];
+    unsigned long long h[HostSlot::NH + 1][8];
     ESN_CUDA_TRY(cudaMemcpy(h[0], p->flags, sizeof(h[0]), cudaMemcpyDeviceToHost));
     for (int k = 0; k < NH; ++k)
         ESN_CUDA_TRY(cudaMemcpy(h[1 + k], slot->helper[k]->flags, sizeof(h[0]), cudaMemcpyDeviceToHost));
@@ -1009,7 +1123,11 @@ static int pipelined(HostSlot *slot, int type, int dim, int64_t M, const double 
         for (int k = 1; k <= NH; ++k) merged[i] = std::min(merged[i], h[k][i]);
     }
     ESN_CUDA_TRY(cudaMemcpy(p->flags, merged, sizeof(merged), cudaMemcpyHostToDevice));
-    return esn_plan_check(p, nullptr);
+    rc = esn_plan_check(p, nullptr);
+    if (trace)
+        fprintf(stderr, "[esn]   flag merge + check %.3f ms\n",
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_sync).count());
+    return rc;
 }
 
 int esn_nufft_host(int type, int dim, int64_t M, const double *x, const double *y, const double *z, int ntransf,
