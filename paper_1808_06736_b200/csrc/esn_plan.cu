@@ -513,7 +513,9 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
         h = std::max(1, std::min({h, 64, std::max(1, (8 << 20) / p->nbins)}));
         // the interpolator only needs bins; sub-cells beyond ~2 keys per
         // point cost key-space work (memset + scans) for nothing
-        const int64_t maxkeys = std::min<int64_t>((int64_t)8 << 20, std::max<int64_t>(2 * M, 1 << 16));
+        static const char *kenv = getenv("ESN_T2_KEYS");
+        int64_t maxkeys = std::min<int64_t>((int64_t)8 << 20, std::max<int64_t>(2 * M, 1 << 16));
+        if (kenv) maxkeys = std::max<int64_t>(1, atoll(kenv));
         if (h != p->nchunk || maxkeys != p->keycap_req) {
             set_key_space(p, h, maxkeys);
             p->keycap_req = maxkeys;
