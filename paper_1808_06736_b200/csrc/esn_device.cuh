@@ -144,6 +144,17 @@ __device__ __forceinline__ Rec load_rec(const Rec *r, int64_t k) {
     return out;
 }
 
+// Ampere-style asynchronous global -> shared copies (LDGSTS): no registers
+// are held while the bytes are in flight; completion per thread by group.
+__device__ __forceinline__ void cp_async16(void *smem, const void *g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+                 "l"(g)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // ---------------------------------------------------------------------------
 // Global-atomic spreader: one thread per sorted point, w^d complex REDs
 // straight into the fine grid (rows reused across the ntransf batch).  Used
@@ -222,60 +233,27 @@ template <typename T, int DIM, int W>
 __device__ __forceinline__ void rows_accumulate(typename Cx<T>::type *acc, int ox,
                                                 typename Cx<T>::type v, const T *r1) {
     constexpr int BX = RowsCfg<T, DIM, W>::BX;
-#define ESN_ROWS_CASE(OX)                                      \
-    case OX: {                                                 \
-        _Pragma("unroll") for (int m = 0; m < W; ++m) {        \
-            const T r = r1[m];                                 \
-            acc[OX + m].x = fma(v.x, r, acc[OX + m].x);        \
-            acc[OX + m].y = fma(v.y, r, acc[OX + m].y);        \
-        }                                                      \
-    } break;
+    // one flat switch (a single jump-table dispatch); cases >= BX are empty
+#define ESN_ROWS_CASE(OX)                                          \
+    case OX:                                                       \
+        if constexpr (OX < BX) {                                   \
+            _Pragma("unroll") for (int m = 0; m < W; ++m) {        \
+                const T r = r1[m];                                 \
+                acc[OX + m].x = fma(v.x, r, acc[OX + m].x);        \
+                acc[OX + m].y = fma(v.y, r, acc[OX + m].y);        \
+            }                                                      \
+        }                                                          \
+        break;
     switch (ox) {
-        ESN_ROWS_CASE(0)
-        ESN_ROWS_CASE(1)
-        ESN_ROWS_CASE(2)
-        ESN_ROWS_CASE(3)
-        ESN_ROWS_CASE(4)
-        ESN_ROWS_CASE(5)
-        ESN_ROWS_CASE(6)
-        ESN_ROWS_CASE(7)
+        ESN_ROWS_CASE(0) ESN_ROWS_CASE(1) ESN_ROWS_CASE(2) ESN_ROWS_CASE(3)
+        ESN_ROWS_CASE(4) ESN_ROWS_CASE(5) ESN_ROWS_CASE(6) ESN_ROWS_CASE(7)
+        ESN_ROWS_CASE(8) ESN_ROWS_CASE(9) ESN_ROWS_CASE(10) ESN_ROWS_CASE(11)
+        ESN_ROWS_CASE(12) ESN_ROWS_CASE(13) ESN_ROWS_CASE(14) ESN_ROWS_CASE(15)
+        ESN_ROWS_CASE(16) ESN_ROWS_CASE(17) ESN_ROWS_CASE(18) ESN_ROWS_CASE(19)
+        ESN_ROWS_CASE(20) ESN_ROWS_CASE(21) ESN_ROWS_CASE(22) ESN_ROWS_CASE(23)
+        ESN_ROWS_CASE(24) ESN_ROWS_CASE(25) ESN_ROWS_CASE(26) ESN_ROWS_CASE(27)
+        ESN_ROWS_CASE(28) ESN_ROWS_CASE(29) ESN_ROWS_CASE(30) ESN_ROWS_CASE(31)
         default:
-            if constexpr (BX > 8) {
-                switch (ox) {
-                    ESN_ROWS_CASE(8)
-                    ESN_ROWS_CASE(9)
-                    ESN_ROWS_CASE(10)
-                    ESN_ROWS_CASE(11)
-                    ESN_ROWS_CASE(12)
-                    ESN_ROWS_CASE(13)
-                    ESN_ROWS_CASE(14)
-                    ESN_ROWS_CASE(15)
-                    default:
-                        if constexpr (BX > 16) {
-                            switch (ox) {
-                                ESN_ROWS_CASE(16)
-                                ESN_ROWS_CASE(17)
-                                ESN_ROWS_CASE(18)
-                                ESN_ROWS_CASE(19)
-                                ESN_ROWS_CASE(20)
-                                ESN_ROWS_CASE(21)
-                                ESN_ROWS_CASE(22)
-                                ESN_ROWS_CASE(23)
-                                ESN_ROWS_CASE(24)
-                                ESN_ROWS_CASE(25)
-                                ESN_ROWS_CASE(26)
-                                ESN_ROWS_CASE(27)
-                                ESN_ROWS_CASE(28)
-                                ESN_ROWS_CASE(29)
-                                ESN_ROWS_CASE(30)
-                                ESN_ROWS_CASE(31)
-                                default:
-                                    break;
-                            }
-                        }
-                        break;
-                }
-            }
             break;
     }
 #undef ESN_ROWS_CASE
@@ -448,24 +426,42 @@ __global__ void __launch_bounds__(256) k_rows2d(SpreadArgs<T> a, PtRows2<W> *tab
     }
 }
 
+// batched 2D spreader: points staged per warp per batch
+constexpr int kBatchPts = 16;
+template <typename T, int W>
+constexpr size_t batch2d_stage_bytes() {
+    return (size_t)kBatchPts * (sizeof(PtRows2<W>) + 32 * 2 * sizeof(T));
+}
+template <typename T, int W>
+constexpr size_t batch2d_smem_bytes() {  // 4 warps x 2 stages (the flush slab aliases them)
+    return 4 * 2 * batch2d_stage_bytes<T, W>();
+}
+
 template <typename T, int W>
 __global__ void __launch_bounds__(128) k_spread_batch2d(SpreadArgs<T> a, const T *cperm, const PtRows2<W> *tab) {
     // Warp-independent: a persistent warp takes work items (subproblem,
     // transform group, tile row) from an atomic queue.  Lane = transform.
     // The item's points are one contiguous run of the finely sorted bin
     // (oy in [row - W + 1, row]); their kernel rows come precomputed
-    // (k_rows2d), their strengths as one coalesced 256-byte line per point.
-    // No block barriers, no shared memory; next point prefetched.
+    // (k_rows2d), their strengths as one 256-byte line per point.  Both are
+    // staged per warp in batches of kBatchPts points with cp.async, one
+    // batch ahead (double buffer), so the loop reads only shared memory.
+    // No block barriers.
     using C = typename Cx<T>::type;
     using Cfg = Batch2Cfg<T, W>;
     constexpr int X = Cfg::X, RY = Cfg::RY;
+    constexpr int TB = sizeof(PtRows2<W>), CB = 32 * sizeof(C);
+    constexpr size_t STAGE = batch2d_stage_bytes<T, W>();
+    static_assert(TB % 16 == 0 && CB % 16 == 0, "16-byte staging chunks");
+    static_assert(2 * STAGE >= (size_t)32 * (X + 1) * sizeof(C), "flush slab must fit the warp's ring");
+    extern __shared__ __align__(16) unsigned char b2_smem[];
     const int lane = threadIdx.x & 31;
+    unsigned char *wbase = b2_smem + (threadIdx.x >> 5) * 2 * STAGE;
     const int n1 = a.g.n[0], n2 = a.g.n[1];
     const int nsub = *a.nsub;
     const int ngroups = (a.ntransf + 31) / 32;
     const int nitems = nsub * ngroups * RY;
     const int kx = a.g.bs[0] >> a.sbl[0];
-    __shared__ C s_slab[4 * 32 * (X + 1)];  // one transposition slab per warp (128 threads)
     for (;;) {
         int item = 0;
         if (lane == 0) item = atomicAdd(a.work, 1);
@@ -485,38 +481,55 @@ __global__ void __launch_bounds__(128) k_spread_batch2d(SpreadArgs<T> a, const T
         const int r1k = (yhi >> a.sbl[1]) + 1;
         const int k1 = min(start + cnt, r1k * kx < a.spb ? ks[r1k * kx] : 0x7fffffff);
         if (k0 >= k1) continue;
-        const int t = tg * 32 + lane;
-        const C *cg = reinterpret_cast<const C *>(cperm) + (int64_t)tg * a.M * 32 + lane;
+        const C *cg = reinterpret_cast<const C *>(cperm) + (int64_t)tg * a.M * 32;
+        auto issue = [&](int kb, int buf) {  // stage points [kb, min(kb + NB, k1))
+            const int n = min(kBatchPts, k1 - kb);
+            if (n > 0) {
+                const char *src = reinterpret_cast<const char *>(tab + kb);
+                unsigned char *dst = wbase + buf * STAGE;
+                for (int c = lane; c < n * TB / 16; c += 32) cp_async16(dst + 16 * c, src + 16 * c);
+                const char *src2 = reinterpret_cast<const char *>(cg + (int64_t)kb * 32);
+                unsigned char *dst2 = dst + kBatchPts * TB;
+                for (int c = lane; c < n * CB / 16; c += 32) cp_async16(dst2 + 16 * c, src2 + 16 * c);
+            }
+            cp_async_commit();
+        };
         C acc[X];
 #pragma unroll
         for (int x = 0; x < X; ++x) acc[x] = C{(T)0, (T)0};
-        PtRows2<W> e = tab[k0];
-        C cq = cg[(int64_t)k0 * 32];
-        for (int k = k0; k < k1; ++k) {
-            const PtRows2<W> cur = e;
-            const C ccur = cq;
-            if (k + 1 < k1) {  // prefetch the next point
-                e = tab[k + 1];
-                cq = cg[(int64_t)(k + 1) * 32];
+        issue(k0, 0);
+        int buf = 0;
+        for (int kb = k0; kb < k1; kb += kBatchPts) {
+            issue(kb + kBatchPts, buf ^ 1);
+            cp_async_wait<1>();
+            __syncwarp();
+            const int n = min(kBatchPts, k1 - kb);
+            const PtRows2<W> *tb = reinterpret_cast<const PtRows2<W> *>(wbase + buf * STAGE);
+            const C *cq = reinterpret_cast<const C *>(wbase + buf * STAGE + kBatchPts * TB);
+            const int row2 = row + lo2;
+            for (int i = 0; i < n; ++i) {
+                const PtRows2<W> &e = tb[i];  // shared memory: loads below are broadcasts
+                const int dy = row2 - e.i2;
+                if ((unsigned)dy >= (unsigned)W) continue;  // warp-uniform (sub-cell edges)
+                const T wy = (T)e.r2[dy];                   // dynamic index into shared memory
+                const C ccur = cq[i * 32 + lane];
+                const C v{ccur.x * wy, ccur.y * wy};
+                T r1[W];
+#pragma unroll
+                for (int m = 0; m < W; ++m) r1[m] = (T)e.r1[m];
+                rows_accumulate<T, 2, W>(acc, e.i1 - lo1, v, r1);
             }
-            const int dy = row - (cur.i2 - lo2);
-            if (dy < 0 || dy >= W) continue;  // warp-uniform (sub-cell edges)
-            T wy = (T)cur.r2[0];
-#pragma unroll
-            for (int m = 1; m < W; ++m) wy = (m == dy) ? (T)cur.r2[m] : wy;
-            const C v{ccur.x * wy, ccur.y * wy};
-            T r1[W];
-#pragma unroll
-            for (int m = 0; m < W; ++m) r1[m] = (T)cur.r1[m];
-            rows_accumulate<T, 2, W>(acc, cur.i1 - lo1, v, r1);
+            __syncwarp();
+            buf ^= 1;
         }
-        // flush: transpose the 32 transforms x X cells through this warp's
-        // shared-memory slab so each RED burst is one transform's contiguous
-        // row (lanes = x): lanes = transforms would scatter 32 planes apart,
-        // which runs at ~4e10 ops/s on B200 vs ~3.7e11 coalesced (measured)
-        (void)t;
-        C *slab = s_slab + (threadIdx.x >> 5) * 32 * (X + 1);
+        cp_async_wait<0>();
         __syncwarp();
+        // flush: transpose the 32 transforms x X cells through this warp's
+        // shared-memory slab (aliasing its idle staging ring) so each RED
+        // burst is one transform's contiguous row (lanes = x): lanes =
+        // transforms would scatter 32 planes apart, which runs at ~4e10
+        // ops/s on B200 vs ~3.7e11 coalesced (measured)
+        C *slab = reinterpret_cast<C *>(wbase);
 #pragma unroll
         for (int x = 0; x < X; ++x) slab[lane * (X + 1) + x] = acc[x];
         __syncwarp();
@@ -546,30 +559,44 @@ __global__ void __launch_bounds__(128) k_spread_batch2d(SpreadArgs<T> a, const T
 template <typename T>
 __global__ void __launch_bounds__(1024) k_permute_strengths(SpreadArgs<T> a, const int *key, const int *rank,
                                                             const int *kstart, T *cperm) {
+    // U tiles of 32 points per iteration: U loads in flight per thread and
+    // one barrier pair per U tiles
     using C = typename Cx<T>::type;
-    __shared__ C tile[32][33];
+    constexpr int U = 4;
+    __shared__ C tile[U][32][33];
+    (void)rank;
+    (void)kstart;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int ngroups = (a.ntransf + 31) / 32;
-    const int64_t jtiles = (a.M + 31) / 32;
-    for (int64_t b = blockIdx.x; b < jtiles * ngroups; b += gridDim.x) {
+    const int64_t jblocks = (a.M + 32 * U - 1) / (32 * U);
+    for (int64_t b = blockIdx.x; b < jblocks * ngroups; b += gridDim.x) {
         const int g = (int)(b % ngroups);
-        const int64_t j0 = (b / ngroups) * 32;
+        const int64_t j0 = (b / ngroups) * 32 * U;
         const int t = g * 32 + ty;
-        const int64_t j = j0 + tx;
-        C v{(T)0, (T)0};
-        if (t < a.ntransf && j < a.M) {
-            v = reinterpret_cast<const C *>(a.c)[(int64_t)t * a.M + j];
-            if (!finite2<T>(v)) flag_min(&a.flags[6], (unsigned long long)(j + a.ibase));
+        C v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t j = j0 + u * 32 + tx;
+            v[u] = C{(T)0, (T)0};
+            if (t < a.ntransf && j < a.M) v[u] = reinterpret_cast<const C *>(a.c)[(int64_t)t * a.M + j];
         }
-        tile[ty][tx] = v;
+        int pos[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t jj = j0 + u * 32 + ty;
+            pos[u] = jj < a.M ? key[jj] : -1;  // setpts leaves each point's sorted position in key[]
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t j = j0 + u * 32 + tx;
+            if (t < a.ntransf && j < a.M && !finite2<T>(v[u]))
+                flag_min(&a.flags[6], (unsigned long long)(j + a.ibase));
+            tile[u][ty][tx] = v[u];
+        }
         __syncthreads();
-        const int64_t jj = j0 + ty;
-        if (jj < a.M) {
-            const int pos = key[jj];  // setpts leaves each point's sorted position in key[]
-            (void)rank;
-            (void)kstart;
-            reinterpret_cast<C *>(cperm)[((int64_t)g * a.M + pos) * 32 + tx] = tile[tx][ty];
-        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (pos[u] >= 0) reinterpret_cast<C *>(cperm)[((int64_t)g * a.M + pos[u]) * 32 + tx] = tile[u][tx][ty];
         __syncthreads();
     }
 }

@@ -83,11 +83,12 @@ struct SpreadBatchOp {
                 reinterpret_cast<char *>(cperm) + (size_t)ngroups * 32 * a.M * 2 * sizeof(T));
             k_rows2d<T, W><<<grid_for(a.M, 256), 256, 0, st>>>(a, tab);
             static int grid = 0;
+            constexpr size_t smem = batch2d_smem_bytes<T, W>();
             if (grid == 0) {
-                int rc = persistent_launch(k_spread_batch2d<T, W>, 128, 0, st, nullptr, &grid);
+                int rc = persistent_launch(k_spread_batch2d<T, W>, 128, smem, st, nullptr, &grid);
                 if (rc) return rc;
             }
-            k_spread_batch2d<T, W><<<grid, 128, 0, st>>>(a, cperm, tab);
+            k_spread_batch2d<T, W><<<grid, 128, smem, st>>>(a, cperm, tab);
             ESN_CUDA_TRY(cudaGetLastError());
             return ESN_SUCCESS;
         } else {
