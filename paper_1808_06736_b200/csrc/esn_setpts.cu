@@ -109,13 +109,14 @@ __device__ __forceinline__ int point_key(const SetptsArgs &a, int64_t i, const d
     return bin * a.spb + loc;
 }
 
-constexpr int kILP = 4;  // points in flight per thread (independent loads / atomics)
+constexpr int kILP = 4;   // points in flight per thread (independent loads / atomics)
+constexpr int kSILP = 8;  // record scatter: points in flight per thread
 
-template <typename XT>
+template <typename XT, int U = kILP>
 __device__ __forceinline__ void load_coords(const SetptsArgs &a, int64_t base, double (*x)[3]) {
     // all loads first (independent, read-only), compute afterwards
 #pragma unroll
-    for (int u = 0; u < kILP; ++u) {
+    for (int u = 0; u < U; ++u) {
         const int64_t i = base + (int64_t)u * blockDim.x;
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
@@ -154,47 +155,31 @@ __global__ void __launch_bounds__(256, 4) k_setpts_count(SetptsArgs a) {
     }
 }
 
-// Pass 2a: pos[i] = start[key[i]] + rank[i] -- a lean kernel (three 4-byte
-// streams and one L2-resident gather) so many lookups are in flight.
-__global__ void __launch_bounds__(256) k_setpts_pos(SetptsArgs a) {
-    constexpr int U = 8;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x * U;
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x * U + threadIdx.x; base < a.M; base += stride) {
-        int key[U], rank[U], st[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t i = base + (int64_t)u * blockDim.x;
-            key[u] = i < a.M ? a.key[i] : 0;
-            rank[u] = i < a.M ? a.rank[i] : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) st[u] = __ldg(a.cursor + key[u]);
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t i = base + (int64_t)u * blockDim.x;
-            if (i < a.M) a.key[i] = st[u] + rank[u];  // key[] now holds the position
-        }
-    }
-}
-
-// Pass 2b: write the point's full record {g, j} at its position with one
-// 256-bit store (a whole L2 sector).  Streams x and pos; no dependent loads.
+// Pass 2: pos = start[key] + rank (start from the L2-resident scan), then the
+// point's full record {g, j} at pos with one 256-bit store (a whole L2
+// sector); key[] keeps pos for the batched spreader's strength permutation.
+// kSILP points per thread, all loads issued before the dependent gather.
 template <typename XT>
 __global__ void __launch_bounds__(256) k_setpts_scatter(SetptsArgs a) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x * kILP;
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x * kILP + threadIdx.x; base < a.M; base += stride) {
-        double x[kILP][3];
-        load_coords<XT>(a, base, x);
-        int pos[kILP];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * kSILP;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x * kSILP + threadIdx.x; base < a.M; base += stride) {
+        int pos[kSILP], rank[kSILP];
 #pragma unroll
-        for (int u = 0; u < kILP; ++u) {
+        for (int u = 0; u < kSILP; ++u) {
             const int64_t i = base + (int64_t)u * blockDim.x;
             pos[u] = i < a.M ? __ldg(a.key + i) : -1;
+            rank[u] = i < a.M ? __ldg(a.rank + i) : 0;
         }
+        double x[kSILP][3];
+        load_coords<XT, kSILP>(a, base, x);
 #pragma unroll
-        for (int u = 0; u < kILP; ++u) {
+        for (int u = 0; u < kSILP; ++u)
+            if (pos[u] >= 0) pos[u] = __ldg(a.cursor + pos[u]) + rank[u];  // start of the key + rank
+#pragma unroll
+        for (int u = 0; u < kSILP; ++u) {
             if (pos[u] < 0) continue;
             const int64_t i = base + (int64_t)u * blockDim.x;
+            a.key[i] = pos[u];  // key[] now holds the position (the batched spreader's permutation)
             double g[3] = {0.0, 0.0, 0.0};
             point_key(a, i, x[u], g, false);
             const unsigned long long j = (unsigned long long)(unsigned)i;
@@ -326,9 +311,20 @@ template <typename XT>
 static int setpts_impl(const SetptsArgs &a, int nbins, int maxsub, int4 *subprob, int *nsub, int *subofs,
                        cudaStream_t st) {
     const int threads = 256;
+    // persistent grids: exactly one wave of resident CTAs (a partial second
+    // wave left SMs idle at the tail)
+    auto resident = [](auto kernel) {
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, 256, 0) != cudaSuccess || occ < 1) {
+            cudaGetLastError();
+            occ = 4;
+        }
+        return (int64_t)device_sm_count() * occ;
+    };
+    static const int64_t cap_count = (int64_t)device_sm_count() * 8;  // (atomics: oversubscribed is faster)
+    static const int64_t cap_scatter = resident(k_setpts_scatter<XT>);
     int64_t blocks = (a.M + threads * kILP - 1) / (threads * kILP);
-    const int64_t cap = (int64_t)device_sm_count() * 8;
-    if (blocks > cap) blocks = cap;
+    if (blocks > cap_count) blocks = cap_count;
     if (blocks < 1) blocks = 1;
     if (a.M > 0) {
         k_setpts_count<XT><<<(int)blocks, threads, 0, st>>>(a);
@@ -340,10 +336,9 @@ static int setpts_impl(const SetptsArgs &a, int nbins, int maxsub, int4 *subprob
     k_scan_down<<<nsb, 1024, 0, st>>>(a.key_count, a.nkeys, a.block_sums, a.cursor, a.bin_start, a.spb, nbins);
     ESN_CUDA_TRY(cudaGetLastError());
     if (a.M > 0) {
-        int64_t pb = (a.M + threads * 8 - 1) / (threads * 8);
-        if (pb > cap) pb = cap;
-        k_setpts_pos<<<(int)pb, threads, 0, st>>>(a);
-        k_setpts_scatter<XT><<<(int)blocks, threads, 0, st>>>(a);
+        int64_t sb = (a.M + threads * kSILP - 1) / (threads * kSILP);
+        if (sb > cap_scatter) sb = cap_scatter;
+        k_setpts_scatter<XT><<<(int)sb, threads, 0, st>>>(a);
         ESN_CUDA_TRY(cudaGetLastError());
     }
     k_scan_subprob<<<1, 1024, 0, st>>>(a.bin_start, nbins, maxsub, subofs, nsub);
