@@ -1,0 +1,77 @@
+"""Cross-checks between the device code paths that must agree.
+
+* fp64 batched transforms (ntransf > 1) against one transform at a time:
+  type 2 bit-identical (each output is computed by one thread with the
+  same operations, esn_device.cuh k_interp_bulk), type 1 to rounding (the
+  global-memory reductions of the row spreader are unordered).
+* the pipelined bulk-copy interpolator against the synchronous tile
+  interpolator (ESN_INTERP=tile, read once per process -> child process):
+  bit-identical outputs.
+"""
+import os
+import subprocess
+import sys
+import textwrap
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dim,nm,tol", [(2, (40, 36), 1e-6), (3, (12, 10, 14), 1e-5)])
+def test_fp64_batched_matches_single(esn, dim, nm, tol):
+    rng = np.random.default_rng(11 + dim)
+    m, T = 20_000, 3
+    coords = [rng.uniform(-np.pi, np.pi, m) for _ in range(dim)]
+    o = esn.TransformOptions(tolerance=tol, isign=-1)
+    f = rng.standard_normal((T,) + nm[::-1]) + 1j * rng.standard_normal((T,) + nm[::-1])
+    outb, _ = esn.exec_type2(coords, f, o)
+    assert outb.shape == (T, m)
+    for t in range(T):
+        single, _ = esn.exec_type2(coords, f[t], o)
+        assert np.array_equal(single, outb[t]), f"type 2 transform {t}"
+    c = rng.standard_normal((T, m)) + 1j * rng.standard_normal((T, m))
+    fb, _ = esn.exec_type1(coords, c, nm, o)
+    assert fb.shape == (T,) + nm[::-1]
+    for t in range(T):
+        single, _ = esn.exec_type1(coords, c[t], nm, o)
+        assert np.linalg.norm(single - fb[t]) <= 1e-13 * np.linalg.norm(single), f"type 1 transform {t}"
+
+
+SCRIPT = textwrap.dedent(r"""
+    import sys, numpy as np
+    sys.path.insert(0, sys.argv[1])
+    import paper_1808_06736_b200 as nu
+    rng = np.random.default_rng(5)
+    for dim, nm, M, tol, T in [(2, (64, 50), 40_000, 1e-5, 1), (2, (30, 30), 10_000, 1e-9, 2),
+                               (3, (16, 14, 12), 30_000, 1e-6, 1), (1, (300,), 5_000, 1e-7, 1)]:
+        xs = [rng.uniform(-np.pi, np.pi, M) for _ in range(dim)]
+        shape = ((T,) if T > 1 else ()) + nm[::-1]
+        f = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+        c, _ = nu.exec_type2(tuple(xs), f, nu.TransformOptions(tolerance=tol, isign=1))
+        np.save(sys.argv[2] + f"/t2_{dim}_{T}.npy", c)
+""")
+
+
+def _run(tmp, env_extra):
+    env = dict(os.environ)
+    env.pop("ESN_INTERP", None)
+    env.update(env_extra)
+    os.makedirs(tmp, exist_ok=True)
+    r = subprocess.run([sys.executable, "-c", SCRIPT, ROOT, tmp], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+
+
+@pytest.mark.gpu
+def test_bulk_and_tile_interpolators_bit_identical(tmp_path, esn):
+    _run(str(tmp_path / "bulk"), {})
+    _run(str(tmp_path / "tile"), {"ESN_INTERP": "tile"})
+    names = sorted(os.listdir(tmp_path / "bulk"))
+    assert len(names) == 4
+    for n in names:
+        a = np.load(tmp_path / "bulk" / n)
+        b = np.load(tmp_path / "tile" / n)
+        assert np.array_equal(a, b), n
