@@ -429,15 +429,46 @@ __global__ void __launch_bounds__(256) k_rows2d(SpreadArgs<T> a, PtRows2<W> *tab
 // batched 2D spreader: points staged per warp per batch
 constexpr int kBatchPts = 16;
 template <typename T, int W>
-constexpr size_t batch2d_stage_bytes() {
-    return (size_t)kBatchPts * (sizeof(PtRows2<W>) + 32 * 2 * sizeof(T));
+constexpr size_t batch2d_stage_bytes() {  // points + strength lines + one row of key starts
+    return (size_t)kBatchPts * (sizeof(PtRows2<W>) + 32 * 2 * sizeof(T)) +
+           (size_t)((Batch2Cfg<T, W>::BX + 1 + 3) / 4 + 1) * 16;
 }
 template <typename T, int W>
 constexpr size_t batch2d_smem_bytes() {  // 4 warps x 2 stages (the flush slab aliases them)
     return 4 * 2 * batch2d_stage_bytes<T, W>();
 }
 
+// flush of one warp's tile row: transpose the 32 transforms x X cells
+// through the warp's shared-memory slab (aliasing its idle staging ring) so
+// each RED burst is one transform's contiguous row (lanes = x): lanes =
+// transforms would scatter 32 planes apart, which runs at ~4e10 ops/s on
+// B200 vs ~3.7e11 coalesced (measured)
 template <typename T, int W>
+__device__ __forceinline__ void batch2d_flush(const typename Cx<T>::type *acc, unsigned char *wbase, int lane,
+                                              int lo1, int lo2, int row, int tg, const SpreadArgs<T> &a) {
+    using C = typename Cx<T>::type;
+    constexpr int X = Batch2Cfg<T, W>::X;
+    const int n1 = a.g.n[0], n2 = a.g.n[1];
+    C *slab = reinterpret_cast<C *>(wbase);
+#pragma unroll
+    for (int x = 0; x < X; ++x) slab[lane * (X + 1) + x] = acc[x];
+    __syncwarp();
+    int g2 = lo2 + row;
+    while (g2 >= n2) g2 -= n2;
+    int g1 = lo1 + lane;
+    while (g1 >= n1) g1 -= n1;
+    const int tmax = min(32, a.ntransf - tg * 32);
+    for (int tt = 0; tt < tmax; ++tt) {
+        if (lane < X) {
+            const C v = slab[tt * (X + 1) + lane];
+            if (v.x != (T)0 || v.y != (T)0)
+                red_add(reinterpret_cast<C *>(a.grid) + (int64_t)(tg * 32 + tt) * a.gstride + (int64_t)g2 * n1 + g1, v);
+        }
+    }
+    __syncwarp();
+}
+
+template <typename T, int W, bool CELLKEYS>
 __global__ void __launch_bounds__(128) k_spread_batch2d(SpreadArgs<T> a, const T *cperm, const PtRows2<W> *tab) {
     // Warp-independent: a persistent warp takes work items (subproblem,
     // transform group, tile row) from an atomic queue.  Lane = transform.
@@ -462,11 +493,14 @@ __global__ void __launch_bounds__(128) k_spread_batch2d(SpreadArgs<T> a, const T
     const int ngroups = (a.ntransf + 31) / 32;
     const int nitems = nsub * ngroups * RY;
     const int kx = a.g.bs[0] >> a.sbl[0];
+    // the next work item is claimed one item ahead (the atomic's latency
+    // overlaps the current item)
+    int next = 0;
+    if (lane == 0) next = atomicAdd(a.work, 1);
     for (;;) {
-        int item = 0;
-        if (lane == 0) item = atomicAdd(a.work, 1);
-        item = __shfl_sync(0xffffffffu, item, 0);
+        const int item = __shfl_sync(0xffffffffu, next, 0);
         if (item >= nitems) break;
+        if (lane == 0) next = atomicAdd(a.work, 1);
         const int row = item % RY;
         const int sg = item / RY;
         const int tg = sg % ngroups;
@@ -482,6 +516,92 @@ __global__ void __launch_bounds__(128) k_spread_batch2d(SpreadArgs<T> a, const T
         const int k1 = min(start + cnt, r1k * kx < a.spb ? ks[r1k * kx] : 0x7fffffff);
         if (k0 >= k1) continue;
         const C *cg = reinterpret_cast<const C *>(cperm) + (int64_t)tg * a.M * 32;
+        if constexpr (CELLKEYS) {
+            // Cell-resolution keys: inside one y row of the bin the points
+            // are grouped by x cell, and every point of a cell shares (ox,
+            // dy).  Pieces of <= kBatchPts points never straddle a y row;
+            // the x offset is swept as a compile-time loop, so the register
+            // window needs no per-point dispatch.
+            constexpr int BX = Cfg::BX;
+            constexpr int KSOFF = kBatchPts * (TB + CB);
+            const int end = start + cnt;
+            // first key start of rows ylo .. yhi + 1, one per lane (one load per item)
+            const int ly = ylo + lane;
+            const int rowk = (lane <= yhi - ylo + 1) ? (ly * kx < a.spb ? ks[ly * kx] : 0x7fffffff) : 0x7fffffff;
+            auto row_lo = [&](int y) { return max(start, __shfl_sync(0xffffffffu, rowk, y - ylo)); };
+            auto row_hi = [&](int y) { return min(end, __shfl_sync(0xffffffffu, rowk, y - ylo + 1)); };
+            // piece state: y row, [kb, ke)
+            int py = ylo, pb = row_lo(ylo);
+            auto advance = [&](int &y, int &kb) {  // next non-empty piece start after [kb, ke)
+                const int he = row_hi(y);
+                const int ke = min(kb + kBatchPts, he);
+                if (ke < he) { kb = ke; return; }
+                for (++y; y <= yhi; ++y) {
+                    kb = row_lo(y);
+                    if (kb < row_hi(y)) return;
+                }
+            };
+            if (pb >= row_hi(py)) advance(py, pb);  // (first row may be empty)
+            auto issue_piece = [&](int y, int kb, int buf) {
+                if (y <= yhi) {
+                    const int n = min(kBatchPts, row_hi(y) - kb);
+                    const char *src = reinterpret_cast<const char *>(tab + kb);
+                    unsigned char *dst = wbase + buf * STAGE;
+                    for (int c = lane; c < n * TB / 16; c += 32) cp_async16(dst + 16 * c, src + 16 * c);
+                    const char *src2 = reinterpret_cast<const char *>(cg + (int64_t)kb * 32);
+                    unsigned char *dst2 = dst + kBatchPts * TB;
+                    for (int c = lane; c < n * CB / 16; c += 32) cp_async16(dst2 + 16 * c, src2 + 16 * c);
+                    // key starts of this row's x cells (+ the next row's first)
+                    const char *src3 = reinterpret_cast<const char *>(ks + y * kx);
+                    for (int c = lane; c < (BX + 1 + 3) / 4; c += 32) cp_async16(dst + KSOFF + 16 * c, src3 + 16 * c);
+                }
+                cp_async_commit();
+            };
+            C acc[X];
+#pragma unroll
+            for (int x = 0; x < X; ++x) acc[x] = C{(T)0, (T)0};
+            issue_piece(py, pb, 0);
+            int buf = 0;
+            while (py <= yhi) {
+                int ny = py, nb = pb;
+                advance(ny, nb);
+                issue_piece(ny, nb, buf ^ 1);
+                cp_async_wait<1>();
+                __syncwarp();
+                const int ke = min(pb + kBatchPts, row_hi(py));
+                const int dy = row - py;
+                const PtRows2<W> *tb = reinterpret_cast<const PtRows2<W> *>(wbase + buf * STAGE);
+                const C *cq = reinterpret_cast<const C *>(wbase + buf * STAGE + kBatchPts * TB) + lane;
+                const int *sks = reinterpret_cast<const int *>(wbase + buf * STAGE + KSOFF);
+                // piece-local [lo, hi) of every x cell
+                int lo = min(max(sks[0], pb), ke) - pb;
+#pragma unroll
+                for (int ox = 0; ox < BX; ++ox) {
+                    const int hi = ox + 1 < BX ? min(max(sks[ox + 1], pb), ke) - pb : ke - pb;
+#pragma unroll 1
+                    for (int k = lo; k < hi; ++k) {
+                        const PtRows2<W> &e = tb[k];
+                        const T wy = (T)e.r2[dy];
+                        const C cc = cq[k * 32];
+                        const C v{cc.x * wy, cc.y * wy};
+#pragma unroll
+                        for (int m = 0; m < W; ++m) {
+                            const T r = (T)e.r1[m];
+                            acc[ox + m].x = fma(v.x, r, acc[ox + m].x);
+                            acc[ox + m].y = fma(v.y, r, acc[ox + m].y);
+                        }
+                    }
+                    lo = hi;
+                }
+                __syncwarp();
+                buf ^= 1;
+                py = ny;
+                pb = nb;
+            }
+            cp_async_wait<0>();
+            __syncwarp();
+            batch2d_flush<T, W>(acc, wbase, lane, lo1, lo2, row, tg, a);
+        } else {
         auto issue = [&](int kb, int buf) {  // stage points [kb, min(kb + NB, k1))
             const int n = min(kBatchPts, k1 - kb);
             if (n > 0) {
@@ -524,30 +644,8 @@ __global__ void __launch_bounds__(128) k_spread_batch2d(SpreadArgs<T> a, const T
         }
         cp_async_wait<0>();
         __syncwarp();
-        // flush: transpose the 32 transforms x X cells through this warp's
-        // shared-memory slab (aliasing its idle staging ring) so each RED
-        // burst is one transform's contiguous row (lanes = x): lanes =
-        // transforms would scatter 32 planes apart, which runs at ~4e10
-        // ops/s on B200 vs ~3.7e11 coalesced (measured)
-        C *slab = reinterpret_cast<C *>(wbase);
-#pragma unroll
-        for (int x = 0; x < X; ++x) slab[lane * (X + 1) + x] = acc[x];
-        __syncwarp();
-        int g2 = lo2 + row;
-        while (g2 >= n2) g2 -= n2;
-        int g1 = lo1 + lane;
-        while (g1 >= n1) g1 -= n1;
-        const int tmax = min(32, a.ntransf - tg * 32);
-        for (int tt = 0; tt < tmax; ++tt) {
-            if (lane < X) {
-                const C v = slab[tt * (X + 1) + lane];
-                if (v.x != (T)0 || v.y != (T)0)
-                    red_add(reinterpret_cast<C *>(a.grid) + (int64_t)(tg * 32 + tt) * a.gstride +
-                                (int64_t)g2 * n1 + g1,
-                            v);
-            }
+        batch2d_flush<T, W>(acc, wbase, lane, lo1, lo2, row, tg, a);
         }
-        __syncwarp();
     }
 }
 

@@ -82,13 +82,23 @@ struct SpreadBatchOp {
             PtRows2<W> *tab = reinterpret_cast<PtRows2<W> *>(
                 reinterpret_cast<char *>(cperm) + (size_t)ngroups * 32 * a.M * 2 * sizeof(T));
             k_rows2d<T, W><<<grid_for(a.M, 256), 256, 0, st>>>(a, tab);
-            static int grid = 0;
             constexpr size_t smem = batch2d_smem_bytes<T, W>();
-            if (grid == 0) {
-                int rc = persistent_launch(k_spread_batch2d<T, W>, 128, smem, st, nullptr, &grid);
-                if (rc) return rc;
+            // cell-resolution sort keys -> static x-offset sweep; else per-point dispatch
+            if (a.sbl[0] == 0 && a.sbl[1] == 0 && a.g.bs[0] == Cfg::BX) {
+                static int grid = 0;
+                if (grid == 0) {
+                    int rc = persistent_launch(k_spread_batch2d<T, W, true>, 128, smem, st, nullptr, &grid);
+                    if (rc) return rc;
+                }
+                k_spread_batch2d<T, W, true><<<grid, 128, smem, st>>>(a, cperm, tab);
+            } else {
+                static int grid = 0;
+                if (grid == 0) {
+                    int rc = persistent_launch(k_spread_batch2d<T, W, false>, 128, smem, st, nullptr, &grid);
+                    if (rc) return rc;
+                }
+                k_spread_batch2d<T, W, false><<<grid, 128, smem, st>>>(a, cperm, tab);
             }
-            k_spread_batch2d<T, W><<<grid, 128, smem, st>>>(a, cperm, tab);
             ESN_CUDA_TRY(cudaGetLastError());
             return ESN_SUCCESS;
         } else {

@@ -149,7 +149,9 @@ static int ensure_key_space(esn_plan p) {
         dfree(p->block_sums);
         p->key_count = p->cursor = p->block_sums = nullptr;
         if ((rc = dmalloc(p, &p->key_count, sizeof(int) * p->nkeys))) return rc;
-        if ((rc = dmalloc(p, &p->cursor, sizeof(int) * p->nkeys))) return rc;
+        // (+64 ints: the batched spreader stages key-start rows with 16-byte
+        // copies that may run past the last key)
+        if ((rc = dmalloc(p, &p->cursor, sizeof(int) * ((size_t)p->nkeys + 64)))) return rc;
         if ((rc = dmalloc(p, &p->block_sums, sizeof(int) * ((p->nkeys + kScanTile - 1) / kScanTile + 1)))) return rc;
         p->keycap = p->nkeys;
     }
