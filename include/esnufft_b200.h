@@ -179,6 +179,24 @@ int esn_plan_destroy(esn_plan p);
 /* fft_exec(FftPlanKey, data) -- fft.py:114-124: in-place unnormalised
  * n-D FFT of ntransf device grids (n_1..n_dim), sign +1 applies
  * e^{+2 pi i l k / n} (the reference "FORWARD"). */
+/* ---- type-3 device pieces (float64 / complex128 device buffers; replace
+ * the numpy steps of transforms.py:267-351 around the composed spread and
+ * type 2).  x0 / s0: per-dimension source / target shifts, gamma: rescale
+ * factors, n: the type-3 fine grid (plan_type3_geometry, :245-264). */
+/* c_out = conj?(c_in) * e^{i sum_d s0_d (x_d - x0_d)};  xr_d = (x_d - x0_d) / gamma_d */
+int esn_type3_prephase(int dim, int64_t M, const double *x, const double *y, const double *z, const double *x0,
+                       const double *s0, const double *gamma, int conj, const void *c_in, void *c_out, double *xr,
+                       double *yr, double *zr, void *stream);
+/* inner type-2 targets t_d = (2 pi / n_d) gamma_d (s_d - s0_d) */
+int esn_type3_targets(int dim, int64_t K, const double *s1, const double *s2, const double *s3, const double *s0,
+                      const double *gamma, const int64_t *n, double *t1, double *t2, double *t3, void *stream);
+/* out *= prod_d (2 pi / n_d) / psi-hat_d(gamma_d (s_d - s0_d)) * e^{i sum_d x0_d s_d}, then conj? (in place) */
+int esn_type3_correct(int dim, int64_t K, const double *s1, const double *s2, const double *s3, const double *x0,
+                      const double *s0, const double *gamma, const int64_t *n, const esn_kernel_params *kp, int conj,
+                      void *out, void *stream);
+/* centring permutation of an (n_d..n_1) complex128 grid (numpy fftshift), out != in */
+int esn_fftshift(int dim, const int64_t *n, const void *in, void *out, void *stream);
+
 int esn_fft(int dim, int dtype, int ntransf, const int64_t *nfine,
             void *data, int sign, void *stream);
 

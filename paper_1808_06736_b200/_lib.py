@@ -69,6 +69,11 @@ SIGNATURES = {
     "esn_plan_bins": (i32, [vp, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)]),
     "esn_fold_coords": (i32, [i64, i32, vp, i64, vp, vp]),
     "esn_fft": (i32, [i32, i32, i32, P_i64, vp, i32, vp]),
+    "esn_type3_prephase": (i32, [i32, i64, vp, vp, vp, P_dbl, P_dbl, P_dbl, i32, vp, vp, vp, vp, vp, vp]),
+    "esn_type3_targets": (i32, [i32, i64, vp, vp, vp, P_dbl, P_dbl, P_i64, vp, vp, vp, vp]),
+    "esn_type3_correct": (i32, [i32, i64, vp, vp, vp, P_dbl, P_dbl, P_dbl, P_i64,
+                                ctypes.POINTER(KernelParamsC), i32, vp, vp]),
+    "esn_fftshift": (i32, [i32, P_i64, vp, vp, vp]),
     "esn_direct": (i32, [i32, i64, vp, vp, vp, vp, i64, vp, vp, vp, i32, vp, vp]),
     "esn_nufft1d1": (i32, [i64, vp, vp, i32, dbl, i64, vp, ctypes.POINTER(OptsC)]),
     "esn_nufft2d1": (i32, [i64, vp, vp, vp, i32, dbl, i64, i64, vp, ctypes.POINTER(OptsC)]),

@@ -15,6 +15,7 @@ knobs (method, bin_size, max_subprob, device).
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass, replace
 
@@ -22,10 +23,11 @@ import numpy as np
 import torch
 
 from . import _device as D
+from . import _lib
 from .errors import BadToleranceError, DataError, ResourceError, SizeError
 from .grid import ModeIndexSet, fine_grid_sizes, next_smooth
 from .kernel import MAX_TOLERANCE, MIN_TOLERANCE, KernelParams, kernel_ft, select_params
-from .plan import PLANS, Plan, raise_data_error
+from .plan import PLANS, Plan, _ptr, raise_data_error
 
 DEFAULT_GRID_CAP = 2 ** 31
 TWO_PI = 2.0 * math.pi
@@ -248,17 +250,6 @@ def plan_type3_geometry(coords, targets, params: KernelParams, sigma: float) -> 
     return Type3Geometry(tuple(x0), tuple(s0), tuple(xw), tuple(sw), tuple(sizes), tuple(gamma))
 
 
-def _psi_hat_device(params: KernelParams, alpha: float, k: torch.Tensor) -> torch.Tensor:
-    """kernel_ft on device: 2 alpha sum_j w_j phi(q_j) cos(alpha k q_j)."""
-    from .kernel import es_eval, gauss_legendre
-    q, wq = gauss_legendre(2 * params.p_quad)
-    h = len(q) // 2
-    q, wq = q[h:], wq[h:]
-    a = torch.as_tensor(wq * es_eval(q, params.beta), device=k.device)
-    qt = torch.as_tensor(np.asarray(q), device=k.device)
-    return 2.0 * alpha * (torch.cos(torch.outer(alpha * k, qt)) @ a)
-
-
 def exec_type3(coords, strengths, targets, opts: TransformOptions):
     """Nonuniform-to-nonuniform transform; returns (values, stage_seconds)."""
     params = opts.kernel_params()
@@ -292,47 +283,46 @@ def exec_type3(coords, strengths, targets, opts: TransformOptions):
         if nk == 0:
             out = torch.empty(0, dtype=torch.complex128, device=dev)
             return D.to_output(out, like_torch), timings
-        if opts.isign < 0:
-            c = torch.conj(c).resolve_conj()
         geo = plan_type3_geometry(xs, ss, params, opts.sigma)
         inner_sizes = fine_grid_sizes(geo.sizes, opts.sigma, params.w)
         _grid_cap_check(int(np.prod(geo.sizes)) + int(np.prod(inner_sizes)), opts.max_grid_values)
-        x_t = [x - sh if sh != 0.0 else x for x, sh in zip(xs, geo.x_shift)]
-        s_t = [s - sh if sh != 0.0 else s for s, sh in zip(ss, geo.s_shift)]
-        if any(sh != 0.0 for sh in geo.s_shift):
-            ph = geo.s_shift[0] * x_t[0]
-            for d in range(1, dim):
-                if geo.s_shift[d] != 0.0:
-                    ph = ph + geo.s_shift[d] * x_t[d]
-            c = c * torch.exp(1j * ph)
-        resc = [(xt / g).contiguous() for xt, g in zip(x_t, geo.gamma)]
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        x0 = (ctypes.c_double * 3)(*geo.x_shift, *([0.0] * (3 - dim)))
+        s0 = (ctypes.c_double * 3)(*geo.s_shift, *([0.0] * (3 - dim)))
+        gam = (ctypes.c_double * 3)(*geo.gamma, *([1.0] * (3 - dim)))
+        nf = _lib.i64_array(list(geo.sizes) + [1] * (3 - dim))
+        p3 = lambda ts: [_ptr(t) for t in ts] + [None] * (3 - dim)  # noqa: E731
+        # pre-phase (+ conjugation for isign < 0) and rescaled sources
+        # (transforms.py:304-312), one kernel
+        c = c.contiguous()
+        cph = torch.empty_like(c)
+        resc = [torch.empty_like(x) for x in xs]
+        _lib.check(_lib.lib.esn_type3_prephase(dim, m, *p3([x.contiguous() for x in xs]), x0, s0, gam,
+                                               int(opts.isign < 0), _ptr(c), _ptr(cph), *p3(resc), stream))
         sp = Plan(0, dim, nfine=geo.sizes, device=dev, params=params, sigma=opts.sigma,
                   use_exact_kernel=opts.use_exact_kernel, method=opts.method, dtype="float64",
                   max_grid_values=opts.max_grid_values, timing=True)
         grid = torch.empty(tuple(reversed(geo.sizes)), dtype=torch.complex128, device=dev)
         sp.setpts(resc)
-        sp.spread(c.contiguous(), grid)
+        sp.spread(cph, grid)
         sp.check()
         t1 = sp.stage_times()
         timings["sort"] += t1["sort"]
         timings["spread"] += t1["spread"]
         sp.close()
-        b = torch.fft.fftshift(grid)
-        inner = [((TWO_PI / n) * g * st).contiguous() for n, g, st in zip(geo.sizes, geo.gamma, s_t)]
+        b = torch.empty_like(grid)
+        _lib.check(_lib.lib.esn_fftshift(dim, nf, _ptr(grid), _ptr(b), stream))
+        del grid
+        inner = [torch.empty_like(s) for s in ss]
+        _lib.check(_lib.lib.esn_type3_targets(dim, nk, *p3([s.contiguous() for s in ss]), s0, gam, nf,
+                                              *p3(inner), stream))
         inner_opts = replace(opts, isign=1, check_bounds=False, params=params, dtype="float64")
-        out, tin = exec_type2(inner, b.contiguous(), inner_opts)
+        out, tin = exec_type2(inner, b, inner_opts)
         _merge_timings(timings, tin)
-        for d in range(dim):
-            alpha = np.pi * params.w / geo.sizes[d]
-            out = out * ((TWO_PI / geo.sizes[d]) / _psi_hat_device(params, alpha, geo.gamma[d] * s_t[d]))
-        if any(sh != 0.0 for sh in geo.x_shift):
-            post = torch.zeros(nk, dtype=torch.float64, device=dev)
-            for d in range(dim):
-                if geo.x_shift[d] != 0.0:
-                    post = post + geo.x_shift[d] * ss[d]
-            out = out * torch.exp(1j * post)
-        if opts.isign < 0:
-            out = torch.conj(out).resolve_conj()
+        # psi-hat correction, post-phase, final conjugation (transforms.py:333-351)
+        kp = params.to_c()
+        _lib.check(_lib.lib.esn_type3_correct(dim, nk, *p3([s.contiguous() for s in ss]), x0, s0, gam, nf,
+                                              ctypes.byref(kp), int(opts.isign < 0), _ptr(out), stream))
     return D.to_output(out, like_torch), timings
 
 
