@@ -168,13 +168,14 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU reference arm (the oracle port of the reference path, all host threads)
 
-def cpu_run(name, M_sample, T_sample, steps, warmup):
+def cpu_run(name, M_sample, T_sample, steps, warmup, dist="uniform"):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import esn_oracle as O
     O.build()
     cores = O.num_procs()
-    coords, data, cfg = cases.make_inputs(name, M=M_sample, ntransf=T_sample)
-    wcoords, wdata, _ = cases.make_inputs(name, M=min(M_sample, 2000), ntransf=T_sample)
+    coords, data, cfg = cases.make_inputs(name, M=M_sample, ntransf=T_sample, dist=dist)
+    M_sample = cfg["M_actual"]
+    wcoords, wdata, _ = cases.make_inputs(name, M=min(M_sample, 2000), ntransf=T_sample, dist=dist)
 
     def one(cs, dd):
         if cfg["ttype"] == 1:
@@ -231,7 +232,8 @@ def gpu_run(args, rank, world, local_rank):
         mode = "points"
     elif world > 1 and T > 1:
         mode = "transforms"
-    coords, data, cfg = cases.make_inputs(name, M=M, ntransf=T)
+    coords, data, cfg = cases.make_inputs(name, M=M, ntransf=T, dist=args.points)
+    M = cfg["M_actual"]
     from paper_1808_06736_b200.distributed import shard_range
     Mr, Tr = M, T
     if mode == "points":
@@ -243,7 +245,7 @@ def gpu_run(args, rank, world, local_rank):
         lo, hi = shard_range(T, rank, world)
         data = data[lo:hi]
         Tr = hi - lo
-    elif rank > 0:
+    elif rank > 0 and args.points == "uniform":
         # replicas: every rank owns an independent shard (its own seed)
         rng = np.random.default_rng(cfg["seed"] + 7919 * rank)
         coords = [rng.uniform(cfg["lo"], cfg["hi"], M) for _ in range(cfg["dim"])]
@@ -315,7 +317,7 @@ def gpu_run(args, rank, world, local_rank):
     hot_s = statistics.mean(hot)
     peak, peak_kind = peaks()
     achieved = B / hot_s / 1e9
-    res = dict(value=value, elapsed=elapsed, hot_s=hot_s, achieved=achieved, peak=peak, mode=mode,
+    res = dict(value=value, elapsed=elapsed, hot_s=hot_s, achieved=achieved, peak=peak, mode=mode, M=M,
                peak_kind=peak_kind, B=B, G=G, clocks=clk.summary(),
                stages={k: v / args.steps for k, v in stages.items()})
     # e2e through the C ABI with pinned host buffers
@@ -369,14 +371,17 @@ def e2e_run(args, cfg, coords, data, M, T, dev):
             "d2h_bytes_per_step": int(d2h), "api": "esn_nufft_host (C ABI, pinned host buffers)"}
 
 
-def config_block(name, world):
+def config_block(name, world, dist="uniform", M=None):
     cfg = cases.CONFIGS[name]
     nm = "x".join(str(v) for v in cfg["nm"])
+    M = cfg["M_full"] if M is None else M
+    pts = "iid uniform, seeded" if dist == "uniform" else f"{dist} quadrature cloud (clustered)"
     return {
-        "workload": f"{name}: {cfg['dim']}D type-{cfg['ttype']}, modes {nm}, M={cfg['M_full']:.0e}"
-                    f" per GPU, eps={cfg['tol']:g}, isign={cfg['isign']:+d}, ntransf={cfg['ntransf']}",
-        "dim": cfg["dim"], "type": cfg["ttype"], "modes": list(cfg["nm"]), "M_per_gpu": cfg["M_full"],
-        "tol": cfg["tol"], "ntransf": cfg["ntransf"], "points": "iid uniform, seeded",
+        "workload": f"{name}: {cfg['dim']}D type-{cfg['ttype']}, modes {nm}, M={M:.0e}"
+                    f" per GPU, eps={cfg['tol']:g}, isign={cfg['isign']:+d}, ntransf={cfg['ntransf']}"
+                    + ("" if dist == "uniform" else f", points {dist}"),
+        "dim": cfg["dim"], "type": cfg["ttype"], "modes": list(cfg["nm"]), "M_per_gpu": M,
+        "tol": cfg["tol"], "ntransf": cfg["ntransf"], "points": pts,
         "parallelism": f"replica shards x{world} (independent points per GPU)" if world > 1 else "1 GPU",
         "l2": "inputs larger than L2 (coords + outputs > 126 MB), no explicit flush",
     }
@@ -390,6 +395,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=list(cases.CONFIGS))
     ap.add_argument("--method", default="auto")
+    ap.add_argument("--points", default="uniform", choices=list(cases.DISTRIBUTIONS),
+                    help="point cloud: the config's iid uniform points, or the paper's clustered "
+                         "disc-quad (2D) / sph-quad (3D) quadrature clouds of about M points")
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu", dest="cpu", action="store_false")
     ap.add_argument("--stage-sync", action="store_true",
@@ -404,15 +412,16 @@ def main():
     base = {"metric": METRIC, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64" if cfg["dtype"] == "float64" else "f32",
-            "data": "synthetic (seeded iid uniform points, N(0,1) complex data; BASELINE.json shapes)"}
+            "data": "synthetic (seeded " + ("iid uniform" if args.points == "uniform" else args.points)
+                    + " points, N(0,1) complex data; BASELINE.json shapes)"}
 
     if args.impl == "reference":
         if rank != 0:
             return
         Ms, Ts = cpu_sample_size(args.config)
-        v, per, cores = cpu_run(args.config, Ms, Ts, max(1, args.steps), args.warmup)
+        v, per, cores = cpu_run(args.config, Ms, Ts, max(1, args.steps), args.warmup, args.points)
         line = dict(base, value=v, ms_per_step=per * 1e3, impl="reference",
-                    config=config_block(args.config, 1),
+                    config=config_block(args.config, 1, args.points),
                     cpu_baseline={"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                                   "sample": f"{args.config} with M={Ms:.0e}, ntransf={Ts} per step "
                                             "(oracle/ C+OpenMP restatement of the reference path, "
@@ -438,12 +447,12 @@ def main():
             except Exception:
                 traffic = None
         kern = "interp" if cfg["ttype"] == 2 else "spread"
-        # our kernels per step: setpts = count, scan x3, pos, scatter, subproblem
-        # scan + fill (8); type 2: amplify + interp; type 1: spread (batched:
+        # our kernels per step: setpts = count, scan x3, scatter, subproblem
+        # scan + fill (7); type 2: amplify + interp; type 1: spread (batched:
         # permute + row table + spread) + deconv.  cuFFT's own kernels excluded.
         hk = hot_kernel_name(cfg)
-        n_launch = 8 + (2 if cfg["ttype"] == 2 else (3 if hk == "k_spread_batch2d" else 1) + 1)
-        cb = config_block(args.config, world)
+        n_launch = 7 + (2 if cfg["ttype"] == 2 else (3 if hk == "k_spread_batch2d" else 1) + 1)
+        cb = config_block(args.config, world, args.points, res["M"])
         if res["mode"] == "points":
             cb["parallelism"] = f"points split x{world}, NCCL reduce of the partial modes"
             base["scaling"] = "strong"
@@ -464,7 +473,7 @@ def main():
         if args.cpu and world == 1:
             try:
                 Ms, Ts = cpu_sample_size(args.config)
-                v, per, cores = cpu_run(args.config, Ms, Ts, 1, 0)
+                v, per, cores = cpu_run(args.config, Ms, Ts, 1, 0, args.points)
                 line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                                         "sample": f"{args.config} with M={Ms:.0e}, ntransf={Ts}, one "
                                                   "full transform (oracle/ C+OpenMP port, scipy FFT)"}

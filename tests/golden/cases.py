@@ -40,17 +40,60 @@ CONFIGS = {
 }
 
 
-def make_inputs(name: str, M: int | None = None, ntransf: int | None = None):
+DISTRIBUTIONS = ("uniform", "disc-quad", "sph-quad")
+
+
+def quad_points(dist: str, m: int, dim: int):
+    """Clustered quadrature point clouds of the paper's benchmark section
+    (esnufft bench.py:100-139 describes them; restated here):
+
+    disc-quad (2D): a polar product grid on the disc of radius pi --
+      round(sqrt(m)) Gauss-Legendre radii on (0, pi) times as many
+      equispaced angles;
+    sph-quad (3D): round(sqrt(m)/2) Gauss-Legendre radial shells on
+      (0, pi), each an (n_lat colatitude midpoints) x (2 n_lat equispaced
+      longitudes) grid with n_lat = round(sqrt(m / (2 n_shells))).
+    The returned count is close to, not equal to, m."""
+    if dist == "disc-quad":
+        if dim != 2:
+            raise ValueError("disc-quad is 2D")
+        k = max(1, round(np.sqrt(m)))
+        r = (np.polynomial.legendre.leggauss(k)[0] + 1.0) * (PI / 2.0)
+        th = 2.0 * PI * np.arange(k) / k
+        rr, tt = np.meshgrid(r, th, indexing="ij")
+        return [(rr * np.cos(tt)).ravel(), (rr * np.sin(tt)).ravel()]
+    if dist == "sph-quad":
+        if dim != 3:
+            raise ValueError("sph-quad is 3D")
+        nr = max(1, round(np.sqrt(m) / 2.0))
+        nlat = max(1, round(np.sqrt(m / (2.0 * nr))))
+        r = (np.polynomial.legendre.leggauss(nr)[0] + 1.0) * (PI / 2.0)
+        colat = PI * (np.arange(nlat) + 0.5) / nlat
+        lon = PI * np.arange(2 * nlat) / nlat
+        rr, cc, ll = np.meshgrid(r, colat, lon, indexing="ij")
+        return [(rr * np.sin(cc) * np.cos(ll)).ravel(), (rr * np.sin(cc) * np.sin(ll)).ravel(),
+                (rr * np.cos(cc)).ravel()]
+    raise ValueError(f"unknown distribution {dist!r}")
+
+
+def make_inputs(name: str, M: int | None = None, ntransf: int | None = None, dist: str = "uniform"):
     """Return (coords list float64, data complex128, cfg) for a config.
 
     data is strengths (ntransf, M) / (M,) for type 1, or the mode array
     (N_d..N_1) for type 2.  For float32 configs coordinates are rounded to
-    float32 (then upcast) and complex data to complex64 (then upcast)."""
+    float32 (then upcast) and complex data to complex64 (then upcast).
+    dist != "uniform" replaces the coordinates by a quadrature cloud
+    (quad_points; cfg["M_actual"] holds its size)."""
     cfg = dict(CONFIGS[name])
     M = cfg["M_full"] if M is None else M
     T = cfg["ntransf"] if ntransf is None else ntransf
     rng = np.random.default_rng(cfg["seed"])
     coords = [rng.uniform(cfg["lo"], cfg["hi"], M) for _ in range(cfg["dim"])]
+    if dist != "uniform":
+        coords = quad_points(dist, M, cfg["dim"])
+        M = len(coords[0])
+    cfg["M_actual"] = M
+    cfg["dist"] = dist
     if cfg["ttype"] == 1:
         shape = (T, M) if T > 1 else (M,)
     else:

@@ -75,3 +75,28 @@ def test_bulk_and_tile_interpolators_bit_identical(tmp_path, esn):
         a = np.load(tmp_path / "bulk" / n)
         b = np.load(tmp_path / "tile" / n)
         assert np.array_equal(a, b), n
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dist,dim,ttype", [("disc-quad", 2, 1), ("disc-quad", 2, 2), ("sph-quad", 3, 1),
+                                            ("sph-quad", 3, 2)])
+def test_clustered_quadrature_clouds(esn, oracle, dist, dim, ttype):
+    """The paper's clustered benchmark clouds (dense near the origin / along
+    the axis: a few bins hold most points, so subproblems split and the
+    spreaders see their worst-case load) against the oracle."""
+    import cases
+    coords = cases.quad_points(dist, 20_000 if dim == 2 else 30_000, dim)
+    m = len(coords[0])
+    rng = np.random.default_rng(17)
+    nm = (48, 40) if dim == 2 else (20, 16, 18)
+    tol = 1e-6
+    o = esn.TransformOptions(tolerance=tol, isign=1)
+    if ttype == 1:
+        c = rng.standard_normal(m) + 1j * rng.standard_normal(m)
+        got, _ = esn.exec_type1(coords, c, nm, o)
+        ref = oracle.exec_type1(coords, c, nm, tol=tol, isign=1)
+    else:
+        f = rng.standard_normal(nm[::-1]) + 1j * rng.standard_normal(nm[::-1])
+        got, _ = esn.exec_type2(coords, f, o)
+        ref = oracle.exec_type2(coords, f, tol=tol, isign=1)
+    assert np.linalg.norm(got - ref) <= 1e-3 * tol * np.linalg.norm(ref)
