@@ -73,7 +73,8 @@ struct SetptsArgs {
     double scale[3];        // n_d / (2 pi), computed on the host (grid.py:167)
     int *key_count;         // nkeys (zeroed before)
     int *cursor;            // nkeys: exclusive scan of key_count (key start)
-    int *key;               // M: fine key of each point (original order)
+    int *key;               // M: sorted position of each point (written when store_pos)
+    int store_pos;          // keep positions in key[] (batched strength permutation)
     int *rank;              // M: rank of the point inside its key
     int *bin_start;         // nbins + 1
     int *block_sums;        // scan scratch

@@ -559,6 +559,7 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
     a.bin_start = p->bin_start;
     a.cursor = p->cursor;
     a.key = p->pkey;
+    a.store_pos = esn::batched_spread(p->dtype, p->dim, p->kp.w, p->ntransf, p->method) ? 1 : 0;
     a.rank = p->prank;
     a.rec = p->rec;
     a.flags = p->flags;

@@ -127,8 +127,8 @@ __device__ __forceinline__ void load_coords(const SetptsArgs &a, int64_t base, d
 }
 
 // Pass 1: key histogram with ranks (atomic with return: the old count is the
-// point's rank inside its key) plus the finite / bounds flags.  Stores key
-// and rank (two coalesced 4-byte writes) so the scatter pass needs no atomics.
+// point's rank inside its key) plus the finite / bounds flags.  Stores the
+// rank (one coalesced 4-byte write) so the scatter pass needs no atomics.
 template <typename XT>
 __global__ void __launch_bounds__(256, 4) k_setpts_count(SetptsArgs a) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * kILP;
@@ -147,18 +147,16 @@ __global__ void __launch_bounds__(256, 4) k_setpts_count(SetptsArgs a) {
 #pragma unroll
         for (int u = 0; u < kILP; ++u) {
             const int64_t i = base + (int64_t)u * blockDim.x;
-            if (i < a.M) {
-                a.key[i] = key[u];
-                a.rank[i] = rank[u];
-            }
+            if (i < a.M) a.rank[i] = rank[u];
         }
     }
 }
 
-// Pass 2: pos = start[key] + rank (start from the L2-resident scan), then the
-// point's full record {g, j} at pos with one 256-bit store (a whole L2
-// sector); key[] keeps pos for the batched spreader's strength permutation.
-// kSILP points per thread, all loads issued before the dependent gather.
+// Pass 2: the key again (recomputed with the grid coordinates), pos =
+// start[key] + rank (start from the L2-resident scan), then the point's full
+// record {g, j} at pos with one 256-bit store (a whole L2 sector).  Batched
+// fp32 plans keep pos in key[] for the strength permutation.  kSILP points
+// per thread, all loads issued before the dependent gather.
 template <typename XT>
 __global__ void __launch_bounds__(256) k_setpts_scatter(SetptsArgs a) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * kSILP;
@@ -167,11 +165,17 @@ __global__ void __launch_bounds__(256) k_setpts_scatter(SetptsArgs a) {
 #pragma unroll
         for (int u = 0; u < kSILP; ++u) {
             const int64_t i = base + (int64_t)u * blockDim.x;
-            pos[u] = i < a.M ? __ldg(a.key + i) : -1;
             rank[u] = i < a.M ? __ldg(a.rank + i) : 0;
         }
         double x[kSILP][3];
         load_coords<XT, kSILP>(a, base, x);
+        double g[kSILP][3];
+#pragma unroll
+        for (int u = 0; u < kSILP; ++u) {
+            const int64_t i = base + (int64_t)u * blockDim.x;
+            g[u][0] = g[u][1] = g[u][2] = 0.0;
+            pos[u] = i < a.M ? point_key(a, i, x[u], g[u], false) : -1;
+        }
 #pragma unroll
         for (int u = 0; u < kSILP; ++u)
             if (pos[u] >= 0) pos[u] = __ldg(a.cursor + pos[u]) + rank[u];  // start of the key + rank
@@ -179,13 +183,11 @@ __global__ void __launch_bounds__(256) k_setpts_scatter(SetptsArgs a) {
         for (int u = 0; u < kSILP; ++u) {
             if (pos[u] < 0) continue;
             const int64_t i = base + (int64_t)u * blockDim.x;
-            a.key[i] = pos[u];  // key[] now holds the position (the batched spreader's permutation)
-            double g[3] = {0.0, 0.0, 0.0};
-            point_key(a, i, x[u], g, false);
+            if (a.store_pos) a.key[i] = pos[u];
             const unsigned long long j = (unsigned long long)(unsigned)i;
             asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(a.rec + pos[u]),
-                         "l"(__double_as_longlong(g[0])), "l"(__double_as_longlong(g[1])),
-                         "l"(__double_as_longlong(g[2])), "l"(j)
+                         "l"(__double_as_longlong(g[u][0])), "l"(__double_as_longlong(g[u][1])),
+                         "l"(__double_as_longlong(g[u][2])), "l"(j)
                          : "memory");
         }
     }
