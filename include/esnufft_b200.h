@@ -146,6 +146,11 @@ int esn_plan_execute(esn_plan p, void *c, void *f);
  * arrays; grid is (ntransf, n_d..n_1)); spread zeroes grid itself. */
 int esn_plan_spread(esn_plan p, const void *c, void *grid);
 int esn_plan_interp(esn_plan p, const void *grid, void *c);
+/* Second half of a type-1 transform on a caller fine grid (e.g. the sum of
+ * per-GPU spreads after an NCCL reduce): cuFFT in place on grid, then the
+ * deconvolution into f (N_d..N_1).  esn_plan_spread(p, c, grid) followed by
+ * esn_plan_finish_type1(p, grid, f) equals esn_plan_execute(p, c, f). */
+int esn_plan_finish_type1(esn_plan p, void *grid, void *f);
 /* Synchronise the plan stream and report data errors found on device:
  * returns ESN_DATA_ERROR / ESN_BOUNDS_VIOLATION with the offending point
  * index in info[0] and the (1-based) dimension in info[1] (0 = strength).*/

@@ -65,6 +65,7 @@ SIGNATURES = {
     "esn_plan_device_bytes": (i64, [vp]),
     "esn_plan_destroy": (i32, [vp]),
     "esn_plan_sort_view": (i32, [vp, vp, vp, vp]),
+    "esn_plan_finish_type1": (i32, [vp, vp, vp]),
     "esn_plan_target_chunks": (i32, [vp, vp]),
     "esn_plan_bins": (i32, [vp, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)]),
     "esn_fold_coords": (i32, [i64, i32, vp, i64, vp, vp]),

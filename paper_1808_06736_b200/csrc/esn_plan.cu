@@ -652,6 +652,20 @@ int esn_plan_spread(esn_plan p, const void *c, void *grid) {
     return do_spread(p, c, grid);
 }
 
+int esn_plan_finish_type1(esn_plan p, void *grid, void *f) {
+    if (!p || p->type != 1) return fail(ESN_SIZE_ERROR, "finish_type1 needs a type-1 plan");
+    if (!grid || !f) return fail(ESN_SIZE_ERROR, "null grid or mode array");
+    int rc;
+    if ((rc = run_fft(p->dim, p->n, p->dtype, p->ntransf, grid, p->isign, p->st))) return rc;
+    if (p->dtype == ESN_F64)
+        rc = launch_deconv<double>(p->dim, p->ntransf, p->n, p->N, (const double *)grid, (const double *)p->pk[0],
+                                   (const double *)p->pk[1], (const double *)p->pk[2], (double *)f, p->st);
+    else
+        rc = launch_deconv<float>(p->dim, p->ntransf, p->n, p->N, (const float *)grid, (const float *)p->pk[0],
+                                  (const float *)p->pk[1], (const float *)p->pk[2], (float *)f, p->st);
+    return rc;
+}
+
 int esn_plan_interp(esn_plan p, const void *grid, void *c) {
     if (!p || !p->points_set) return fail(ESN_SIZE_ERROR, "plan has no points (call esn_plan_setpts first)");
     return do_interp(p, grid, c);

@@ -2,11 +2,13 @@
 
 SURVEY.md section 8(e):
 
-* one large type-1 transform (config c3) splits its POINTS across ranks;
-  each rank spreads its shard into its own fine grid, FFTs and
-  deconvolves, and the partial mode arrays are summed with one NCCL reduce
-  (exact by linearity of spreading, FFT and the diagonal correction; the
-  mode array is sigma^d = 8x smaller than the fine grid it replaces);
+* one large type-1 transform (config c3) splits its POINTS across ranks,
+  in two variants: exec_type1_point_sharded -- each rank
+  spreads its shard into its own fine grid, FFTs and deconvolves, and the
+  partial MODE arrays are summed with one NCCL reduce (exact by linearity
+  of spreading, FFT and the diagonal correction; the mode array is
+  sigma^d = 8x smaller than the fine grid); exec_type1_grid_reduced --
+  the partial FINE GRIDS are reduced and only the root runs FFT + deconv;
 * batched transforms (config c5) split their TRANSFORMS across ranks: every
   rank sorts the shared point set itself and runs its slice of strength
   vectors -- no data-path collective; the slices are gathered at the end;
@@ -72,6 +74,41 @@ def exec_type1_point_sharded(coords, strengths, num_modes, opts, *, group=None, 
         return t
     dist.reduce(buf, dst=dst, op=dist.ReduceOp.SUM, group=group)
     return t if rank == dst else None
+
+
+def _gpu_spread(coords, strengths, num_modes, opts):
+    from .transforms import spread_type1_grid
+    return spread_type1_grid(coords, strengths, num_modes, opts)
+
+
+def _gpu_finish(state, grid, num_modes, opts):
+    from .transforms import finish_type1_grid
+    return finish_type1_grid(state, grid)
+
+
+def exec_type1_grid_reduced(coords, strengths, num_modes, opts, *, group=None, dst: int | None = 0,
+                            spread=None, finish=None):
+    """Type 1 over points distributed across ranks, reducing the FINE GRID
+    (first variant): every rank spreads its shard
+    into a full fine grid, the grids are summed with one NCCL reduce (exact:
+    spreading is linear) and ``dst`` alone runs the FFT + deconvolution.  The
+    message is sigma^d x the mode array of exec_type1_point_sharded, which
+    in exchange skips the FFT on the other ranks.  ``spread(coords, c, nm,
+    opts) -> (grid, state)`` and ``finish(state, grid, nm, opts) -> modes``
+    are injectable (CPU tests)."""
+    spread = spread or _gpu_spread
+    finish = finish or _gpu_finish
+    rank, world = _world(group)
+    grid, state = spread(coords, strengths, num_modes, opts)
+    if world > 1:
+        buf = _as_real_view(grid)
+        if dst is None:
+            dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+        else:
+            dist.reduce(buf, dst=dst, op=dist.ReduceOp.SUM, group=group)
+            if rank != dst:
+                return None
+    return finish(state, grid, num_modes, opts)
 
 
 def exec_type1_transform_sharded(coords, strengths_all, num_modes, opts, *, group=None, compute=None):

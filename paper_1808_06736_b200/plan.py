@@ -128,6 +128,10 @@ class Plan:
     def spread(self, c: torch.Tensor, grid: torch.Tensor):
         _lib.check(_lib.lib.esn_plan_spread(self.h, _ptr(c), _ptr(grid)))
 
+    def finish_type1(self, grid: torch.Tensor, f: torch.Tensor):
+        """cuFFT (in place on ``grid``) + deconvolution into ``f``."""
+        _lib.check(_lib.lib.esn_plan_finish_type1(self.h, _ptr(grid), _ptr(f)))
+
     def interp(self, grid: torch.Tensor, c: torch.Tensor):
         _lib.check(_lib.lib.esn_plan_interp(self.h, _ptr(grid), _ptr(c)))
 

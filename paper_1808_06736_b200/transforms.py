@@ -168,6 +168,47 @@ def exec_type1(coords, strengths, num_modes, opts: TransformOptions):
     return D.to_output(out, like_torch), timings
 
 
+def spread_type1_grid(coords, strengths, num_modes, opts: TransformOptions):
+    """First half of a type-1 transform: the fine grid of the spread
+    (device tensor (T, n_d..n_1) / (n_d..n_1)) plus the plan that finishes it
+    with ``finish_type1_grid``.  The grid of several point shards can be
+    summed (e.g. an NCCL reduce) before finishing: spreading is linear."""
+    params = opts.kernel_params()
+    dim = len(coords)
+    nm = _as_mode_tuple(num_modes, dim)
+    ModeIndexSet(nm)
+    sizes = fine_grid_sizes(nm, opts.sigma, params.w)
+    _grid_cap_check(int(np.prod(sizes)), opts.max_grid_values)
+    dev = D.device_of(opts.device)
+    with torch.cuda.device(dev):
+        xs, m = _coords_to_device(coords, dev)
+        c = D.as_complex(strengths, dev, D.CPLX[opts.dtype])
+        ntransf = 1 if c.dim() == 1 else c.shape[0]
+        if c.shape[-1:] != (m,) or c.dim() > 2 or ntransf < 1:
+            raise SizeError(f"strengths shape {tuple(c.shape)} does not match M={m}")
+        plan = _plan_for(1, dim, nm, opts.isign, ntransf, params, opts, dev)
+        grid = torch.empty(((ntransf,) if c.dim() == 2 else ()) + tuple(reversed(sizes)), dtype=plan.cplx,
+                           device=dev)
+        with plan.lock:
+            plan.setpts(xs)
+            plan.spread(c, grid)
+            st, idx, d = plan.check_info()
+            if st:
+                raise_data_error(st, idx, d, xs, "strength")
+    return grid, plan
+
+
+def finish_type1_grid(plan: Plan, grid: torch.Tensor):
+    """Second half: cuFFT (in place on ``grid``) and deconvolution
+    (esn_plan_finish_type1); returns the modes (T, N_d..N_1) / (N_d..N_1)."""
+    lead = tuple(grid.shape[:-plan.dim])
+    out = torch.empty(lead + tuple(reversed(plan.nmodes)), dtype=plan.cplx, device=grid.device)
+    with plan.lock:
+        plan.finish_type1(grid, out)
+        plan.check()
+    return out
+
+
 def exec_type2(coords, mode_coeffs, opts: TransformOptions):
     """Uniform-to-nonuniform transform; returns (strengths, stage_seconds).
 

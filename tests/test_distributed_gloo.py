@@ -32,6 +32,28 @@ def _oracle_compute(coords, c, nm, opts):
     return torch.from_numpy(np.ascontiguousarray(out))
 
 
+def _oracle_spread(coords, c, nm, opts):
+    """First half of the oracle's type 1 (esn_oracle.exec_type1 up to the
+    spread), returning (grid tensor, state) like spread_type1_grid."""
+    import esn_oracle as O
+    params = O.select_params(opts["tol"])
+    sizes = O.fine_grid_sizes(nm, 2.0, params.w)
+    gs = [O.grid_coords(np.asarray(x), n)[0] for x, n in zip(coords, sizes)]
+    perm, _ = O.bin_sort(gs, sizes)
+    grid = O.spread(gs, perm, np.asarray(c), sizes, params)
+    return torch.from_numpy(np.ascontiguousarray(grid)), (params, sizes)
+
+
+def _oracle_finish(state, grid, nm, opts):
+    import esn_oracle as O
+    params, sizes = state
+    big = O.fft_forward(grid.numpy())
+    bins = [np.mod(O.centered(k), n) for k, n in zip(nm, sizes)]
+    out = np.ascontiguousarray(big[np.ix_(*reversed(bins))])
+    O._apply_separable(out, O._axis_corr(params, nm, sizes))
+    return torch.from_numpy(out)
+
+
 def _worker(rank, world, port, q):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -40,7 +62,7 @@ def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_1808_06736_b200.distributed import (exec_type1_point_sharded,
+        from paper_1808_06736_b200.distributed import (exec_type1_grid_reduced, exec_type1_point_sharded,
                                                        exec_type1_transform_sharded, shard_range)
         rng = np.random.default_rng(5)
         M, nm = 3000, (12, 10)
@@ -54,7 +76,12 @@ def _worker(rank, world, port, q):
         T = 5
         cb = rng.standard_normal((T, M)) + 1j * rng.standard_normal((T, M))
         batched = exec_type1_transform_sharded(coords, torch.from_numpy(cb), nm, opts, compute=_oracle_compute)
-        q.put((rank, None if full is None else full.numpy(), allr.numpy(), batched.numpy()))
+        gfull = exec_type1_grid_reduced(mine, c[lo:hi], nm, opts, dst=0, spread=_oracle_spread,
+                                        finish=_oracle_finish)
+        gall = exec_type1_grid_reduced(mine, c[lo:hi], nm, opts, dst=None, spread=_oracle_spread,
+                                       finish=_oracle_finish)
+        q.put((rank, None if full is None else full.numpy(), allr.numpy(), batched.numpy(),
+               None if gfull is None else gfull.numpy(), gall.numpy()))
     finally:
         dist.destroy_process_group()
 
@@ -80,8 +107,8 @@ def test_point_and_transform_sharding_world2(oracle):
         p.start()
     res = {}
     for _ in procs:
-        r, full, allr, batched = q.get(timeout=300)
-        res[r] = (full, allr, batched)
+        r, full, allr, batched, gfull, gall = q.get(timeout=300)
+        res[r] = (full, allr, batched, gfull, gall)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -95,6 +122,11 @@ def test_point_and_transform_sharding_world2(oracle):
     assert res[1][0] is None
     for r in (0, 1):
         assert np.linalg.norm(res[r][1] - ref) <= 1e-12 * np.linalg.norm(ref)
+    # fine-grid reduce variant: root (or every rank for all-reduce) finishes
+    assert np.linalg.norm(res[0][3] - ref) <= 1e-12 * np.linalg.norm(ref)
+    assert res[1][3] is None
+    for r in (0, 1):
+        assert np.linalg.norm(res[r][4] - ref) <= 1e-12 * np.linalg.norm(ref)
     cb = rng.standard_normal((5, M)) + 1j * rng.standard_normal((5, M))
     refb = np.stack([O.exec_type1(coords, ci, nm, tol=1e-9) for ci in cb])
     for r in (0, 1):

@@ -100,3 +100,28 @@ def test_clustered_quadrature_clouds(esn, oracle, dist, dim, ttype):
         got, _ = esn.exec_type2(coords, f, o)
         ref = oracle.exec_type2(coords, f, tol=tol, isign=1)
     assert np.linalg.norm(got - ref) <= 1e-3 * tol * np.linalg.norm(ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dim,nm,T", [(2, (40, 30), 1), (3, (16, 12, 10), 1), (3, (10, 10, 10), 3)])
+def test_spread_then_finish_equals_type1(esn, dim, nm, T):
+    """spread_type1_grid + finish_type1_grid (the fine-grid-reduce multi-GPU
+    variant's two halves, esn_plan_spread + esn_plan_finish_type1) equal the
+    one-call type 1; a sum of two shards' grids equals the unsplit result."""
+    import torch
+    from paper_1808_06736_b200.transforms import finish_type1_grid, spread_type1_grid
+    rng = np.random.default_rng(23)
+    m = 12_000
+    coords = [rng.uniform(-np.pi, np.pi, m) for _ in range(dim)]
+    c = rng.standard_normal((T, m) if T > 1 else m) + 1j * rng.standard_normal((T, m) if T > 1 else m)
+    o = esn.TransformOptions(tolerance=1e-6, isign=-1)
+    ref, _ = esn.exec_type1(coords, c, nm, o)
+    g, plan = spread_type1_grid(coords, c, nm, o)
+    got = finish_type1_grid(plan, g).cpu().numpy()
+    assert np.linalg.norm(got - ref) <= 1e-13 * np.linalg.norm(ref)
+    h = m // 2
+    g1, p1 = spread_type1_grid([x[:h] for x in coords], c[..., :h], nm, o)
+    g1 = g1.clone()
+    g2, _ = spread_type1_grid([x[h:] for x in coords], c[..., h:], nm, o)
+    both = finish_type1_grid(p1, g1 + g2).cpu().numpy()
+    assert np.linalg.norm(both - ref) <= 1e-12 * np.linalg.norm(ref)
