@@ -268,8 +268,20 @@ def gpu_run(args, rank, world, local_rank):
         gathered = [torch.empty((width,) + tuple(out.shape[1:]), dtype=cplx, device=dev) for _ in range(world)]
         padded = torch.zeros_like(gathered[0])
 
+    fine = None
+    if mode == "points" and args.reduce == "grid":
+        fine = torch.empty(tuple(reversed(plan.nfine)), dtype=cplx, device=dev)
+
     def step():
         plan.setpts(xs)
+        if fine is not None:
+            # fine-grid reduce variant: spread, NCCL-reduce the fine grids,
+            # root alone runs FFT + deconvolution
+            plan.spread(cin, fine)
+            dist.reduce(torch.view_as_real(fine), dst=0, op=dist.ReduceOp.SUM)
+            if rank == 0:
+                plan.finish_type1(fine, fout)
+            return
         plan.execute(cin, fout)
         if mode == "points":
             dist.reduce(torch.view_as_real(out), dst=0, op=dist.ReduceOp.SUM)
@@ -395,6 +407,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=list(cases.CONFIGS))
     ap.add_argument("--method", default="auto")
+    ap.add_argument("--reduce", default="modes", choices=["modes", "grid"],
+                    help="multi-GPU single 3D type 1: NCCL-reduce the per-rank mode arrays (each rank "
+                         "FFTs + deconvolves) or the fine grids (root alone finishes)")
     ap.add_argument("--points", default="uniform", choices=list(cases.DISTRIBUTIONS),
                     help="point cloud: the config's iid uniform points, or the paper's clustered "
                          "disc-quad (2D) / sph-quad (3D) quadrature clouds of about M points")
@@ -454,7 +469,8 @@ def main():
         n_launch = 7 + (2 if cfg["ttype"] == 2 else (3 if hk == "k_spread_batch2d" else 1) + 1)
         cb = config_block(args.config, world, args.points, res["M"])
         if res["mode"] == "points":
-            cb["parallelism"] = f"points split x{world}, NCCL reduce of the partial modes"
+            cb["parallelism"] = (f"points split x{world}, NCCL reduce of the partial "
+                                 + ("fine grids, root FFT + deconv" if args.reduce == "grid" else "modes"))
             base["scaling"] = "strong"
         elif res["mode"] == "transforms":
             cb["parallelism"] = f"transforms split x{world}, all-gather of the results"
