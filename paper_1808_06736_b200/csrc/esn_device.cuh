@@ -1277,6 +1277,43 @@ __global__ void __launch_bounds__(256) k_interp_group(SpreadArgs<T> a, T *cout, 
 // p1[k1] p2[k2] p3[k3] * FFT[k mod n], one thread per output mode, k1
 // fastest so both the gather (two contiguous runs per row) and the store
 // are coalesced.
+
+// Long mode rows (N1 >= 256): block items over rows (t, k3, k2) or 256-wide
+// row segments; the row's bin offsets and correction factor are computed
+// once per item and the k1 sweep is coalesced on both sides.
+template <typename T>
+__global__ void k_deconv_rows(int ntransf, int n1, int n2, int n3, int64_t N1, int64_t N2, int64_t N3,
+                              const T *grid, const T *p1, const T *p2, const T *p3, T *f, int seg) {
+    using C = typename Cx<T>::type;
+    const int64_t G = (int64_t)n1 * n2 * n3;
+    const int64_t rows = (int64_t)ntransf * N3 * N2;
+    const int nn1 = (int)N1;
+    const int nseg = (nn1 + seg - 1) / seg;
+    for (int64_t item = blockIdx.x; item < rows * nseg; item += gridDim.x) {
+        const int64_t row = item / nseg;
+        const int s0 = (int)(item - row * nseg) * seg, s1 = min(nn1, s0 + seg);
+        const int64_t t = row / (N3 * N2);
+        const int64_t r = row - t * (N3 * N2);
+        const int64_t k3i = r / N2, k2i = r - k3i * N2;
+        int64_t k2 = k2i - N2 / 2, k3 = k3i - N3 / 2;
+        if (k2 < 0) k2 += n2;
+        if (k3 < 0) k3 += n3;
+        const T f2 = p2 ? p2[k2i] : (T)1, f3 = p3 ? p3[k3i] : (T)1;
+        const C *src = reinterpret_cast<const C *>(grid) + t * G + (k3 * n2 + k2) * n1;
+        C *dst = reinterpret_cast<C *>(f) + row * N1;
+        for (int k1i = s0 + threadIdx.x; k1i < s1; k1i += blockDim.x) {
+            int k1 = k1i - nn1 / 2;
+            if (k1 < 0) k1 += n1;
+            T fac = p1[k1i];  // (p1 p2) p3
+            if (p2) fac *= f2;
+            if (p3) fac *= f3;
+            const C v = src[k1];
+            dst[k1i] = C{v.x * fac, v.y * fac};
+        }
+    }
+}
+
+// Short mode rows: one thread per mode.
 template <typename T>
 __global__ void k_deconv(int ntransf, int n1, int n2, int n3, int64_t N1, int64_t N2, int64_t N3,
                          const T *grid, const T *p1, const T *p2, const T *p3, T *f) {
@@ -1304,39 +1341,50 @@ __global__ void k_deconv(int ntransf, int n1, int n2, int n3, int64_t N1, int64_
 
 // Type-2 amplify + zero pad (transforms.py:194-200): writes the whole fine
 // grid in one pass, p_k f_k at bins k mod n and zeros elsewhere.  Also the
-// finiteness check of the mode coefficients (transforms.py:190).
+// finiteness check of the mode coefficients (transforms.py:190).  One
+// block-stride pass per grid row (t, l3, l2).
 template <typename T>
 __global__ void k_amplify(int ntransf, int n1, int n2, int n3, int64_t N1, int64_t N2, int64_t N3,
                           const T *f, const T *p1, const T *p2, const T *p3, T *grid,
-                          unsigned long long *flag) {
+                          unsigned long long *flag, int kRowSeg) {
     using C = typename Cx<T>::type;
-    const int64_t G = (int64_t)n1 * n2 * n3, total = G * ntransf, per = N1 * N2 * N3;
-    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t t = idx / G;
-        int64_t r = idx - t * G;
-        const int64_t l1 = r % n1;
-        r /= n1;
-        const int64_t l2 = r % n2;
-        const int64_t l3 = r / n2;
-        // bin l -> centered mode k: k = l for l <= N - N/2 - 1, l - n for l >= n - N/2
-        auto mode = [](int64_t l, int64_t n, int64_t N) -> int64_t {
-            if (l <= N - N / 2 - 1) return l + N / 2;
-            if (l >= n - N / 2) return l - n + N / 2;
-            return -1;
-        };
-        const int64_t m1 = mode(l1, n1, N1), m2 = mode(l2, n2, N2), m3 = mode(l3, n3, N3);
-        C out{(T)0, (T)0};
-        if (m1 >= 0 && m2 >= 0 && m3 >= 0) {
-            const int64_t fi = t * per + (m3 * N2 + m2) * N1 + m1;
-            const C v = reinterpret_cast<const C *>(f)[fi];
-            if (!finite2<T>(v)) flag_min(flag, (unsigned long long)fi);
-            T fac = p1[m1];
-            if (p2) fac *= p2[m2];
-            if (p3) fac *= p3[m3];
-            out = C{v.x * fac, v.y * fac};
+    const int64_t G = (int64_t)n1 * n2 * n3, per = N1 * N2 * N3;
+    const int64_t rows = (int64_t)ntransf * n3 * n2;
+    // bin l -> centered mode k: k = l for l <= N - N/2 - 1, l - n for l >= n - N/2
+    auto mode = [](int64_t l, int64_t n, int64_t N) -> int64_t {
+        if (l <= N - N / 2 - 1) return l + N / 2;
+        if (l >= n - N / 2) return l - n + N / 2;
+        return -1;
+    };
+    const int nseg = (n1 + kRowSeg - 1) / kRowSeg;
+    for (int64_t item = blockIdx.x; item < rows * nseg; item += gridDim.x) {
+        const int64_t row = item / nseg;
+        const int seg0 = (int)(item - row * nseg) * kRowSeg, seg1 = min(n1, seg0 + kRowSeg);
+        const int64_t t = row / ((int64_t)n3 * n2);
+        const int64_t r = row - t * ((int64_t)n3 * n2);
+        const int64_t l3 = r / n2, l2 = r - l3 * n2;
+        const int64_t m2 = mode(l2, n2, N2), m3 = mode(l3, n3, N3);
+        C *dst = reinterpret_cast<C *>(grid) + t * G + (l3 * n2 + l2) * n1;
+        if (m2 < 0 || m3 < 0) {
+            for (int l1 = seg0 + threadIdx.x; l1 < seg1; l1 += blockDim.x) dst[l1] = C{(T)0, (T)0};
+            continue;
         }
-        reinterpret_cast<C *>(grid)[idx] = out;
+        const T f2 = p2 ? p2[m2] : (T)1, f3 = p3 ? p3[m3] : (T)1;
+        const int64_t fbase = t * per + (m3 * N2 + m2) * N1;
+        for (int l1 = seg0 + threadIdx.x; l1 < seg1; l1 += blockDim.x) {
+            const int64_t m1 = mode(l1, n1, N1);
+            C out{(T)0, (T)0};
+            if (m1 >= 0) {
+                const int64_t fi = fbase + m1;
+                const C v = reinterpret_cast<const C *>(f)[fi];
+                if (!finite2<T>(v)) flag_min(flag, (unsigned long long)fi);
+                T fac = p1[m1];  // (p1 p2) p3
+                if (p2) fac *= f2;
+                if (p3) fac *= f3;
+                out = C{v.x * fac, v.y * fac};
+            }
+            dst[l1] = out;
+        }
     }
 }
 

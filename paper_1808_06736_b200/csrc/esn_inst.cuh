@@ -185,8 +185,17 @@ int launch_deconv<ESN_T>(int dim, int ntransf, const int *n, const int64_t *N, c
     (void)dim;
     const int64_t total = N[0] * N[1] * N[2] * ntransf;
     if (total == 0) return ESN_SUCCESS;
-    k_deconv<ESN_T><<<grid_for(total, 256), 256, 0, st>>>(ntransf, n[0], n[1], n[2], N[0], N[1], N[2],
-                                                          grid, p1, p2, p3, f);
+    if (N[0] >= 256) {  // long rows: whole rows per block item when there are enough, else segments
+        const int64_t rows = total / N[0];
+        const int seg = rows >= (int64_t)device_sm_count() * 8 ? (int)N[0] : 256;
+        const int64_t items = rows * ((N[0] + seg - 1) / seg);
+        const int blocks = (int)std::min<int64_t>(items, (int64_t)device_sm_count() * 32);
+        k_deconv_rows<ESN_T><<<blocks, 256, 0, st>>>(ntransf, n[0], n[1], n[2], N[0], N[1], N[2], grid, p1, p2,
+                                                     p3, f, seg);
+    } else {
+        k_deconv<ESN_T><<<grid_for(total, 256), 256, 0, st>>>(ntransf, n[0], n[1], n[2], N[0], N[1], N[2], grid, p1,
+                                                               p2, p3, f);
+    }
     ESN_CUDA_TRY(cudaGetLastError());
     return ESN_SUCCESS;
 }
@@ -198,8 +207,12 @@ int launch_amplify<ESN_T>(int dim, int ntransf, const int *n, const int64_t *N, 
     (void)dim;
     const int64_t total = (int64_t)n[0] * n[1] * n[2] * ntransf;
     if (total == 0) return ESN_SUCCESS;
-    k_amplify<ESN_T><<<grid_for(total, 256), 256, 0, st>>>(ntransf, n[0], n[1], n[2], N[0], N[1], N[2],
-                                                           f, p1, p2, p3, grid, flag);
+    const int64_t rows = total / n[0];
+    const int seg = rows >= (int64_t)device_sm_count() * 8 ? n[0] : 256;
+    const int64_t items = rows * ((n[0] + seg - 1) / seg);
+    const int blocks = (int)std::min<int64_t>(items, (int64_t)device_sm_count() * 32);
+    k_amplify<ESN_T><<<blocks, 256, 0, st>>>(ntransf, n[0], n[1], n[2], N[0], N[1], N[2],
+                                             f, p1, p2, p3, grid, flag, seg);
     ESN_CUDA_TRY(cudaGetLastError());
     return ESN_SUCCESS;
 }
