@@ -242,6 +242,14 @@ int esn_nufft3d2(int64_t M, const double *x, const double *y, const double *z,
                  int64_t N3, const void *f, const esn_opts *opts);
 /* Batched host-buffer type 1/2 (ntransf strength / mode vectors sharing
  * one point set); x,y,z may be NULL beyond dim. */
+/* Type 3 on host buffers (esnufftpy nufft{1,2,3}d3): f[k] = sum_j c[j]
+ * exp(isign i s_k . x_j) for K targets (s, t, u); float64 / complex128. */
+int esn_nufft1d3(int64_t M, const double *x, const void *c, int isign, double tol, int64_t K, const double *s,
+                 void *f, const esn_opts *opts);
+int esn_nufft2d3(int64_t M, const double *x, const double *y, const void *c, int isign, double tol, int64_t K,
+                 const double *s, const double *t, void *f, const esn_opts *opts);
+int esn_nufft3d3(int64_t M, const double *x, const double *y, const double *z, const void *c, int isign, double tol,
+                 int64_t K, const double *s, const double *t, const double *u, void *f, const esn_opts *opts);
 int esn_nufft_host(int type, int dim, int64_t M, const double *x,
                    const double *y, const double *z, int ntransf, void *c,
                    int isign, double tol, const int64_t *nmodes, void *f,

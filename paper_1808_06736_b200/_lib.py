@@ -76,6 +76,9 @@ SIGNATURES = {
                                 ctypes.POINTER(KernelParamsC), i32, vp, vp]),
     "esn_fftshift": (i32, [i32, P_i64, vp, vp, vp]),
     "esn_direct": (i32, [i32, i64, vp, vp, vp, vp, i64, vp, vp, vp, i32, vp, vp]),
+    "esn_nufft1d3": (i32, [i64, vp, vp, i32, dbl, i64, vp, vp, ctypes.POINTER(OptsC)]),
+    "esn_nufft2d3": (i32, [i64, vp, vp, vp, i32, dbl, i64, vp, vp, vp, ctypes.POINTER(OptsC)]),
+    "esn_nufft3d3": (i32, [i64, vp, vp, vp, vp, i32, dbl, i64, vp, vp, vp, vp, ctypes.POINTER(OptsC)]),
     "esn_nufft1d1": (i32, [i64, vp, vp, i32, dbl, i64, vp, ctypes.POINTER(OptsC)]),
     "esn_nufft2d1": (i32, [i64, vp, vp, vp, i32, dbl, i64, i64, vp, ctypes.POINTER(OptsC)]),
     "esn_nufft3d1": (i32, [i64, vp, vp, vp, vp, i32, dbl, i64, i64, i64, vp, ctypes.POINTER(OptsC)]),

@@ -12,6 +12,7 @@
 // is float64 only).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
 #include <cmath>
 #include <vector>
@@ -235,6 +236,184 @@ int esn_fftshift(int dim, const int64_t *n, const void *in, void *out, void *str
                                                                    (double2 *)out);
     ESN_CUDA_TRY(cudaGetLastError());
     return ESN_SUCCESS;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// One-shot host-buffer type 3 (the esnufftpy nufft{1,2,3}d3 analog,
+// bindings/src/esnufftpy/__init__.py:155-215 over transforms.py:267-351):
+// geometry on the host (min / max of the host arrays, as
+// plan_type3_geometry), then the device composition prephase -> spreader
+// plan -> fftshift -> inner type-2 plan -> correction.
+namespace {
+
+double axis_shift(double vmin, double vmax) {  // transforms.py:233-242
+    const double mid = 0.5 * (vmin + vmax);
+    if (mid == 0.0) return 0.0;
+    const double before = std::max(std::fabs(vmin), std::fabs(vmax));
+    const double after = 0.5 * (vmax - vmin);
+    return 2.0 * after < before ? mid : 0.0;
+}
+
+struct DevBuf {
+    void *p = nullptr;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    int alloc(size_t bytes) {
+        if (cudaMalloc(&p, bytes ? bytes : 16) != cudaSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+            return fail(ESN_RESOURCE_ERROR, "device allocation of %zu bytes failed", bytes);
+        }
+        return ESN_SUCCESS;
+    }
+};
+
+struct PlanGuard {
+    esn_plan p = nullptr;
+    ~PlanGuard() {
+        if (p) esn_plan_destroy(p);
+    }
+};
+
+struct StreamGuard {
+    cudaStream_t s = nullptr;
+    ~StreamGuard() {
+        if (s) cudaStreamDestroy(s);
+    }
+};
+
+int nufft_type3_host(int dim, int64_t M, const double *const *xs, const void *c, int isign, double tol, int64_t K,
+                     const double *const *ss, void *f, const esn_opts *opts) {
+    // argument misuse -> SIZE_ERROR before any core work
+    if (M < 0 || K < 0) return fail(ESN_SIZE_ERROR, "negative point or target count");
+    if (isign != 1 && isign != -1) return fail(ESN_SIZE_ERROR, "isign must be +1 or -1");
+    if ((M > 0 && !c) || (K > 0 && !f)) return fail(ESN_SIZE_ERROR, "null array argument");
+    for (int d = 0; d < dim; ++d) {
+        if (M > 0 && !xs[d]) return fail(ESN_SIZE_ERROR, "coordinate array %d missing", d + 1);
+        if (K > 0 && !ss[d]) return fail(ESN_SIZE_ERROR, "target array %d missing", d + 1);
+    }
+    esn_opts o;
+    if (opts) o = *opts; else esn_default_opts(&o);
+    o.dtype = ESN_F64;  // the reference's type 3 is float64
+    o.stream = nullptr;
+    o.timing = 0;
+    esn_kernel_params kp;
+    int rc;
+    if (o.params) kp = *o.params;
+    else if ((rc = esn_select_params(tol, o.sigma, &kp))) return rc;
+    if (K == 0) return ESN_SUCCESS;
+    // finiteness (transforms.py:282-296)
+    const double2 *ch = reinterpret_cast<const double2 *>(c);
+    for (int d = 0; d < dim; ++d) {
+        for (int64_t j = 0; j < M; ++j)
+            if (!std::isfinite(xs[d][j])) return fail(ESN_DATA_ERROR, "non-finite coordinate in dimension %d", d + 1);
+        for (int64_t k = 0; k < K; ++k)
+            if (!std::isfinite(ss[d][k])) return fail(ESN_DATA_ERROR, "non-finite target in dimension %d", d + 1);
+    }
+    for (int64_t j = 0; j < M; ++j)
+        if (!std::isfinite(ch[j].x) || !std::isfinite(ch[j].y))
+            return fail(ESN_DATA_ERROR, "non-finite strength at index %lld", (long long)j);
+    // geometry (plan_type3_geometry, transforms.py:245-264)
+    double x0[3] = {0, 0, 0}, s0[3] = {0, 0, 0}, gam[3] = {1, 1, 1};
+    int64_t n[3] = {1, 1, 1};
+    for (int d = 0; d < dim; ++d) {
+        double xmn = 0, xmx = 0, smn = 0, smx = 0;
+        if (M > 0) {
+            xmn = xmx = xs[d][0];
+            for (int64_t j = 1; j < M; ++j) { xmn = std::min(xmn, xs[d][j]); xmx = std::max(xmx, xs[d][j]); }
+        }
+        smn = smx = ss[d][0];
+        for (int64_t k = 1; k < K; ++k) { smn = std::min(smn, ss[d][k]); smx = std::max(smx, ss[d][k]); }
+        x0[d] = M > 0 ? axis_shift(xmn, xmx) : 0.0;
+        s0[d] = axis_shift(smn, smx);
+        double xh = 0.0, sh = 0.0;
+        for (int64_t j = 0; j < M; ++j) xh = std::max(xh, std::fabs(xs[d][j] - x0[d]));
+        for (int64_t k = 0; k < K; ++k) sh = std::max(sh, std::fabs(ss[d][k] - s0[d]));
+        const double se = sh > 0.0 ? sh : 1.0;
+        const int64_t want = std::max<int64_t>((int64_t)std::ceil((2.0 * o.sigma / M_PI) * xh * se) + kp.w, 2 * kp.w);
+        if ((rc = esn_next_smooth(want, &n[d]))) return rc;
+        gam[d] = (double)n[d] / (2.0 * o.sigma * se);
+    }
+    int64_t inner[3] = {1, 1, 1};
+    if ((rc = esn_fine_grid_sizes(dim, n, o.sigma, kp.w, inner))) return rc;
+    int64_t G = 1, Gi = 1;
+    for (int d = 0; d < dim; ++d) { G *= n[d]; Gi *= inner[d]; }
+    if (G + Gi > o.max_grid_values)
+        return fail(ESN_RESOURCE_ERROR, "type-3 grids need %lld complex values, over the cap of %lld",
+                    (long long)(G + Gi), (long long)o.max_grid_values);
+    // device buffers
+    StreamGuard sg;
+    ESN_CUDA_TRY(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+    o.stream = sg.s;
+    o.params = &kp;
+    DevBuf dx, dc, dcph, dxr, ds, dt, dgrid, db, dout;
+    if ((rc = dx.alloc(sizeof(double) * dim * M)) || (rc = dc.alloc(16 * M)) || (rc = dcph.alloc(16 * M)) ||
+        (rc = dxr.alloc(sizeof(double) * dim * M)) || (rc = ds.alloc(sizeof(double) * dim * K)) ||
+        (rc = dt.alloc(sizeof(double) * dim * K)) || (rc = dgrid.alloc(16 * G)) || (rc = db.alloc(16 * G)) ||
+        (rc = dout.alloc(16 * K)))
+        return rc;
+    double *px[3] = {nullptr, nullptr, nullptr}, *pr[3] = {nullptr, nullptr, nullptr};
+    double *ps[3] = {nullptr, nullptr, nullptr}, *pt[3] = {nullptr, nullptr, nullptr};
+    for (int d = 0; d < dim; ++d) {
+        px[d] = (double *)dx.p + d * M;
+        pr[d] = (double *)dxr.p + d * M;
+        ps[d] = (double *)ds.p + d * K;
+        pt[d] = (double *)dt.p + d * K;
+        if (M > 0) ESN_CUDA_TRY(cudaMemcpyAsync(px[d], xs[d], sizeof(double) * M, cudaMemcpyHostToDevice, sg.s));
+        ESN_CUDA_TRY(cudaMemcpyAsync(ps[d], ss[d], sizeof(double) * K, cudaMemcpyHostToDevice, sg.s));
+    }
+    if (M > 0) ESN_CUDA_TRY(cudaMemcpyAsync(dc.p, c, 16 * M, cudaMemcpyHostToDevice, sg.s));
+    const int conj = isign < 0;
+    if ((rc = esn_type3_prephase(dim, M, px[0], px[1], px[2], x0, s0, gam, conj, dc.p, dcph.p, pr[0], pr[1], pr[2],
+                                 sg.s)))
+        return rc;
+    {
+        PlanGuard sp;
+        esn_opts os = o;
+        os.check_bounds = 0;
+        if ((rc = esn_spreader_create(dim, n, 1, &os, &sp.p))) return rc;
+        if ((rc = esn_plan_setpts(sp.p, M, ESN_F64, pr[0], pr[1], pr[2]))) return rc;
+        if ((rc = esn_plan_spread(sp.p, dcph.p, dgrid.p))) return rc;
+        if ((rc = esn_plan_check(sp.p, nullptr))) return rc;
+    }
+    if ((rc = esn_fftshift(dim, n, dgrid.p, db.p, sg.s))) return rc;
+    if ((rc = esn_type3_targets(dim, K, ps[0], ps[1], ps[2], s0, gam, n, pt[0], pt[1], pt[2], sg.s))) return rc;
+    {
+        PlanGuard p2;
+        esn_opts o2 = o;
+        o2.check_bounds = 0;
+        if ((rc = esn_plan_create(2, dim, n, 1, 1, tol, &o2, &p2.p))) return rc;
+        if ((rc = esn_plan_setpts(p2.p, K, ESN_F64, pt[0], pt[1], pt[2]))) return rc;
+        if ((rc = esn_plan_execute(p2.p, dout.p, db.p))) return rc;
+        if ((rc = esn_plan_check(p2.p, nullptr))) return rc;
+    }
+    if ((rc = esn_type3_correct(dim, K, ps[0], ps[1], ps[2], x0, s0, gam, n, &kp, conj, dout.p, sg.s))) return rc;
+    ESN_CUDA_TRY(cudaMemcpyAsync(f, dout.p, 16 * K, cudaMemcpyDeviceToHost, sg.s));
+    ESN_CUDA_TRY(cudaStreamSynchronize(sg.s));
+    return ESN_SUCCESS;
+}
+
+}  // namespace
+
+extern "C" {
+
+int esn_nufft1d3(int64_t M, const double *x, const void *c, int isign, double tol, int64_t K, const double *s,
+                 void *f, const esn_opts *opts) {
+    const double *xs[3] = {x, nullptr, nullptr}, *ss[3] = {s, nullptr, nullptr};
+    return nufft_type3_host(1, M, xs, c, isign, tol, K, ss, f, opts);
+}
+int esn_nufft2d3(int64_t M, const double *x, const double *y, const void *c, int isign, double tol, int64_t K,
+                 const double *s, const double *t, void *f, const esn_opts *opts) {
+    const double *xs[3] = {x, y, nullptr}, *ss[3] = {s, t, nullptr};
+    return nufft_type3_host(2, M, xs, c, isign, tol, K, ss, f, opts);
+}
+int esn_nufft3d3(int64_t M, const double *x, const double *y, const double *z, const void *c, int isign, double tol,
+                 int64_t K, const double *s, const double *t, const double *u, void *f, const esn_opts *opts) {
+    const double *xs[3] = {x, y, z}, *ss[3] = {s, t, u};
+    return nufft_type3_host(3, M, xs, c, isign, tol, K, ss, f, opts);
 }
 
 }  // extern "C"

@@ -74,3 +74,40 @@ def test_host_status_codes(esn):
     st, _ = _call_host(1, [np.array([0.5])], np.ones(1, complex), (8,), 1e-20, 1, pinned=False)
     assert st == 1  # BAD_TOLERANCE
     assert "tolerance" in _lib.last_error()
+
+
+@pytest.mark.parametrize("dim", [1, 2, 3])
+@pytest.mark.parametrize("isign", [1, -1])
+def test_host_type3_matches_device_and_oracle(esn, oracle, dim, isign):
+    """esn_nufft{1,2,3}d3 (host buffers, C++ composition) against the
+    Python device composition (same kernels) and the oracle's type 3."""
+    from paper_1808_06736_b200 import _lib
+    from paper_1808_06736_b200.plan import make_opts
+    rng = np.random.default_rng(40 + dim)
+    M, K, tol = 3000, 2500, 1e-6
+    xs = [np.ascontiguousarray(rng.uniform(-2.0, 3.5, M)) for _ in range(dim)]
+    ss = [np.ascontiguousarray(rng.uniform(-40.0, 25.0, K)) for _ in range(dim)]
+    c = np.ascontiguousarray(rng.standard_normal(M) + 1j * rng.standard_normal(M))
+    f = np.zeros(K, dtype=np.complex128)
+    o, keep = make_opts(timing=False)
+    P = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+    fn = {1: _lib.lib.esn_nufft1d3, 2: _lib.lib.esn_nufft2d3, 3: _lib.lib.esn_nufft3d3}[dim]
+    st = fn(M, *[P(x) for x in xs], P(c), isign, tol, K, *[P(s) for s in ss], P(f), ctypes.byref(o))
+    assert st == 0, _lib.last_error()
+    dev, _ = esn.exec_type3(xs, c, ss, esn.TransformOptions(tolerance=tol, isign=isign))
+    assert np.linalg.norm(f - dev) <= 1e-13 * np.linalg.norm(dev)
+    ref = oracle.exec_type3(xs, c, ss, tol=tol, isign=isign)
+    assert np.linalg.norm(f - ref) <= 1e-3 * tol * np.linalg.norm(ref)
+
+
+def test_host_type3_status_codes(esn):
+    from paper_1808_06736_b200 import _lib
+    x = np.array([0.5, 1.0])
+    c = np.ones(2, complex)
+    s = np.array([1.0, np.inf])
+    f = np.zeros(2, complex)
+    P = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+    assert _lib.lib.esn_nufft1d3(2, P(x), P(c), 2, 1e-6, 2, P(s), P(f), None) == 3  # isign
+    assert _lib.lib.esn_nufft1d3(2, P(x), P(c), 1, 1e-6, 2, P(s), P(f), None) == 5  # non-finite target
+    assert "target" in _lib.last_error()
+    assert _lib.lib.esn_nufft1d3(2, P(x), P(c), 1, 1e-6, 0, P(s), P(f), None) == 0  # no targets
