@@ -1395,7 +1395,11 @@ int dispatch_w(int w, Args &&...args) {
     switch (w) {
 // ESN_WMASK (bit w set = width w compiled) trims a development build
 #ifndef ESN_WMASK
+#ifdef ESN_WMASK_DEV
+#define ESN_WMASK (ESN_WMASK_DEV)
+#else
 #define ESN_WMASK 0x1fffc
+#endif
 #endif
 #define ESN_CASE_W(WW)                                   \
     case WW:                                             \

@@ -4,6 +4,19 @@
 
 namespace esn {
 
+template <typename T, int D>
+static int launch_spread_d(const SpreadArgs<T> &a, int method, const int *key, const int *rank, const int *kstart,
+                           T *cperm, cudaStream_t st) {
+    return a.g.w <= kWidthSplit ? launch_spread_dp<T, D, 0>(a, method, key, rank, kstart, cperm, st)
+                                : launch_spread_dp<T, D, 1>(a, method, key, rank, kstart, cperm, st);
+}
+
+template <typename T, int D>
+static int launch_interp_d(const SpreadArgs<T> &a, T *cout, const T *grid, cudaStream_t st) {
+    return a.g.w <= kWidthSplit ? launch_interp_dp<T, D, 0>(a, cout, grid, st)
+                                : launch_interp_dp<T, D, 1>(a, cout, grid, st);
+}
+
 template <typename T>
 int launch_spread(const SpreadArgs<T> &a, int method, int nbins, const int *key, const int *rank, const int *kstart,
                   T *cperm, cudaStream_t st) {

@@ -5,6 +5,17 @@
 #include <cstdlib>
 #include <string>
 
+// this unit compiles the widths of part ESN_PART only (esn_internal.h
+// kWidthSplit), intersected with a development ESN_WMASK if one is given
+#ifndef ESN_PART
+#error "define ESN_PART (0: widths 2..8, 1: widths 9..16)"
+#endif
+#ifdef ESN_WMASK_DEV
+#define ESN_WMASK ((ESN_WMASK_DEV) & (ESN_PART == 0 ? 0x1fc : 0x1fe00))
+#else
+#define ESN_WMASK (0x1fffc & (ESN_PART == 0 ? 0x1fc : 0x1fe00))
+#endif
+
 #include "esn_device.cuh"
 
 namespace esn {
@@ -165,8 +176,8 @@ struct InterpOp {
 };
 
 template <>
-int launch_spread_d<ESN_T, ESN_D>(const SpreadArgs<ESN_T> &a, int method, const int *key, const int *rank,
-                                  const int *kstart, ESN_T *cperm, cudaStream_t st) {
+int launch_spread_dp<ESN_T, ESN_D, ESN_PART>(const SpreadArgs<ESN_T> &a, int method, const int *key, const int *rank,
+                                             const int *kstart, ESN_T *cperm, cudaStream_t st) {
     if (method == ESN_METHOD_GLOBAL || ESN_D == 1) return dispatch_w<ESN_T, ESN_D, SpreadGlobalOp>(a.g.w, a, st);
     if (batched_spread(sizeof(ESN_T) == 8 ? ESN_F64 : ESN_F32, ESN_D, a.g.w, a.ntransf, method))
         return dispatch_w<ESN_T, ESN_D, SpreadBatchOp>(a.g.w, a, key, rank, kstart, cperm, st);
@@ -174,11 +185,12 @@ int launch_spread_d<ESN_T, ESN_D>(const SpreadArgs<ESN_T> &a, int method, const 
 }
 
 template <>
-int launch_interp_d<ESN_T, ESN_D>(const SpreadArgs<ESN_T> &a, ESN_T *cout, const ESN_T *grid, cudaStream_t st) {
+int launch_interp_dp<ESN_T, ESN_D, ESN_PART>(const SpreadArgs<ESN_T> &a, ESN_T *cout, const ESN_T *grid,
+                                             cudaStream_t st) {
     return dispatch_w<ESN_T, ESN_D, InterpOp>(a.g.w, a, cout, grid, st);
 }
 
-#if ESN_D == 1
+#if ESN_D == 1 && ESN_PART == 0
 template <>
 int launch_deconv<ESN_T>(int dim, int ntransf, const int *n, const int64_t *N, const ESN_T *grid,
                          const ESN_T *p1, const ESN_T *p2, const ESN_T *p3, ESN_T *f, cudaStream_t st) {

@@ -1,0 +1,5 @@
+// Instantiation: complex64/float32, 1D, kernel widths 9..16.
+#define ESN_T float
+#define ESN_D 1
+#define ESN_PART 1
+#include "esn_inst.cuh"

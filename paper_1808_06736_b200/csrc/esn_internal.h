@@ -145,12 +145,15 @@ int launch_spread(const SpreadArgs<T> &a, int method, int nbins, const int *key,
 bool batched_spread(int dtype, int dim, int w, int ntransf, int method);
 template <typename T>
 int launch_interp(const SpreadArgs<T> &a, T *cout, const T *grid, cudaStream_t st);
-// per-dimension instantiations (one translation unit per (dtype, dim))
-template <typename T, int D>
-int launch_spread_d(const SpreadArgs<T> &a, int method, const int *key, const int *rank, const int *kstart,
-                    T *cperm, cudaStream_t st);
-template <typename T, int D>
-int launch_interp_d(const SpreadArgs<T> &a, T *cout, const T *grid, cudaStream_t st);
+// per-(dtype, dim, width part) instantiations, one translation unit each
+// so the heavy template sets compile in parallel: part 0 = widths 2..8,
+// part 1 = widths 9..16 (kWidthSplit)
+constexpr int kWidthSplit = 8;
+template <typename T, int D, int P>
+int launch_spread_dp(const SpreadArgs<T> &a, int method, const int *key, const int *rank, const int *kstart,
+                     T *cperm, cudaStream_t st);
+template <typename T, int D, int P>
+int launch_interp_dp(const SpreadArgs<T> &a, T *cout, const T *grid, cudaStream_t st);
 template <typename T>
 int launch_deconv(int dim, int ntransf, const int *n, const int64_t *N, const T *grid, const T *p1,
                   const T *p2, const T *p3, T *f, cudaStream_t st);
