@@ -394,6 +394,330 @@ __global__ void __launch_bounds__(RowsCfg<T, DIM, W>::NT, RowsCfg<T, DIM, W>::MI
 }
 
 // ---------------------------------------------------------------------------
+// 3D row spreader, pipelined ("rows3").  Same register ownership as
+// k_spread_rows (thread = one x-row of the bin tile, warps = 8 y x 4 z row
+// blocks), restructured around three measured costs of that kernel (c3 ncu:
+// 61 issue slots per (point, warp) pair for 16 FP64 ops, 24 % barrier and
+// exposed load latency in phase A):
+//  * the sort key inside a 3D bin is the x cell of the footprint origin only
+//    (plan: sbl = {0, inf, inf}), so a CONTIGUOUS chunk of the bin is ordered
+//    by x offset: each warp's list of covering points is a sequence of runs
+//    of equal ox, and the ox dispatch (static register window) is one switch
+//    per run instead of one per point;
+//  * a point's staged record (r1, r2 + a zero, c * r3, offsets) is one padded
+//    AoS block: every phase-B load is a broadcast or a conflict-free gather
+//    with an immediate offset, coverage is folded into the r2 index (uncovered
+//    rows read the zero), no per-lane predication;
+//  * phase A of chunk k + 1 (records + strength gather by cp.async two / one
+//    chunk ahead, Horner rows) runs after phase B of chunk k behind ONE barrier
+//    per chunk; lists are built per warp by ballot compaction (no atomics).
+template <typename T, int W>
+struct Rows3Cfg {
+    using R = RowsCfg<T, 3, W>;
+    static constexpr int BX = R::BX, X = R::X, RY = R::RY, RZ = R::RZ, NT = R::NT, MINB = R::MINB;
+    static constexpr int NW = NT / 32;
+    static constexpr int VT = 16 / (int)sizeof(T);                // T per 16-byte vector
+    static constexpr int OFN = VT;                                // (oy, oz, ox, pad) ints
+    static constexpr int R1N = (W + VT - 1) / VT * VT;           // r1, whole vectors
+    static constexpr int R2N = (W + 1 + VT - 1) / VT * VT;       // r2 + zero (uncovered rows)
+    static constexpr int CZN = 2 * W;                             // c * r3 (complex)
+    static constexpr int O_R1 = OFN, O_R2 = OFN + R1N, O_CZ = OFN + R1N + R2N;
+    static constexpr int RECN = (O_CZ + CZN + VT - 1) / VT * VT;
+    static constexpr int RECS = RECN + VT;  // stride: +16 B keeps phase-A stores conflict-free
+    static constexpr int CH = (2 * 128 * RECS * (int)sizeof(T) <= 100 * 1024) ? 128 : 64;  // points per chunk
+    static constexpr size_t STAGE_B = (size_t)CH * RECS * sizeof(T);
+    static constexpr size_t RING_B = (size_t)2 * CH * sizeof(Rec);
+    static constexpr size_t CRING_B = (size_t)CH * 2 * sizeof(T);
+    static constexpr size_t LIST_B = (size_t)NW * CH * sizeof(unsigned);
+    static constexpr size_t SMEM = 2 * STAGE_B + RING_B + CRING_B + LIST_B;
+    static_assert(2 * STAGE_B / 16 <= 0xffff && (RECS * sizeof(T)) % 16 == 0, "list entries address 16-byte units");
+    static constexpr size_t TILE_B = (size_t)RY * RZ * X * 2 * sizeof(T);
+    // flush passes over z slabs so one slab fits the two stages (the record
+    // ring may still have copies in flight)
+    static constexpr size_t FL_B = 2 * STAGE_B;
+    static constexpr int FP = TILE_B <= FL_B ? 1 : (TILE_B <= 2 * FL_B ? 2 : (TILE_B <= 4 * FL_B ? 4 : 8));
+};
+
+// phase-B operands of one point, loaded one point ahead (software pipeline)
+template <typename T>
+struct Rows3Pre {
+    typename Cx<T>::type cz;
+    T f;
+    unsigned off;  // record offset in 16-byte units
+};
+
+template <typename T, int W>
+__device__ __forceinline__ Rows3Pre<T> rows3_load(const unsigned char *stage, unsigned e, int ry, int rz) {
+    using C = typename Cx<T>::type;
+    using Cfg = Rows3Cfg<T, W>;
+    Rows3Pre<T> p;
+    p.off = e & 0xffffu;
+    const T *rec = reinterpret_cast<const T *>(stage + 16u * p.off);
+    const int2 oyz = *reinterpret_cast<const int2 *>(rec);
+    const int dy = ry - oyz.x, dz = rz - oyz.y;
+    const bool cov = (unsigned)dy < (unsigned)W && (unsigned)dz < (unsigned)W;
+    p.f = rec[Cfg::O_R2 + (cov ? dy : W)];  // r2[W] == 0
+    p.cz = *reinterpret_cast<const C *>(rec + Cfg::O_CZ + 2 * (cov ? dz : 0));
+    return p;
+}
+
+template <typename T, int W, int OX>
+__device__ __forceinline__ void rows3_apply(typename Cx<T>::type *acc, const unsigned char *stage,
+                                            const Rows3Pre<T> &p) {
+    using C = typename Cx<T>::type;
+    using Cfg = Rows3Cfg<T, W>;
+    const T *rec = reinterpret_cast<const T *>(stage + 16u * p.off);
+    const C v{p.cz.x * p.f, p.cz.y * p.f};
+    T r1[Cfg::R1N];
+    if constexpr (sizeof(T) == 8) {
+#pragma unroll
+        for (int m = 0; m < Cfg::R1N; m += 2) {
+            const double2 q = *reinterpret_cast<const double2 *>(rec + Cfg::O_R1 + m);
+            r1[m] = q.x;
+            r1[m + 1] = q.y;
+        }
+    } else {
+#pragma unroll
+        for (int m = 0; m < Cfg::R1N; m += 4) {
+            const float4 q = *reinterpret_cast<const float4 *>(rec + Cfg::O_R1 + m);
+            r1[m] = q.x;
+            r1[m + 1] = q.y;
+            r1[m + 2] = q.z;
+            r1[m + 3] = q.w;
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < W; ++m) {
+        acc[OX + m].x = fma(v.x, r1[m], acc[OX + m].x);
+        acc[OX + m].y = fma(v.y, r1[m], acc[OX + m].y);
+    }
+}
+
+// one run of equal x offset OX from the warp list (entry = record offset in
+// 16-byte units | ox << 16); the next point's operands load before this one's FMAs
+template <typename T, int W, int OX>
+__device__ __forceinline__ int rows3_run(typename Cx<T>::type *acc, const unsigned char *stage,
+                                         const unsigned *list, int i, int nq, int ry, int rz) {
+    unsigned e = list[i];
+    for (;;) {
+        rows3_apply<T, W, OX>(acc, stage, rows3_load<T, W>(stage, e, ry, rz));
+        if (++i >= nq) break;
+        e = list[i];
+        if ((e >> 16) != (unsigned)OX) break;
+    }
+    return i;
+}
+
+template <typename T, int W>
+__global__ void __launch_bounds__(Rows3Cfg<T, W>::NT, Rows3Cfg<T, W>::MINB) k_spread_rows3(SpreadArgs<T> a) {
+    using C = typename Cx<T>::type;
+    using Cfg = Rows3Cfg<T, W>;
+    constexpr int X = Cfg::X, RY = Cfg::RY, RZ = Cfg::RZ, CH = Cfg::CH, NT = Cfg::NT, RECS = Cfg::RECS;
+    constexpr int BX = Cfg::BX;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T *s_stage = reinterpret_cast<T *>(smem_raw);                                        // 2 x CH x RECS
+    Rec *s_ring = reinterpret_cast<Rec *>(smem_raw + 2 * Cfg::STAGE_B);                  // 2 x CH
+    C *s_c = reinterpret_cast<C *>(smem_raw + 2 * Cfg::STAGE_B + Cfg::RING_B);           // CH
+    unsigned *s_list = reinterpret_cast<unsigned *>(smem_raw + 2 * Cfg::STAGE_B + Cfg::RING_B + Cfg::CRING_B);  // NW x CH
+    C *s_tile = reinterpret_cast<C *>(smem_raw);  // flush slab (aliases the stages)
+    __shared__ int s_sub;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wy = warp & 1, wz = warp >> 1;  // 2 x 4 row blocks of 8 (y) x 4 (z)
+    const int ry = wy * 8 + (lane & 7), rz = wz * 4 + (lane >> 3);
+    const int by0 = wy * 8, bz0 = wz * 4;
+    // point threads (phase A, one staged point each) are the warps of the two
+    // z-edge row blocks, whose lists are about half as long as the others'
+    static_assert(NT == 256 && RZ == 16, "point-thread map assumes 2 x 4 row blocks");
+    const int pt = wz == 0 ? warp * 32 + lane : (wz == 3 ? (warp - 4) * 32 + lane : CH);  // warps 0,1,6,7
+    const int n1 = a.g.n[0], n2 = a.g.n[1], n3 = a.g.n[2];
+    const int nsub = *a.nsub;
+    unsigned *mylist = s_list + warp * CH;
+    for (;;) {
+        if (tid == 0) s_sub = atomicAdd(a.work, 1);
+        __syncthreads();
+        const int s = s_sub;
+        __syncthreads();
+        if (s >= nsub) break;
+        const int4 sp = a.subprob[s];
+        const int bin = sp.x, start = sp.y, cnt = sp.z;
+        const int b1 = bin % a.g.nb[0];
+        const int b2 = (bin / a.g.nb[0]) % a.g.nb[1];
+        const int b3 = bin / (a.g.nb[0] * a.g.nb[1]);
+        const int lo1 = b1 * a.g.bs[0], lo2 = b2 * a.g.bs[1], lo3 = b3 * a.g.bs[2];
+        const int nck = (cnt + CH - 1) / CH;
+        const int nsteps = nck * a.ntransf;
+        auto nch_of = [&](int ci) { return min(CH, cnt - ci * CH); };
+        // asynchronous staging: each point thread copies and later reads only
+        // its own ring / strength slots (no cross-thread hazards)
+        auto issue_rec = [&](int st) {
+            if (st < nsteps) {
+                const int ci = st % nck;
+                if (pt < nch_of(ci)) {
+                    const Rec *src = a.rec + start + ci * CH + pt;
+                    Rec *dst = s_ring + (st & 1) * CH + pt;
+                    cp_async16(dst, src);
+                    cp_async16(reinterpret_cast<char *>(dst) + 16, reinterpret_cast<const char *>(src) + 16);
+                }
+            }
+            cp_async_commit();
+        };
+        auto issue_c = [&](int st) {
+            if (st < nsteps) {
+                const int ci = st % nck, t = st / nck;
+                if (pt < nch_of(ci)) {
+                    const int j = s_ring[(st & 1) * CH + pt].j;
+                    const C *src = reinterpret_cast<const C *>(a.c) + (int64_t)t * a.M + j;
+                    if constexpr (sizeof(C) == 16) {
+                        cp_async16(s_c + pt, src);
+                    } else {
+                        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                                         static_cast<uint32_t>(__cvta_generic_to_shared(s_c + pt))),
+                                     "l"(src)
+                                     : "memory");
+                    }
+                }
+            }
+            cp_async_commit();
+        };
+        // phase A: kernel rows of the thread's point of step st -> stage
+        auto phase_a = [&](int st) {
+            const int ci = st % nck;
+            if (st < nsteps && pt < nch_of(ci)) {
+                const Rec rc = s_ring[(st & 1) * CH + pt];
+                const C c = s_c[pt];
+                if (!finite2<T>(c)) flag_min(&a.flags[6], (unsigned long long)(rc.j + a.ibase));
+                T *rec = s_stage + (st & 1) * CH * RECS + pt * RECS;
+                T r[W];
+                int i0 = kernel_row<T, W>(rc.g[0], a.k, r);
+                const int ox = (i0 < 0 ? i0 + n1 : i0) - lo1;
+#pragma unroll
+                for (int m = 0; m < Cfg::R1N; ++m) rec[Cfg::O_R1 + m] = m < W ? r[m] : (T)0;
+                i0 = kernel_row<T, W>(rc.g[1], a.k, r);
+                const int oy = (i0 < 0 ? i0 + n2 : i0) - lo2;
+#pragma unroll
+                for (int m = 0; m < Cfg::R2N; ++m) rec[Cfg::O_R2 + m] = m < W ? r[m] : (T)0;
+                i0 = kernel_row<T, W>(rc.g[2], a.k, r);
+                const int oz = (i0 < 0 ? i0 + n3 : i0) - lo3;
+#pragma unroll
+                for (int m = 0; m < W; ++m)
+                    *reinterpret_cast<C *>(rec + Cfg::O_CZ + 2 * m) = C{c.x * r[m], c.y * r[m]};
+                *reinterpret_cast<int4 *>(rec) = make_int4(oy, oz, ox, 0);
+            }
+        };
+        // list of the chunk's points whose w x w row footprint meets this
+        // warp's row block, in chunk (= x offset) order
+        int nq = 0;
+        auto build_list = [&](int st) {
+            const int nch = nch_of(st % nck);
+            const T *stg = s_stage + (st & 1) * CH * RECS;
+            int n = 0;
+            for (int b = 0; b < nch; b += 32) {
+                const int q = b + lane;
+                bool cov = false;
+                int ox = 0;
+                if (q < nch) {
+                    const int4 o = *reinterpret_cast<const int4 *>(stg + q * RECS);
+                    cov = o.x <= by0 + 7 && o.x + W - 1 >= by0 && o.y <= bz0 + 3 && o.y + W - 1 >= bz0;
+                    ox = o.z;
+                }
+                const unsigned bal = __ballot_sync(0xffffffffu, cov);
+                if (cov)
+                    mylist[n + __popc(bal & ((1u << lane) - 1u))] =
+                        (unsigned)(((st & 1) * Cfg::STAGE_B + q * RECS * sizeof(T)) / 16) | ((unsigned)ox << 16);
+                n += __popc(bal);
+            }
+            __syncwarp();
+            nq = n;
+        };
+        C acc[X];
+#pragma unroll
+        for (int x = 0; x < X; ++x) acc[x] = C{(T)0, (T)0};
+        auto flush = [&](int t) {
+            C *grid = reinterpret_cast<C *>(a.grid) + (int64_t)t * a.gstride;
+            constexpr int ZS = RZ / Cfg::FP;  // z rows per pass
+#pragma unroll 1
+            for (int p = 0; p < Cfg::FP; ++p) {
+                const int zlo = p * ZS;
+                if (rz >= zlo && rz < zlo + ZS) {
+                    C *dst = s_tile + ((rz - zlo) * RY + ry) * X;
+#pragma unroll
+                    for (int x = 0; x < X; ++x) dst[x] = acc[x];
+                }
+                __syncthreads();
+                for (int i = tid; i < ZS * RY * X; i += NT) {
+                    const C v = s_tile[i];
+                    if (v.x == (T)0 && v.y == (T)0) continue;
+                    const int row = i / X, x = i - row * X;
+                    const int yy = row % RY, zz = zlo + row / RY;
+                    int g1 = lo1 + x;
+                    while (g1 >= n1) g1 -= n1;
+                    int g2 = lo2 + yy;
+                    while (g2 >= n2) g2 -= n2;
+                    int g3 = lo3 + zz;
+                    while (g3 >= n3) g3 -= n3;
+                    red_add(grid + ((int64_t)g3 * n2 + g2) * n1 + g1, v);
+                }
+                __syncthreads();
+            }
+#pragma unroll
+            for (int x = 0; x < X; ++x) acc[x] = C{(T)0, (T)0};
+        };
+        // prologue: step 0 staged and listed
+        issue_rec(0);
+        cp_async_wait<0>();
+        issue_c(0);
+        issue_rec(1);
+        cp_async_wait<1>();
+        phase_a(0);
+        __syncthreads();
+        build_list(0);
+#pragma unroll 1
+        for (int st = 0; st < nsteps; ++st) {
+            cp_async_wait<0>();  // own record of step st + 1
+            issue_c(st + 1);
+            issue_rec(st + 2);
+            // phase B: runs of equal x offset, one static dispatch per run
+            {
+                const unsigned char *stg = smem_raw;
+                int i = 0;
+                while (i < nq) {
+                    const int ox = mylist[i] >> 16;
+                    switch (ox) {
+#define ESN_R3_CASE(OX)                                                                  \
+    case OX:                                                                             \
+        if constexpr (OX < BX) i = rows3_run<T, W, OX>(acc, stg, mylist, i, nq, ry, rz); \
+        else i = nq;                                                                     \
+        break;
+                        ESN_R3_CASE(0) ESN_R3_CASE(1) ESN_R3_CASE(2) ESN_R3_CASE(3)
+                        ESN_R3_CASE(4) ESN_R3_CASE(5) ESN_R3_CASE(6) ESN_R3_CASE(7)
+                        ESN_R3_CASE(8) ESN_R3_CASE(9) ESN_R3_CASE(10) ESN_R3_CASE(11)
+                        ESN_R3_CASE(12) ESN_R3_CASE(13) ESN_R3_CASE(14) ESN_R3_CASE(15)
+                        ESN_R3_CASE(16) ESN_R3_CASE(17) ESN_R3_CASE(18) ESN_R3_CASE(19)
+                        ESN_R3_CASE(20) ESN_R3_CASE(21) ESN_R3_CASE(22) ESN_R3_CASE(23)
+                        ESN_R3_CASE(24) ESN_R3_CASE(25) ESN_R3_CASE(26) ESN_R3_CASE(27)
+                        ESN_R3_CASE(28) ESN_R3_CASE(29) ESN_R3_CASE(30) ESN_R3_CASE(31)
+#undef ESN_R3_CASE
+                        default:
+                            i = nq;
+                            break;
+                    }
+                }
+            }
+            cp_async_wait<1>();  // own strength of step st + 1
+            if ((st + 1) % nck == 0) {  // transform st / nck complete
+                __syncthreads();
+                flush(st / nck);
+            }
+            phase_a(st + 1);
+            __syncthreads();
+            if (st + 1 < nsteps) build_list(st + 1);
+        }
+        cp_async_wait<0>();
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Batched 2D spreader (ntransf > 1): lanes are transforms.  A CTA owns one
 // bin tile (rows y of length X in registers) for 32 transforms at a time
 // (one warp per tile row, lane = transform); every staged point is applied by

@@ -58,6 +58,23 @@ struct SpreadRowsOp {
         if constexpr (D == 1) {
             return SpreadGlobalOp<T, D, W>::run(a, st);
         } else {
+        if constexpr (D == 3) {
+            static const bool old_rows = [] {
+                const char *e = getenv("ESN_SPREAD3");
+                return e && std::string(e) == "rows";
+            }();
+            if (!old_rows) {
+                using Cfg3 = Rows3Cfg<T, W>;
+                static int grid3 = 0;
+                if (grid3 == 0) {
+                    int rc = persistent_launch(k_spread_rows3<T, W>, Cfg3::NT, Cfg3::SMEM, st, nullptr, &grid3);
+                    if (rc) return rc;
+                }
+                k_spread_rows3<T, W><<<grid3, Cfg3::NT, Cfg3::SMEM, st>>>(a);
+                ESN_CUDA_TRY(cudaGetLastError());
+                return ESN_SUCCESS;
+            }
+        }
         using Cfg = RowsCfg<T, D, W>;
         using C = typename Cx<T>::type;
         constexpr int NZ = D == 3 ? W : 1;

@@ -255,11 +255,21 @@ static void set_key_space(esn_plan p, int nchunk, int64_t maxkeys) {
     p->nchunk = nchunk;
     p->nbk = p->nbins * nchunk;
     for (int d = 0; d < 3; ++d) p->sbl[d] = 0;
+    // sub-cells per bin along d: ceil(bs / 2^sbl)
+    auto sub = [&](int d) { return ((p->geom.bs[d] - 1) >> p->sbl[d]) + 1; };
     auto keys = [&]() {
         int64_t k = p->nbk;
-        for (int d = 0; d < dim; ++d) k *= (p->geom.bs[d] >> p->sbl[d]);
+        for (int d = 0; d < dim; ++d) k *= sub(d);
         return k;
     };
+    if (dim == 3 && p->type != 2 && p->method != ESN_METHOD_GLOBAL) {
+        // 3D row spreader (k_spread_rows3): the key inside a bin is the x cell
+        // of the footprint origin only, so contiguous chunks are x-ordered
+        p->sbl[1] = p->sbl[2] = 30;
+        p->spb = sub(0);
+        p->nkeys = (int)keys();
+        return;
+    }
     for (int guard = 0; guard < 64 && keys() > maxkeys; ++guard) {
         bool grew = false;
         for (int d = 0; d < dim && keys() > maxkeys; ++d) {
@@ -272,7 +282,7 @@ static void set_key_space(esn_plan p, int nchunk, int64_t maxkeys) {
         if (!grew) break;
     }
     p->spb = 1;
-    for (int d = 0; d < dim; ++d) p->spb *= p->geom.bs[d] >> p->sbl[d];
+    for (int d = 0; d < dim; ++d) p->spb *= sub(d);
     p->nkeys = (int)keys();
 }
 

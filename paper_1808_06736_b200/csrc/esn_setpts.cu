@@ -103,7 +103,7 @@ __device__ __forceinline__ int point_key(const SetptsArgs &a, int64_t i, const d
         bin += q * bmul;
         bmul *= a.g.nb[d];
         loc += ((i0 - q * bs) >> a.sbl[d]) * lmul;
-        lmul *= bs >> a.sbl[d];
+        lmul *= ((bs - 1) >> a.sbl[d]) + 1;
     }
     if (a.chunk_len > 0) bin += (int)(i / a.chunk_len) * a.nbins_geo;
     return bin * a.spb + loc;
