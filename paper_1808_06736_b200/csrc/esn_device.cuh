@@ -973,6 +973,253 @@ __global__ void __launch_bounds__(128) k_spread_batch2d(SpreadArgs<T> a, const T
     }
 }
 
+// ---------------------------------------------------------------------------
+// Batched 2D spreader, owner-computes ("b2own").  A bin of 16 x 16 footprint
+// origins is also an OUTPUT block: the warp of work item (bin, transform
+// group, output row pair) owns fine cells [lo1, lo1 + 16) of rows gy, gy + 1
+// for 32 transforms (lane = transform) and gathers every point whose
+// footprint reaches them -- origins in rows gy - w + 1 .. gy + 1 (wrapped,
+// possibly in the bin below) and columns lo1 - w + 1 .. lo1 + 15 (wrapped,
+// possibly in the bin to the left).  Each fine cell is written exactly once
+// with a plain coalesced store: no grid memset, no atomics, no halo flush
+// (the tile spreader k_spread_batch2d spent ~1/3 of its time in RED flushes
+// and the grid was zeroed first); DRAM traffic is the algorithmic bytes
+// (ncu: 570 MB read, 500 MB written for c5).  Points come in pieces of
+// <= kBatchPts staged by cp.async one piece ahead (tab rows + 256-byte
+// strength lines) in source-cell order; the x offset (= source cell, kept
+// per slot, so periodic duplicates on tiny grids are ordinary cells) selects
+// a static register window through one switch per point (a branch tree on
+// sm_100a, ~10 instructions) that serves both output rows, and only the
+// FMAs that land in owned columns are formed.
+// per-warp shared memory: 2 piece stages + per source row the lanes' first
+// point / staged offset (plus the row's total and run mask)
+constexpr int kB2Rows = 2;  // output rows per work item (register window per row: 2 (w - 1) + 16 cells)
+template <typename T, int W>
+constexpr size_t b2own_row_bytes() { return ((size_t)(W + kB2Rows - 1) * (2 * 32 + 2) * sizeof(int) + 15) / 16 * 16; }
+template <typename T, int W>
+constexpr size_t b2own_smem_bytes() { return 4 * (2 * batch2d_stage_bytes<T, W>() + b2own_row_bytes<T, W>()); }
+
+template <typename T, int W>
+__global__ void __launch_bounds__(128) k_spread_b2own(SpreadArgs<T> a, const T *cperm, const PtRows2<W> *tab) {
+    constexpr int R = kB2Rows;
+    using C = typename Cx<T>::type;
+    constexpr int BX = Batch2Cfg<T, W>::BX, BY = Batch2Cfg<T, W>::BY;
+    constexpr int H = W - 1;            // halo cells
+    constexpr int SRC = BX + H;         // source cells per source row (lanes)
+    constexpr int NR = W + R - 1;       // source rows per item
+    constexpr int NB = kBatchPts;
+    constexpr int TB = sizeof(PtRows2<W>), CB = 32 * sizeof(C);
+    constexpr size_t STAGE = batch2d_stage_bytes<T, W>();
+    static_assert(SRC < 32, "one lane per source cell (+ the end lane)");
+    static_assert((size_t)NB * (TB + CB) + NB <= STAGE, "stage holds a piece and its x offsets");
+    static_assert(2 * STAGE >= (size_t)32 * (BX + 1) * sizeof(C), "store slab fits the ring");
+    static_assert(BY % R == 0, "row groups tile the bin");
+    extern __shared__ __align__(16) unsigned char b2_smem[];
+    const int lane = threadIdx.x & 31;
+    unsigned char *wbase = b2_smem + (threadIdx.x >> 5) * (2 * STAGE + b2own_row_bytes<T, W>());
+    int *rs = reinterpret_cast<int *>(wbase + 2 * STAGE);  // [d][32] first point of the lane's cell
+    int *ro = rs + NR * 32;                                  // [d][32] staged offset of the lane's cell
+    int *rt = ro + NR * 32;                                  // [d] row total
+    unsigned *rr = reinterpret_cast<unsigned *>(rt + NR);    // [d] run-start mask
+    const int n1 = a.g.n[0], n2 = a.g.n[1], nb0 = a.g.nb[0];
+    const int ngroups = (a.ntransf + 31) / 32;
+    const int nitems = a.g.nb[0] * a.g.nb[1] * ngroups * (BY / R);
+    int next = 0;
+    if (lane == 0) next = atomicAdd(a.work, 1);
+    for (;;) {
+        const int item = __shfl_sync(0xffffffffu, next, 0);
+        if (item >= nitems) break;
+        if (lane == 0) next = atomicAdd(a.work, 1);
+        const int yp = item % (BY / R);
+        const int sg = item / (BY / R);
+        const int tg = sg % ngroups, bin = sg / ngroups;
+        const int lo1 = (bin % nb0) * BX, lo2 = (bin / nb0) * BY;
+        const int gy = lo2 + R * yp;  // output rows gy .. gy + R - 1 (acc[0..R))
+        if (gy >= n2) continue;       // partial last bin row
+        // lane k < SRC: source cell column lo1 - H + k (wrapped); own columns
+        // past n1 (partial last bin) hold no points
+        int xa = lo1 - H + lane;
+        const bool valid = lane < SRC && !(lane >= H && xa >= n1);
+        while (xa < 0) xa += n1;  // (loops only on grids narrower than the halo)
+        while (xa >= n1) xa -= n1;
+        __syncwarp();  // previous item's readers of the row tables are done
+        // source row d: origin row gy + R - 1 - d (output row gy + rr takes r2[rr + d - R + 1])
+#pragma unroll
+        for (int d = 0; d < NR; ++d) {
+            int r = gy + R - 1 - d;
+            while (r < 0) r += n2;
+            while (r >= n2) r -= n2;
+            int s = 0, e = 0;
+            if (valid) {
+                const int key = (((r / BY) * nb0 + xa / BX) * BY + (r % BY)) * BX + (xa % BX);
+                s = a.kstart[key];
+                e = a.kstart[key + 1];
+            }
+            const int cnt = e - s;
+            int inc = cnt;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, inc, off);
+                if (lane >= off) inc += v;
+            }
+            const int eprev = __shfl_up_sync(0xffffffffu, e, 1);
+            // a run is a chain of abutting ranges (empty cells may start one)
+            const unsigned runs = __ballot_sync(0xffffffffu, valid && (lane == 0 || s != eprev));
+            rs[d * 32 + lane] = s;
+            ro[d * 32 + lane] = inc - cnt;  // lane SRC holds the row total
+            if (lane == 31) {
+                rt[d] = inc;
+                rr[d] = runs;
+            }
+        }
+        __syncwarp();
+        const C *cg = reinterpret_cast<const C *>(cperm) + (int64_t)tg * a.M * 32;
+        // stage piece (d, q0): staged indices [q0, q0 + NB) of source row d
+        auto issue_piece = [&](int d, int q0, int buf) {
+            if (d < NR) {
+                unsigned char *dst = wbase + buf * STAGE;
+                const int tot = rt[d];
+                const int q1 = min(q0 + NB, tot);
+                unsigned rm = rr[d];
+                while (rm) {
+                    const int k0 = __ffs(rm) - 1;
+                    rm &= rm - 1;
+                    const int k1 = rm ? __ffs(rm) - 1 : 32;
+                    const int ok0 = ro[d * 32 + k0];
+                    const int ok1 = k1 < 32 ? ro[d * 32 + k1] : tot;
+                    const int a0 = max(ok0, q0), a1 = min(ok1, q1);
+                    if (a0 >= a1) continue;
+                    const int n = a1 - a0, src0 = rs[d * 32 + k0] + (a0 - ok0), slot0 = a0 - q0;
+                    const char *ts = reinterpret_cast<const char *>(tab + src0);
+                    for (int c = lane; c < n * TB / 16; c += 32)
+                        cp_async16(dst + slot0 * TB + 16 * c, ts + 16 * c);
+                    const char *cs = reinterpret_cast<const char *>(cg + (int64_t)src0 * 32);
+                    for (int c = lane; c < n * CB / 16; c += 32)
+                        cp_async16(dst + NB * TB + slot0 * CB + 16 * c, cs + 16 * c);
+                }
+                // x offset (= source cell) of every staged slot
+                unsigned char *sox = dst + NB * (TB + CB);
+                const int myo = ro[d * 32 + lane];
+                const int c0 = max(myo, q0), c1 = min(lane + 1 < 32 ? ro[d * 32 + lane + 1] : myo, q1);
+                for (int q = c0; q < c1; ++q) sox[q - q0] = (unsigned char)lane;
+            }
+            cp_async_commit();
+        };
+        auto advance = [&](int &d, int &q0) {  // next non-empty piece after (d, q0)
+            q0 += NB;
+            if (q0 < rt[d]) return;
+            q0 = 0;
+            for (++d; d < NR && rt[d] == 0; ++d) {
+            }
+        };
+        // owned cells only: contributions that land in the halo columns
+        // belong to the neighbouring block's warp and are never formed
+        C acc[R][BX];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+            for (int x = 0; x < BX; ++x) acc[rr][x] = C{(T)0, (T)0};
+        int pd = 0, pq = 0;
+        while (pd < NR && rt[pd] == 0) ++pd;
+        issue_piece(pd, pq, 0);
+        int buf = 0;
+        while (pd < NR) {
+            int nd = pd, nq = pq;
+            advance(nd, nq);
+            issue_piece(nd, nq, buf ^ 1);
+            cp_async_wait<1>();
+            __syncwarp();
+            const int np = min(NB, rt[pd] - pq);
+            const unsigned char *sb = wbase + buf * STAGE;
+            const PtRows2<W> *tb = reinterpret_cast<const PtRows2<W> *>(sb);
+            const C *cq = reinterpret_cast<const C *>(sb + NB * TB) + lane;
+            int wi[R];
+            bool wh[R];
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) {
+                const int dy = rr + pd - (R - 1);
+                wh[rr] = dy >= 0 && dy < W;
+                wi[rr] = wh[rr] ? dy : 0;
+            }
+            const unsigned char *sox = sb + NB * (TB + CB);
+#pragma unroll 1
+            for (int k = 0; k < np; ++k) {
+                const PtRows2<W> &e = tb[k];
+                const C cc = cq[k * 32];
+                C v[R];
+#pragma unroll
+                for (int rr = 0; rr < R; ++rr) {
+                    const T wy = wh[rr] ? (T)e.r2[wi[rr]] : (T)0;
+                    v[rr] = C{cc.x * wy, cc.y * wy};
+                }
+                T r1[W];
+#pragma unroll
+                for (int m = 0; m < W; ++m) r1[m] = (T)e.r1[m];
+                // one static dispatch per point (branch tree) serves all R rows
+#define ESN_B2O_CASE(OX)                                                      \
+    case OX:                                                                  \
+        if constexpr (OX < SRC) {                                             \
+            _Pragma("unroll") for (int m = 0; m < W; ++m) {                   \
+                constexpr int XL = OX - H;                                    \
+                if (XL + m >= 0 && XL + m < BX) {                             \
+                    _Pragma("unroll") for (int rr = 0; rr < R; ++rr) {        \
+                        acc[rr][XL + m].x = fma(v[rr].x, r1[m], acc[rr][XL + m].x); \
+                        acc[rr][XL + m].y = fma(v[rr].y, r1[m], acc[rr][XL + m].y); \
+                    }                                                         \
+                }                                                             \
+            }                                                                 \
+        }                                                                     \
+        break;
+                switch (sox[k]) {
+                    ESN_B2O_CASE(0) ESN_B2O_CASE(1) ESN_B2O_CASE(2) ESN_B2O_CASE(3)
+                    ESN_B2O_CASE(4) ESN_B2O_CASE(5) ESN_B2O_CASE(6) ESN_B2O_CASE(7)
+                    ESN_B2O_CASE(8) ESN_B2O_CASE(9) ESN_B2O_CASE(10) ESN_B2O_CASE(11)
+                    ESN_B2O_CASE(12) ESN_B2O_CASE(13) ESN_B2O_CASE(14) ESN_B2O_CASE(15)
+                    ESN_B2O_CASE(16) ESN_B2O_CASE(17) ESN_B2O_CASE(18) ESN_B2O_CASE(19)
+                    ESN_B2O_CASE(20) ESN_B2O_CASE(21) ESN_B2O_CASE(22) ESN_B2O_CASE(23)
+                    ESN_B2O_CASE(24) ESN_B2O_CASE(25) ESN_B2O_CASE(26) ESN_B2O_CASE(27)
+                    ESN_B2O_CASE(28) ESN_B2O_CASE(29) ESN_B2O_CASE(30)
+                    default:
+                        break;
+                }
+#undef ESN_B2O_CASE
+            }
+            __syncwarp();
+            buf ^= 1;
+            pd = nd;
+            pq = nq;
+        }
+        cp_async_wait<0>();
+        __syncwarp();
+        // owned cells: transpose through the warp's ring so
+        // each store covers one transform's contiguous 16-cell run (two
+        // transforms per instruction)
+        C *slab = reinterpret_cast<C *>(wbase);
+        const int hx = lane & (BX - 1), ht = lane / BX;
+        const int g1 = lo1 + hx;
+        const int tmax = min(32, a.ntransf - tg * 32);
+#pragma unroll
+        for (int row = 0; row < R; ++row) {
+            const int gyr = gy + row;
+#pragma unroll
+            for (int x = 0; x < BX; ++x) slab[lane * (BX + 1) + x] = acc[row][x];
+            __syncwarp();
+            if (g1 < n1 && gyr < n2) {
+                for (int tt = ht; tt < tmax; tt += 32 / BX) {
+                    C *dstp = reinterpret_cast<C *>(a.grid) + (int64_t)(tg * 32 + tt) * a.gstride +
+                              (int64_t)gyr * n1 + g1;
+                    const C v = slab[tt * (BX + 1) + hx];
+                    if (a.accumulate)
+                        red_add(dstp, v);  // concurrent partial spreads (pipelined host path) into one grid
+                    else
+                        *dstp = v;
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
 // Batched strengths into sorted order, 32 transforms per point:
 // cperm[g][pos(j)][l] = c[32 g + l][j] with pos(j) = start[key[j]] + rank[j].
 // A 32 x 32 tile transpose through shared memory: coalesced reads along j,

@@ -112,7 +112,15 @@ struct SpreadBatchOp {
             k_rows2d<T, W><<<grid_for(a.M, 256), 256, 0, st>>>(a, tab);
             constexpr size_t smem = batch2d_smem_bytes<T, W>();
             // cell-resolution sort keys -> static x-offset sweep; else per-point dispatch
-            if (a.sbl[0] == 0 && a.sbl[1] == 0 && a.g.bs[0] == Cfg::BX) {
+            if (batched_owner(ESN_F32, 2, W, a.ntransf, ESN_METHOD_TILE, a.sbl, a.g.bs)) {
+                constexpr size_t osmem = b2own_smem_bytes<T, W>();
+                static int grid = 0;
+                if (grid == 0) {
+                    int rc = persistent_launch(k_spread_b2own<T, W>, 128, osmem, st, nullptr, &grid);
+                    if (rc) return rc;
+                }
+                k_spread_b2own<T, W><<<grid, 128, osmem, st>>>(a, cperm, tab);
+            } else if (a.sbl[0] == 0 && a.sbl[1] == 0 && a.g.bs[0] == Cfg::BX) {
                 static int grid = 0;
                 if (grid == 0) {
                     int rc = persistent_launch(k_spread_batch2d<T, W, true>, 128, smem, st, nullptr, &grid);

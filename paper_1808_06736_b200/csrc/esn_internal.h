@@ -103,6 +103,7 @@ struct SpreadArgs {
     int64_t gstride;         // complex cells per transform
     int64_t ibase;           // index offset of this point chunk (error reports)
     unsigned long long *flags;  // [6] first non-finite strength
+    int accumulate;          // add into the grid (owner-computes spreaders; else they overwrite it)
 };
 
 // ---- compile-time geometry of the spreaders (shared with the host planner)
@@ -143,6 +144,9 @@ int launch_spread(const SpreadArgs<T> &a, int method, int nbins, const int *key,
                   const int *kstart, T *cperm, cudaStream_t st);
 // does the batched 2D path (needs a permuted-strength scratch) apply?
 bool batched_spread(int dtype, int dim, int w, int ntransf, int method);
+// does the batched 2D owner-computes spreader (writes every fine cell, no
+// memset needed) apply?  Needs cell-resolution keys over 16 x 16 bins.
+bool batched_owner(int dtype, int dim, int w, int ntransf, int method, const int *sbl, const int *bs);
 template <typename T>
 int launch_interp(const SpreadArgs<T> &a, T *cout, const T *grid, cudaStream_t st);
 // per-(dtype, dim, width part) instantiations, one translation unit each

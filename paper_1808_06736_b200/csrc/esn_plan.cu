@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <string>
 #include <mutex>
 #include <chrono>
 #include <tuple>
@@ -612,6 +613,15 @@ bool esn::batched_spread(int dtype, int dim, int w, int ntransf, int method) {
     return method != ESN_METHOD_GLOBAL && dim == 2 && dtype == ESN_F32 && ntransf > 1 && w <= 10;
 }
 
+bool esn::batched_owner(int dtype, int dim, int w, int ntransf, int method, const int *sbl, const int *bs) {
+    static const bool off = [] {
+        const char *e = getenv("ESN_B2");
+        return e && std::string(e) == "tile";
+    }();
+    return !off && batched_spread(dtype, dim, w, ntransf, method) && sbl[0] == 0 && sbl[1] == 0 &&
+           bs[0] == Batch2Cfg<float, 2>::BX && bs[1] == Batch2Cfg<float, 2>::BY;
+}
+
 static int do_spread(esn_plan p, const void *c, void *grid, bool zero = true) {
     // the bin-structured spreaders need their own bin geometry and the
     // geometric sort; a type-2 plan (interpolation bins, possibly a
@@ -630,14 +640,22 @@ static int do_spread(esn_plan p, const void *c, void *grid, bool zero = true) {
             p->cperm_bytes = need;
         }
     }
-    if (zero) ESN_CUDA_TRY(cudaMemsetAsync(grid, 0, real_size(p->dtype) * 2 * (size_t)p->G * p->ntransf, p->st));
+    // the owner-computes batched spreader writes every fine cell itself
+    const bool owner = esn::batched_owner(p->dtype, p->dim, p->kp.w, p->ntransf, method, p->sbl, p->geom.bs);
+    if (zero && !owner)
+        ESN_CUDA_TRY(cudaMemsetAsync(grid, 0, real_size(p->dtype) * 2 * (size_t)p->G * p->ntransf, p->st));
     ESN_CUDA_TRY(cudaMemsetAsync(p->work, 0, sizeof(int), p->st));
     if (p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[6], p->st));
-    int rc = p->dtype == ESN_F64
-                 ? launch_spread<double>(make_spread_args<double>(p, c, grid), method, p->nbins, p->pkey,
-                                         p->prank, p->cursor, (double *)p->cperm, p->st)
-                 : launch_spread<float>(make_spread_args<float>(p, c, grid), method, p->nbins, p->pkey,
-                                        p->prank, p->cursor, (float *)p->cperm, p->st);
+    int rc;
+    if (p->dtype == ESN_F64) {
+        SpreadArgs<double> a = make_spread_args<double>(p, c, grid);
+        a.accumulate = zero ? 0 : 1;
+        rc = launch_spread<double>(a, method, p->nbins, p->pkey, p->prank, p->cursor, (double *)p->cperm, p->st);
+    } else {
+        SpreadArgs<float> a = make_spread_args<float>(p, c, grid);
+        a.accumulate = zero ? 0 : 1;
+        rc = launch_spread<float>(a, method, p->nbins, p->pkey, p->prank, p->cursor, (float *)p->cperm, p->st);
+    }
     if (!rc && p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[7], p->st));
     return rc;
 }

@@ -275,7 +275,10 @@ __global__ void __launch_bounds__(1024) k_scan_down(const int *cnt, int n, const
         }
         e += v[u];
     }
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) bin_start[nbins] = block_sums[gridDim.x];
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+        bin_start[nbins] = block_sums[gridDim.x];
+        cursor[n] = block_sums[gridDim.x];  // end of the last key (cell-range readers use key + 1)
+    }
 }
 
 // Subproblem counts per bin (ceil(count / max_subprob)) -> exclusive scan ->

@@ -125,3 +125,27 @@ def test_spread_then_finish_equals_type1(esn, dim, nm, T):
     g2, _ = spread_type1_grid([x[h:] for x in coords], c[..., h:], nm, o)
     both = finish_type1_grid(p1, g1 + g2).cpu().numpy()
     assert np.linalg.norm(both - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nm,T,m,clustered", [
+    ((13, 9), 3, 4000, False),      # fine grid narrower than one 16 x 16 block: wrapped halo cells
+    ((37, 21), 33, 20_000, False),  # partial last blocks in x and y, a partial second transform group
+    ((64, 48), 4, 60_000, True),    # clustered: hundreds of points per cell, many pieces per source row
+])
+def test_batched_owner_spreader(esn, oracle, nm, T, m, clustered):
+    """float32 batched 2D type 1 goes through the owner-computes spreader
+    (k_spread_b2own: every fine cell written once by its block's warp); the
+    single transforms go through the row spreader, an independent kernel."""
+    rng = np.random.default_rng(11)
+    lo, hi = (-np.pi, -np.pi + 0.3) if clustered else (-np.pi, np.pi)
+    coords = [rng.uniform(lo, hi, m).astype(np.float32) for _ in range(2)]
+    c = (rng.standard_normal((T, m)) + 1j * rng.standard_normal((T, m))).astype(np.complex64)
+    o = esn.TransformOptions(tolerance=1e-4, dtype="float32")
+    batched, _ = esn.exec_type1(coords, c, nm, o)
+    c64 = [x.astype(np.float64) for x in coords]
+    for t in sorted({0, T // 2, T - 1}):
+        single, _ = esn.exec_type1(coords, c[t], nm, o)
+        assert np.linalg.norm(single - batched[t]) <= 2e-5 * np.linalg.norm(single), t
+        ref = oracle.exec_type1(c64, c[t].astype(np.complex128), nm, tol=1e-4)
+        assert np.linalg.norm(batched[t] - ref) <= 10 * 1e-4 * np.linalg.norm(ref), t
