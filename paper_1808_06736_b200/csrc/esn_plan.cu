@@ -122,6 +122,12 @@ struct esn_plan_s {
     bool borrowed = false;    // pk[] and grid belong to another plan (pipeline helper)
     bool keep_flags = false;  // setpts keeps accumulating error flags (chunked runs)
     int64_t ibase = 0;        // original index of this plan's point 0 (chunked runs)
+    // type-2 plans sort on a side stream (st2), so the next execute's
+    // amplify + FFT (independent of the points) overlap the sort; consumers
+    // of the sorted points join e_sorted on st first (join_sort)
+    cudaStream_t st2 = nullptr;
+    cudaEvent_t e_in = nullptr, e_sorted = nullptr;
+    bool sort_pending = false;
     float last_ms[4] = {0, 0, 0, 0};  // sort, spread, fft, correct
 };
 
@@ -399,8 +405,14 @@ void esn_default_opts(esn_opts *o) {
 
 int esn_plan_destroy(esn_plan p) {
     if (!p) return ESN_SUCCESS;
+    if (p->st2) cudaStreamSynchronize(p->st2);
     if (p->st) cudaStreamSynchronize(p->st);
     else cudaDeviceSynchronize();
+    if (p->st2) {
+        cudaEventDestroy(p->e_in);
+        cudaEventDestroy(p->e_sorted);
+        cudaStreamDestroy(p->st2);
+    }
     if (!p->borrowed) {
         for (int d = 0; d < 3; ++d) dfree(p->pk[d]);
         dfree(p->grid);
@@ -461,7 +473,31 @@ int esn_plan_create(int type, int dim, const int64_t *nmodes, int isign, int ntr
         esn_plan_destroy(p);
         return rc;
     }
+    static const bool overlap = [] {
+        const char *e = getenv("ESN_SORT_OVERLAP");
+        return !(e && std::string(e) == "0");
+    }();
+    if (type == 2 && overlap) {
+        int prio = 0;
+        cudaStreamGetPriority(p->st, &prio);
+        if (cudaStreamCreateWithPriority(&p->st2, cudaStreamNonBlocking, prio) != cudaSuccess ||
+            cudaEventCreateWithFlags(&p->e_in, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&p->e_sorted, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            esn_plan_destroy(p);
+            return fail(ESN_INTERNAL_ERROR, "side stream creation failed");
+        }
+    }
     *out = p;
+    return ESN_SUCCESS;
+}
+
+// make the plan stream wait for an in-flight side-stream sort
+static int join_sort(esn_plan p) {
+    if (p->sort_pending) {
+        ESN_CUDA_TRY(cudaStreamWaitEvent(p->st, p->e_sorted, 0));
+        p->sort_pending = false;
+    }
     return ESN_SUCCESS;
 }
 
@@ -544,9 +580,20 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
         p->subcap = subneed;
     }
     p->M = M;
-    if (p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[0], p->st));
-    ESN_CUDA_TRY(cudaMemsetAsync(p->key_count, 0, sizeof(int) * p->nkeys, p->st));
-    if (!p->keep_flags) ESN_CUDA_TRY(cudaMemsetAsync(p->flags, 0xff, sizeof(unsigned long long) * 8, p->st));
+    // side stream: ordered after everything queued on the plan stream so far
+    // (the previous execute may still read the records this sort rewrites)
+    cudaStream_t ss = p->st;
+    if (p->st2) {
+        ESN_CUDA_TRY(cudaEventRecord(p->e_in, p->st));
+        ESN_CUDA_TRY(cudaStreamWaitEvent(p->st2, p->e_in, 0));
+        ss = p->st2;
+    }
+    if (p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[0], ss));
+    ESN_CUDA_TRY(cudaMemsetAsync(p->key_count, 0, sizeof(int) * p->nkeys, ss));
+    // point flags [0..5] only when overlapped: flag 6 (data) belongs to the
+    // concurrent execute on the plan stream
+    if (!p->keep_flags)
+        ESN_CUDA_TRY(cudaMemsetAsync(p->flags, 0xff, sizeof(unsigned long long) * (p->st2 ? 6 : 8), ss));
     SetptsArgs a{};
     a.ibase = p->ibase;
     a.g = p->geom;
@@ -575,8 +622,12 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
     a.rec = p->rec;
     a.flags = p->flags;
     a.check_bounds = p->opts.check_bounds;
-    if ((rc = launch_setpts(a, p->nbk, p->maxsub, p->subprob, p->nsub, p->subofs, p->st))) return rc;
-    if (p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[1], p->st));
+    if ((rc = launch_setpts(a, p->nbk, p->maxsub, p->subprob, p->nsub, p->subofs, ss))) return rc;
+    if (p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[1], ss));
+    if (p->st2) {
+        ESN_CUDA_TRY(cudaEventRecord(p->e_sorted, p->st2));
+        p->sort_pending = true;
+    }
     p->points_set = true;
     return ESN_SUCCESS;
 }
@@ -623,6 +674,7 @@ bool esn::batched_owner(int dtype, int dim, int w, int ntransf, int method, cons
 }
 
 static int do_spread(esn_plan p, const void *c, void *grid, bool zero = true) {
+    if (int jr = join_sort(p)) return jr;
     // the bin-structured spreaders need their own bin geometry and the
     // geometric sort; a type-2 plan (interpolation bins, possibly a
     // target-chunked order) spreads its adjoint with the order-agnostic
@@ -661,6 +713,7 @@ static int do_spread(esn_plan p, const void *c, void *grid, bool zero = true) {
 }
 
 static int do_interp(esn_plan p, const void *grid, void *c) {
+    if (int jr = join_sort(p)) return jr;
     ESN_CUDA_TRY(cudaMemsetAsync(p->work, 0, sizeof(int), p->st));
     if (p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[6], p->st));
     int rc = p->dtype == ESN_F64
@@ -741,6 +794,7 @@ int esn_plan_execute(esn_plan p, void *c, void *f) {
 
 int esn_plan_check(esn_plan p, int64_t *info) {
     if (!p) return fail(ESN_SIZE_ERROR, "null plan");
+    if (int jr = join_sort(p)) return jr;
     ESN_CUDA_TRY(cudaStreamSynchronize(p->st));
     unsigned long long h[8];
     ESN_CUDA_TRY(cudaMemcpy(h, p->flags, sizeof(h), cudaMemcpyDeviceToHost));
@@ -780,6 +834,7 @@ int esn_plan_check(esn_plan p, int64_t *info) {
 
 int esn_plan_stage_times(esn_plan p, double *sort_s, double *spread_s, double *fft_s, double *correct_s) {
     if (!p || !p->have_events) return fail(ESN_SIZE_ERROR, "plan was created without opts.timing");
+    if (int jr = join_sort(p)) return jr;
     ESN_CUDA_TRY(cudaStreamSynchronize(p->st));
     float ms[4] = {0, 0, 0, 0};
     if (p->points_set) cudaEventElapsedTime(&ms[0], p->ev[0], p->ev[1]);
@@ -804,6 +859,7 @@ int esn_plan_stage_times(esn_plan p, double *sort_s, double *spread_s, double *f
 
 int esn_plan_hot_kernel_seconds(esn_plan p, double *seconds) {
     if (!p || !p->have_events) return fail(ESN_SIZE_ERROR, "plan was created without opts.timing");
+    if (int jr = join_sort(p)) return jr;
     ESN_CUDA_TRY(cudaStreamSynchronize(p->st));
     float ms = 0.f;
     ESN_CUDA_TRY(cudaEventElapsedTime(&ms, p->ev[6], p->ev[7]));
@@ -832,6 +888,7 @@ int esn_plan_bins(esn_plan p, int *nbins, int *bin_size, int *bins_per_dim) {
 int esn_plan_sort_view(esn_plan p, void *perm, void *keys, void *bin_start) {
     if (!p || !p->points_set) return fail(ESN_SIZE_ERROR, "plan has no points");
     if (p->nchunk > 1) return fail(ESN_SIZE_ERROR, "sort view needs a spreader plan (this plan's order is target-chunked)");
+    if (int jr = join_sort(p)) return jr;
     int rc = launch_sort_view(p->dtype, p->rec, p->bin_start, p->nbins, p->M, (int *)perm, (int *)keys, p->st);
     if (rc) return rc;
     if (bin_start)
