@@ -126,16 +126,16 @@ __device__ __forceinline__ void load_coords(const SetptsArgs &a, int64_t base, d
     }
 }
 
-// Pass 1: key histogram with ranks (atomic with return: the old count is the
-// point's rank inside its key) plus the finite / bounds flags.  Stores the
-// rank (one coalesced 4-byte write) so the scatter pass needs no atomics.
+// Pass 1: key histogram (fire-and-forget REDs: no return trip, no per-point
+// state written) plus the finite / bounds flags.  The ranks come from the
+// scatter pass's fill cursors.
 template <typename XT>
 __global__ void __launch_bounds__(256, 4) k_setpts_count(SetptsArgs a) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * kILP;
     for (int64_t base = (int64_t)blockIdx.x * blockDim.x * kILP + threadIdx.x; base < a.M; base += stride) {
         double x[kILP][3];
         load_coords<XT>(a, base, x);
-        int key[kILP], rank[kILP];
+        int key[kILP];
 #pragma unroll
         for (int u = 0; u < kILP; ++u) {
             const int64_t i = base + (int64_t)u * blockDim.x;
@@ -143,17 +143,14 @@ __global__ void __launch_bounds__(256, 4) k_setpts_count(SetptsArgs a) {
             key[u] = i < a.M ? point_key(a, i, x[u], g, true) : -1;
         }
 #pragma unroll
-        for (int u = 0; u < kILP; ++u) rank[u] = key[u] >= 0 ? atomicAdd(&a.key_count[key[u]], 1) : 0;
-#pragma unroll
-        for (int u = 0; u < kILP; ++u) {
-            const int64_t i = base + (int64_t)u * blockDim.x;
-            if (i < a.M) a.rank[i] = rank[u];
-        }
+        for (int u = 0; u < kILP; ++u)
+            if (key[u] >= 0) atomicAdd(&a.key_count[key[u]], 1);
     }
 }
 
-// Pass 2: the key again (recomputed with the grid coordinates), pos =
-// start[key] + rank (start from the L2-resident scan), then the point's full
+// Pass 2: the key again (recomputed with the grid coordinates), pos = an
+// atomic fill cursor of the key (key_count holds the key starts after the
+// scan; L2-resident), then the point's full
 // record {g, j} at pos with one 256-bit store (a whole L2 sector).  Batched
 // fp32 plans keep pos in key[] for the strength permutation.  kSILP points
 // per thread, all loads issued before the dependent gather.
@@ -161,12 +158,7 @@ template <typename XT>
 __global__ void __launch_bounds__(256) k_setpts_scatter(SetptsArgs a) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * kSILP;
     for (int64_t base = (int64_t)blockIdx.x * blockDim.x * kSILP + threadIdx.x; base < a.M; base += stride) {
-        int pos[kSILP], rank[kSILP];
-#pragma unroll
-        for (int u = 0; u < kSILP; ++u) {
-            const int64_t i = base + (int64_t)u * blockDim.x;
-            rank[u] = i < a.M ? __ldg(a.rank + i) : 0;
-        }
+        int pos[kSILP];
         double x[kSILP][3];
         load_coords<XT, kSILP>(a, base, x);
         double g[kSILP][3];
@@ -178,7 +170,7 @@ __global__ void __launch_bounds__(256) k_setpts_scatter(SetptsArgs a) {
         }
 #pragma unroll
         for (int u = 0; u < kSILP; ++u)
-            if (pos[u] >= 0) pos[u] = __ldg(a.cursor + pos[u]) + rank[u];  // start of the key + rank
+            if (pos[u] >= 0) pos[u] = atomicAdd(a.key_count + pos[u], 1);  // fill cursor of the key
 #pragma unroll
         for (int u = 0; u < kSILP; ++u) {
             if (pos[u] < 0) continue;
@@ -252,8 +244,10 @@ __global__ void __launch_bounds__(1024) k_scan_top(int *block_sums, int nblocks)
     if (threadIdx.x == 0) block_sums[nblocks] = carry;
 }
 
-// writes cursor[k] = exclusive prefix, and bin_start at every bin head
-__global__ void __launch_bounds__(1024) k_scan_down(const int *cnt, int n, const int *block_sums, int *cursor,
+// writes cursor[k] = exclusive prefix (kept: the spreaders read key starts)
+// and the same into cnt[k] (the scatter's fill cursors), and bin_start at
+// every bin head
+__global__ void __launch_bounds__(1024) k_scan_down(int *cnt, int n, const int *block_sums, int *cursor,
                                                    int *bin_start, int spb, int nbins) {
     __shared__ int wsum[32];
     constexpr int U = kScanTile / 1024;
@@ -271,6 +265,7 @@ __global__ void __launch_bounds__(1024) k_scan_down(const int *cnt, int n, const
         const int k = base + u;
         if (k < n) {
             cursor[k] = e;
+            cnt[k] = e;
             if (k % spb == 0) bin_start[k / spb] = e;
         }
         e += v[u];
