@@ -1645,10 +1645,13 @@ __global__ void __launch_bounds__(256, interp_minb<DIM, W>())
             }
             T are = 0, aim = 0;
             const C *base = patch + (o3 * P2 + o2) * P1 + o1;
+            // 2D: rows unrolled (static r2 index; a select chain per row cost
+            // 2 (w - 1) instructions); 3D keeps rolled loops (registers)
+            constexpr int U2 = DIM == 2 ? W : 1;
 #pragma unroll 1
             for (int m3 = 0; m3 < (DIM > 2 ? W : 1); ++m3) {
                 T p3re = 0, p3im = 0;
-#pragma unroll 1
+#pragma unroll U2
                 for (int m2 = 0; m2 < (DIM > 1 ? W : 1); ++m2) {
                     T pre = 0, pim = 0;
 #pragma unroll
