@@ -1088,7 +1088,14 @@ static int pipelined(HostSlot *slot, int type, int dim, int64_t M, const double 
         tev_init = true;
     }
     if (trace) cudaEventRecord(tev[0][0], st);
-    const int K = (int)std::min<int64_t>(KMAX, (M + (1 << 19) - 1) >> 19);
+    // type 1: every chunk's spread pays a full halo flush of every bin it
+    // touches, so few large chunks win (3D 1e7 points: K = 12 11.6 ms, K = 4
+    // 10.4 ms, K = 3 10.2 ms; c5 flat at 13.7 ms; c3 fp32 best at K = 4)
+    static const int KMAX1 = [] {
+        const char *e = getenv("ESN_PIPE_CHUNKS");
+        return std::max(1, std::min(e ? atoi(e) : 4, HostSlot::KC));
+    }();
+    const int K = (int)std::min<int64_t>(type == 1 ? KMAX1 : KMAX, (M + (1 << 19) - 1) >> 19);
     // chunk boundaries: short first chunks (compute and the download start
     // early) and geometrically shrinking last ones (short tail after the
     // final upload); equal chunks in between
