@@ -1221,19 +1221,19 @@ __global__ void __launch_bounds__(128) k_spread_b2own(SpreadArgs<T> a, const T *
 }
 
 // Batched strengths into sorted order, 32 transforms per point:
-// cperm[g][pos(j)][l] = c[32 g + l][j] with pos(j) = start[key[j]] + rank[j].
+// cperm[g][pos(j)][l] = c[32 g + l][j] with pos(j) the sorted position setpts
+// left in key[j].
 // A 32 x 32 tile transpose through shared memory: coalesced reads along j,
 // one contiguous 32-transform record per point on the write side.  Also the
 // finiteness check of the strengths.
 template <typename T>
-__global__ void __launch_bounds__(1024) k_permute_strengths(SpreadArgs<T> a, const int *key, const int *rank,
+__global__ void __launch_bounds__(1024) k_permute_strengths(SpreadArgs<T> a, const int *key,
                                                             const int *kstart, T *cperm) {
     // U tiles of 32 points per iteration: U loads in flight per thread and
     // one barrier pair per U tiles
     using C = typename Cx<T>::type;
     constexpr int U = 4;
     __shared__ C tile[U][32][33];
-    (void)rank;
     (void)kstart;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int ngroups = (a.ntransf + 31) / 32;

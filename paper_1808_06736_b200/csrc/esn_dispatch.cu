@@ -5,10 +5,10 @@
 namespace esn {
 
 template <typename T, int D>
-static int launch_spread_d(const SpreadArgs<T> &a, int method, const int *key, const int *rank, const int *kstart,
+static int launch_spread_d(const SpreadArgs<T> &a, int method, const int *key, const int *kstart,
                            T *cperm, cudaStream_t st) {
-    return a.g.w <= kWidthSplit ? launch_spread_dp<T, D, 0>(a, method, key, rank, kstart, cperm, st)
-                                : launch_spread_dp<T, D, 1>(a, method, key, rank, kstart, cperm, st);
+    return a.g.w <= kWidthSplit ? launch_spread_dp<T, D, 0>(a, method, key, kstart, cperm, st)
+                                : launch_spread_dp<T, D, 1>(a, method, key, kstart, cperm, st);
 }
 
 template <typename T, int D>
@@ -18,16 +18,16 @@ static int launch_interp_d(const SpreadArgs<T> &a, T *cout, const T *grid, cudaS
 }
 
 template <typename T>
-int launch_spread(const SpreadArgs<T> &a, int method, int nbins, const int *key, const int *rank, const int *kstart,
+int launch_spread(const SpreadArgs<T> &a, int method, int nbins, const int *key, const int *kstart,
                   T *cperm, cudaStream_t st) {
     (void)nbins;
     switch (a.g.dim) {
         case 1:
-            return launch_spread_d<T, 1>(a, method, key, rank, kstart, cperm, st);
+            return launch_spread_d<T, 1>(a, method, key, kstart, cperm, st);
         case 2:
-            return launch_spread_d<T, 2>(a, method, key, rank, kstart, cperm, st);
+            return launch_spread_d<T, 2>(a, method, key, kstart, cperm, st);
         case 3:
-            return launch_spread_d<T, 3>(a, method, key, rank, kstart, cperm, st);
+            return launch_spread_d<T, 3>(a, method, key, kstart, cperm, st);
     }
     return fail(ESN_SIZE_ERROR, "dimension must be 1, 2, or 3");
 }
@@ -45,9 +45,9 @@ int launch_interp(const SpreadArgs<T> &a, T *cout, const T *grid, cudaStream_t s
     return fail(ESN_SIZE_ERROR, "dimension must be 1, 2, or 3");
 }
 
-template int launch_spread<double>(const SpreadArgs<double> &, int, int, const int *, const int *, const int *,
-                                   double *, cudaStream_t);
-template int launch_spread<float>(const SpreadArgs<float> &, int, int, const int *, const int *, const int *, float *,
+template int launch_spread<double>(const SpreadArgs<double> &, int, int, const int *, const int *, double *,
+                                   cudaStream_t);
+template int launch_spread<float>(const SpreadArgs<float> &, int, int, const int *, const int *, float *,
                                   cudaStream_t);
 template int launch_interp<double>(const SpreadArgs<double> &, double *, const double *, cudaStream_t);
 template int launch_interp<float>(const SpreadArgs<float> &, float *, const float *, cudaStream_t);

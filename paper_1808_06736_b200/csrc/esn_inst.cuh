@@ -96,7 +96,7 @@ struct SpreadRowsOp {
 
 template <typename T, int D, int W>
 struct SpreadBatchOp {
-    static int run(const SpreadArgs<T> &a, const int *key, const int *rank, const int *kstart, T *cperm,
+    static int run(const SpreadArgs<T> &a, const int *key, const int *kstart, T *cperm,
                    cudaStream_t st) {
         if (a.M == 0) return ESN_SUCCESS;
         if constexpr (D == 2 && sizeof(T) == 4 && W <= 10) {
@@ -104,7 +104,7 @@ struct SpreadBatchOp {
             const int ngroups = (a.ntransf + 31) / 32;
             int64_t pb = ((a.M + 31) / 32) * ngroups;
             if (pb > (int64_t)device_sm_count() * 16) pb = (int64_t)device_sm_count() * 16;
-            k_permute_strengths<T><<<(int)pb, 1024, 0, st>>>(a, key, rank, kstart, cperm);
+            k_permute_strengths<T><<<(int)pb, 1024, 0, st>>>(a, key, kstart, cperm);
             ESN_CUDA_TRY(cudaGetLastError());
             // per-point rows table lives behind the permuted strengths
             PtRows2<W> *tab = reinterpret_cast<PtRows2<W> *>(
@@ -201,11 +201,11 @@ struct InterpOp {
 };
 
 template <>
-int launch_spread_dp<ESN_T, ESN_D, ESN_PART>(const SpreadArgs<ESN_T> &a, int method, const int *key, const int *rank,
+int launch_spread_dp<ESN_T, ESN_D, ESN_PART>(const SpreadArgs<ESN_T> &a, int method, const int *key,
                                              const int *kstart, ESN_T *cperm, cudaStream_t st) {
     if (method == ESN_METHOD_GLOBAL || ESN_D == 1) return dispatch_w<ESN_T, ESN_D, SpreadGlobalOp>(a.g.w, a, st);
     if (batched_spread(sizeof(ESN_T) == 8 ? ESN_F64 : ESN_F32, ESN_D, a.g.w, a.ntransf, method))
-        return dispatch_w<ESN_T, ESN_D, SpreadBatchOp>(a.g.w, a, key, rank, kstart, cperm, st);
+        return dispatch_w<ESN_T, ESN_D, SpreadBatchOp>(a.g.w, a, key, kstart, cperm, st);
     return dispatch_w<ESN_T, ESN_D, SpreadRowsOp>(a.g.w, a, st);
 }
 

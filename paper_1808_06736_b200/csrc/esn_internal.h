@@ -75,7 +75,6 @@ struct SetptsArgs {
     int *cursor;            // nkeys: exclusive scan of key_count (key start)
     int *key;               // M: sorted position of each point (written when store_pos)
     int store_pos;          // keep positions in key[] (batched strength permutation)
-    int *rank;              // M: rank of the point inside its key
     int *bin_start;         // nbins + 1
     int *block_sums;        // scan scratch
     Rec *rec;               // M sorted records
@@ -140,7 +139,7 @@ int launch_sort_view(int dtype, const void *rec, const int *bin_start, int nbins
 // method has no fixed geometry (global atomics).
 int spreader_bins(int method, int dtype, int dim, int w, int ntransf, int *bs);
 template <typename T>
-int launch_spread(const SpreadArgs<T> &a, int method, int nbins, const int *key, const int *rank,
+int launch_spread(const SpreadArgs<T> &a, int method, int nbins, const int *key,
                   const int *kstart, T *cperm, cudaStream_t st);
 // does the batched 2D path (needs a permuted-strength scratch) apply?
 bool batched_spread(int dtype, int dim, int w, int ntransf, int method);
@@ -154,7 +153,7 @@ int launch_interp(const SpreadArgs<T> &a, T *cout, const T *grid, cudaStream_t s
 // part 1 = widths 9..16 (kWidthSplit)
 constexpr int kWidthSplit = 8;
 template <typename T, int D, int P>
-int launch_spread_dp(const SpreadArgs<T> &a, int method, const int *key, const int *rank, const int *kstart,
+int launch_spread_dp(const SpreadArgs<T> &a, int method, const int *key, const int *kstart,
                      T *cperm, cudaStream_t st);
 template <typename T, int D, int P>
 int launch_interp_dp(const SpreadArgs<T> &a, T *cout, const T *grid, cudaStream_t st);

@@ -98,7 +98,7 @@ struct esn_plan_s {
     // device state
     void *pk[3] = {nullptr, nullptr, nullptr};
     Rec *rec = nullptr;  // sorted point records
-    int *pkey = nullptr, *prank = nullptr;  // per-point key / rank (setpts scratch)
+    int *pkey = nullptr;  // per-point sorted position (batched plans: strength permutation)
     void *cperm = nullptr;                  // batched strengths in sorted order
     int64_t cperm_bytes = 0;
     int *cursor = nullptr, *key_count = nullptr, *block_sums = nullptr;
@@ -419,7 +419,6 @@ int esn_plan_destroy(esn_plan p) {
     }
     dfree(p->rec);
     dfree(p->pkey);
-    dfree(p->prank);
     dfree(p->cperm);
     dfree(p->cursor);
     dfree(p->key_count);
@@ -535,15 +534,14 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
     for (int d = 0; d < p->dim; ++d)
         if (M > 0 && !xs[d]) return fail(ESN_SIZE_ERROR, "coordinate array %d missing", d + 1);
     int rc;
+    const bool store_pos = esn::batched_spread(p->dtype, p->dim, p->kp.w, p->ntransf, p->method);
     if (M > p->Mcap) {
         dfree(p->rec);
         dfree(p->pkey);
-        dfree(p->prank);
         p->rec = nullptr;
-        p->pkey = p->prank = nullptr;
+        p->pkey = nullptr;
         if ((rc = dmalloc(p, &p->rec, sizeof(Rec) * M))) return rc;
-        if ((rc = dmalloc(p, &p->pkey, sizeof(int) * M))) return rc;
-        if ((rc = dmalloc(p, &p->prank, sizeof(int) * M))) return rc;
+        if (store_pos && (rc = dmalloc(p, &p->pkey, sizeof(int) * M))) return rc;
         p->Mcap = M;
     }
     if (p->type == 2) {
@@ -620,8 +618,7 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
     a.bin_start = p->bin_start;
     a.cursor = p->cursor;
     a.key = p->pkey;
-    a.store_pos = esn::batched_spread(p->dtype, p->dim, p->kp.w, p->ntransf, p->method) ? 1 : 0;
-    a.rank = p->prank;
+    a.store_pos = store_pos ? 1 : 0;
     a.rec = p->rec;
     a.flags = p->flags;
     a.check_bounds = p->opts.check_bounds;
@@ -705,11 +702,11 @@ static int do_spread(esn_plan p, const void *c, void *grid, bool zero = true) {
     if (p->dtype == ESN_F64) {
         SpreadArgs<double> a = make_spread_args<double>(p, c, grid);
         a.accumulate = zero ? 0 : 1;
-        rc = launch_spread<double>(a, method, p->nbins, p->pkey, p->prank, p->cursor, (double *)p->cperm, p->st);
+        rc = launch_spread<double>(a, method, p->nbins, p->pkey, p->cursor, (double *)p->cperm, p->st);
     } else {
         SpreadArgs<float> a = make_spread_args<float>(p, c, grid);
         a.accumulate = zero ? 0 : 1;
-        rc = launch_spread<float>(a, method, p->nbins, p->pkey, p->prank, p->cursor, (float *)p->cperm, p->st);
+        rc = launch_spread<float>(a, method, p->nbins, p->pkey, p->cursor, (float *)p->cperm, p->st);
     }
     if (!rc && p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[7], p->st));
     return rc;
