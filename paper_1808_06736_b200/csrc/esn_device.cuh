@@ -431,6 +431,7 @@ struct Rows3Cfg {
     static constexpr size_t LIST_B = (size_t)NW * CH * sizeof(unsigned);
     static constexpr size_t SMEM = 2 * STAGE_B + RING_B + CRING_B + LIST_B;
     static_assert(2 * STAGE_B / 16 <= 0xffff && (RECS * sizeof(T)) % 16 == 0, "list entries address 16-byte units");
+    static_assert(BX <= 32 && RY - W + 1 <= 16 && RZ - W + 1 <= 16, "list entries pack ox (5), oy (4), oz (4) bits");
     static constexpr size_t TILE_B = (size_t)RY * RZ * X * 2 * sizeof(T);
     // flush passes over z slabs so one slab fits the two stages (the record
     // ring may still have copies in flight)
@@ -453,8 +454,8 @@ __device__ __forceinline__ Rows3Pre<T> rows3_load(const unsigned char *stage, un
     Rows3Pre<T> p;
     p.off = e & 0xffffu;
     const T *rec = reinterpret_cast<const T *>(stage + 16u * p.off);
-    const int2 oyz = *reinterpret_cast<const int2 *>(rec);
-    const int dy = ry - oyz.x, dz = rz - oyz.y;
+    // (y, z) offsets ride in the list entry: no dependent shared load
+    const int dy = ry - (int)((e >> 21) & 15u), dz = rz - (int)((e >> 25) & 15u);
     const bool cov = (unsigned)dy < (unsigned)W && (unsigned)dz < (unsigned)W;
     p.f = rec[Cfg::O_R2 + (cov ? dy : W)];  // r2[W] == 0
     p.cz = *reinterpret_cast<const C *>(rec + Cfg::O_CZ + 2 * (cov ? dz : 0));
@@ -494,7 +495,7 @@ __device__ __forceinline__ void rows3_apply(typename Cx<T>::type *acc, const uns
 }
 
 // one run of equal x offset OX from the warp list (entry = record offset in
-// 16-byte units | ox << 16); the next point's operands load before this one's FMAs
+// 16-byte units | ox << 16 | oy << 21 | oz << 25); the next point's operands load before this one's FMAs
 template <typename T, int W, int OX>
 __device__ __forceinline__ int rows3_run(typename Cx<T>::type *acc, const unsigned char *stage,
                                          const unsigned *list, int i, int nq, int ry, int rz) {
@@ -503,7 +504,7 @@ __device__ __forceinline__ int rows3_run(typename Cx<T>::type *acc, const unsign
         rows3_apply<T, W, OX>(acc, stage, rows3_load<T, W>(stage, e, ry, rz));
         if (++i >= nq) break;
         e = list[i];
-        if ((e >> 16) != (unsigned)OX) break;
+        if (((e >> 16) & 31u) != (unsigned)OX) break;
     }
     return i;
 }
@@ -615,16 +616,19 @@ __global__ void __launch_bounds__(Rows3Cfg<T, W>::NT, Rows3Cfg<T, W>::MINB) k_sp
             for (int b = 0; b < nch; b += 32) {
                 const int q = b + lane;
                 bool cov = false;
-                int ox = 0;
+                int ox = 0, oy = 0, oz = 0;
                 if (q < nch) {
                     const int4 o = *reinterpret_cast<const int4 *>(stg + q * RECS);
                     cov = o.x <= by0 + 7 && o.x + W - 1 >= by0 && o.y <= bz0 + 3 && o.y + W - 1 >= bz0;
                     ox = o.z;
+                    oy = o.x;
+                    oz = o.y;
                 }
                 const unsigned bal = __ballot_sync(0xffffffffu, cov);
                 if (cov)
                     mylist[n + __popc(bal & ((1u << lane) - 1u))] =
-                        (unsigned)(((st & 1) * Cfg::STAGE_B + q * RECS * sizeof(T)) / 16) | ((unsigned)ox << 16);
+                        (unsigned)(((st & 1) * Cfg::STAGE_B + q * RECS * sizeof(T)) / 16) | ((unsigned)ox << 16) |
+                        ((unsigned)oy << 21) | ((unsigned)oz << 25);
                 n += __popc(bal);
             }
             __syncwarp();
@@ -682,7 +686,7 @@ __global__ void __launch_bounds__(Rows3Cfg<T, W>::NT, Rows3Cfg<T, W>::MINB) k_sp
                 const unsigned char *stg = smem_raw;
                 int i = 0;
                 while (i < nq) {
-                    const int ox = mylist[i] >> 16;
+                    const int ox = (mylist[i] >> 16) & 31;
                     switch (ox) {
 #define ESN_R3_CASE(OX)                                                                  \
     case OX:                                                                             \
