@@ -1879,14 +1879,31 @@ __global__ void k_deconv_rows(int ntransf, int n1, int n2, int n3, int64_t N1, i
         const T f2 = p2 ? p2[k2i] : (T)1, f3 = p3 ? p3[k3i] : (T)1;
         const C *src = reinterpret_cast<const C *>(grid) + t * G + (k3 * n2 + k2) * n1;
         C *dst = reinterpret_cast<C *>(f) + row * N1;
-        for (int k1i = s0 + threadIdx.x; k1i < s1; k1i += blockDim.x) {
-            int k1 = k1i - nn1 / 2;
-            if (k1 < 0) k1 += n1;
-            T fac = p1[k1i];  // (p1 p2) p3
-            if (p2) fac *= f2;
-            if (p3) fac *= f3;
-            const C v = src[k1];
-            dst[k1i] = C{v.x * fac, v.y * fac};
+        // four elements per thread per pass, all loads issued first
+        constexpr int U = 4;
+        for (int b = s0 + threadIdx.x; b < s1; b += U * blockDim.x) {
+            C v[U];
+            T fac[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int k1i = b + u * blockDim.x;
+                if (k1i < s1) {
+                    int k1 = k1i - nn1 / 2;
+                    if (k1 < 0) k1 += n1;
+                    v[u] = src[k1];
+                    fac[u] = p1[k1i];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int k1i = b + u * blockDim.x;
+                if (k1i < s1) {
+                    T fc = fac[u];  // (p1 p2) p3
+                    if (p2) fc *= f2;
+                    if (p3) fc *= f3;
+                    dst[k1i] = C{v[u].x * fc, v[u].y * fc};
+                }
+            }
         }
     }
 }

@@ -227,7 +227,7 @@ int launch_deconv<ESN_T>(int dim, int ntransf, const int *n, const int64_t *N, c
         const int seg = rows >= (int64_t)device_sm_count() * 8 ? (int)N[0] : 256;
         const int64_t items = rows * ((N[0] + seg - 1) / seg);
         const int blocks = (int)std::min<int64_t>(items, (int64_t)device_sm_count() * 32);
-        k_deconv_rows<ESN_T><<<blocks, 256, 0, st>>>(ntransf, n[0], n[1], n[2], N[0], N[1], N[2], grid, p1, p2,
+        k_deconv_rows<ESN_T><<<blocks, 128, 0, st>>>(ntransf, n[0], n[1], n[2], N[0], N[1], N[2], grid, p1, p2,
                                                      p3, f, seg);
     } else {
         k_deconv<ESN_T><<<grid_for(total, 256), 256, 0, st>>>(ntransf, n[0], n[1], n[2], N[0], N[1], N[2], grid, p1,
