@@ -1,0 +1,91 @@
+"""The kernel variants kept behind environment switches must agree with the
+defaults on the same inputs (each switch is read once per process, so every
+variant runs in a child process):
+
+* ESN_SORT_OVERLAP=0 -- type-2 setpts on the plan stream instead of the side
+  stream: the same kernels on the same data, so BIT-identical outputs;
+* ESN_SPREAD3=rows   -- the first 3D row spreader (k_spread_rows) instead of
+  k_spread_rows3: a different summation order, fp64 rounding only;
+* ESN_B2=tile        -- the RED-flush batched 2D spreader (k_spread_batch2d)
+  instead of the owner-computes k_spread_b2own: fp32 rounding only.
+"""
+import os
+import subprocess
+import sys
+import textwrap
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = textwrap.dedent(r"""
+    import sys, numpy as np
+    sys.path.insert(0, sys.argv[1])
+    import paper_1808_06736_b200 as nu
+    rng = np.random.default_rng(5)
+    out = sys.argv[2]
+    # type 2, 2D and 3D (side-stream sort)
+    for dim, nm in ((2, (120, 90)), (3, (20, 18, 16))):
+        xs = [rng.uniform(-np.pi, np.pi, 200_000) for _ in range(dim)]
+        f = rng.standard_normal(nm[::-1]) + 1j * rng.standard_normal(nm[::-1])
+        c, _ = nu.exec_type2(tuple(xs), f, nu.TransformOptions(tolerance=1e-6, isign=-1))
+        np.save(out + f"/t2_{dim}.npy", c)
+    # type 1, 3D fp64 (ε = 1e-6 and 1e-9) and fp32
+    for tag, tol, dt in (("f64", 1e-6, "float64"), ("f64w", 1e-9, "float64"), ("f32", 1e-4, "float32")):
+        xs = [rng.uniform(-np.pi, np.pi, 150_000) for _ in range(3)]
+        c = rng.standard_normal(150_000) + 1j * rng.standard_normal(150_000)
+        if dt == "float32":
+            xs = [x.astype(np.float32) for x in xs]
+            c = c.astype(np.complex64)
+        f, _ = nu.exec_type1(tuple(xs), c, (40, 36, 32), nu.TransformOptions(tolerance=tol, dtype=dt))
+        np.save(out + f"/t1_3d_{tag}.npy", f)
+    # type 1, 2D batched fp32
+    xs = [rng.uniform(-np.pi, np.pi, 100_000).astype(np.float32) for _ in range(2)]
+    c = (rng.standard_normal((40, 100_000)) + 1j * rng.standard_normal((40, 100_000))).astype(np.complex64)
+    f, _ = nu.exec_type1(tuple(xs), c, (96, 80), nu.TransformOptions(tolerance=1e-4, dtype="float32"))
+    np.save(out + "/t1_2d_batch.npy", f)
+    print("ok")
+""")
+
+
+def _run(tmp, env_extra):
+    env = dict(os.environ)
+    for k in ("ESN_SORT_OVERLAP", "ESN_SPREAD3", "ESN_B2"):
+        env.pop(k, None)
+    env.update(env_extra)
+    os.makedirs(tmp, exist_ok=True)
+    r = subprocess.run([sys.executable, "-c", SCRIPT, ROOT, tmp], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return {f[:-4]: np.load(os.path.join(tmp, f)) for f in os.listdir(tmp) if f.endswith(".npy")}
+
+
+@pytest.fixture(scope="module")
+def default_out(tmp_path_factory):
+    return _run(str(tmp_path_factory.mktemp("default")), {})
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+@pytest.mark.gpu
+def test_sort_overlap_bit_identical(tmp_path, default_out):
+    alt = _run(str(tmp_path), {"ESN_SORT_OVERLAP": "0"})
+    for k in ("t2_2", "t2_3"):
+        assert np.array_equal(alt[k], default_out[k]), k
+
+
+@pytest.mark.gpu
+def test_rows3_matches_first_row_spreader(tmp_path, default_out):
+    alt = _run(str(tmp_path), {"ESN_SPREAD3": "rows"})
+    assert _rel(default_out["t1_3d_f64"], alt["t1_3d_f64"]) <= 1e-13
+    assert _rel(default_out["t1_3d_f64w"], alt["t1_3d_f64w"]) <= 1e-13
+    assert _rel(default_out["t1_3d_f32"], alt["t1_3d_f32"]) <= 1e-6
+
+
+@pytest.mark.gpu
+def test_b2own_matches_tile_batched_spreader(tmp_path, default_out):
+    alt = _run(str(tmp_path), {"ESN_B2": "tile"})
+    assert _rel(default_out["t1_2d_batch"], alt["t1_2d_batch"]) <= 1e-6
