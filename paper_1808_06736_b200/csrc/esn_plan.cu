@@ -128,11 +128,28 @@ struct esn_plan_s {
     cudaStream_t st2 = nullptr;
     cudaEvent_t e_in = nullptr, e_sorted = nullptr;
     bool sort_pending = false;
+    // CUDA-graph replay of launch-bound calls (small M): the stream work of
+    // setpts / execute is captured once per signature on a private stream
+    // and replayed as one graph launch (slot 0: setpts, 1: execute)
+    cudaStream_t gs = nullptr;
+    cudaEvent_t g_in = nullptr, g_out = nullptr;
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    uint64_t gsig[2] = {0, 0};
+    int64_t gen = 0;        // bumped whenever a device buffer is (re)allocated
+    bool capturing = false;
+    bool graphs_off = false;  // a capture failed once: run directly from then on
     float last_ms[4] = {0, 0, 0, 0};  // sort, spread, fft, correct
 };
 
+// timing events: inside a graph capture they become EXTERNAL event-record
+// nodes (plain captured records cannot be timed)
+static cudaError_t rec_ev(esn_plan p, cudaEvent_t e, cudaStream_t st) {
+    return p->capturing ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal) : cudaEventRecord(e, st);
+}
+
 template <typename P>
 static int dmalloc(esn_plan p, P **ptr, size_t bytes) {
+    ++p->gen;  // captured graphs hold device pointers
     if (bytes == 0) bytes = 16;
     cudaError_t e = cudaMalloc((void **)ptr, bytes);
     if (e != cudaSuccess) {
@@ -413,6 +430,14 @@ int esn_plan_destroy(esn_plan p) {
         cudaEventDestroy(p->e_sorted);
         cudaStreamDestroy(p->st2);
     }
+    if (p->gs) {
+        cudaStreamSynchronize(p->gs);
+        for (auto &g : p->gexec)
+            if (g) cudaGraphExecDestroy(g);
+        cudaEventDestroy(p->g_in);
+        cudaEventDestroy(p->g_out);
+        cudaStreamDestroy(p->gs);
+    }
     if (!p->borrowed) {
         for (int d = 0; d < 3; ++d) dfree(p->pk[d]);
         dfree(p->grid);
@@ -500,6 +525,84 @@ static int join_sort(esn_plan p) {
     return ESN_SUCCESS;
 }
 
+// Launch-bound problems (M <= ESN_GRAPH_MAX_M, default 2^19) replay each
+// setpts / execute as one CUDA graph: ~15-20 launches and memsets per call
+// otherwise cost more host time than the GPU work (c1: 62 us of kernels in
+// a 112 us step).  The body enqueues on p->st; for a capture p->st is
+// swapped for the private stream gs (captures cannot run on the legacy
+// stream), and replays are ordered against the caller's stream by events.
+static uint64_t mix(uint64_t h, uint64_t v) {
+    h ^= v + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+    return h;
+}
+
+static bool graph_eligible(esn_plan p) {
+    static const int64_t lim = [] {
+        const char *e = getenv("ESN_GRAPH_MAX_M");
+        return e ? atoll(e) : (int64_t)1 << 19;
+    }();
+    return !p->graphs_off && !p->borrowed && p->M >= 0 && p->M <= lim;
+}
+
+extern "C++" {
+template <class F>
+static int run_graphed(esn_plan p, int slot, uint64_t sig, F &&body) {
+    if (!p->gs) {
+        if (cudaStreamCreateWithFlags(&p->gs, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&p->g_in, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&p->g_out, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            p->graphs_off = true;
+            return body();
+        }
+    }
+    sig = mix(mix(sig, (uint64_t)p->gen), (uint64_t)(uintptr_t)p->st);
+    if (!p->gexec[slot] || p->gsig[slot] != sig) {
+        if (p->gexec[slot]) {
+            cudaGraphExecDestroy(p->gexec[slot]);
+            p->gexec[slot] = nullptr;
+        }
+        const int64_t gen0 = p->gen;
+        cudaStream_t user = p->st;
+        // the capture stream starts after the caller's queued work, like a replay
+        ESN_CUDA_TRY(cudaEventRecord(p->g_in, user));
+        ESN_CUDA_TRY(cudaStreamWaitEvent(p->gs, p->g_in, 0));
+        if (cudaStreamBeginCapture(p->gs, cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+            cudaGetLastError();
+            p->graphs_off = true;
+            return body();
+        }
+        p->st = p->gs;
+        p->capturing = true;
+        const int rc = body();
+        cudaGraph_t graph = nullptr;
+        const cudaError_t e = cudaStreamEndCapture(p->gs, &graph);
+        p->st = user;
+        p->capturing = false;
+        cudaGraphExec_t exec = nullptr;
+        const bool ok = rc == ESN_SUCCESS && e == cudaSuccess && graph &&
+                        cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+        if (graph) cudaGraphDestroy(graph);
+        if (!ok) {
+            cudaGetLastError();
+            if (rc != ESN_SUCCESS) return rc;  // (argument / resource errors surface as before)
+            p->graphs_off = true;              // capture unsupported here: run directly
+            return body();
+        }
+        p->gexec[slot] = exec;
+        // allocations inside the body (first call) invalidate other slots' pointers
+        p->gsig[slot] = p->gen == gen0 ? sig : 0;
+        if (p->gen != gen0) p->gsig[1 - slot] = 0;
+    }
+    ESN_CUDA_TRY(cudaEventRecord(p->g_in, p->st));
+    ESN_CUDA_TRY(cudaStreamWaitEvent(p->gs, p->g_in, 0));
+    ESN_CUDA_TRY(cudaGraphLaunch(p->gexec[slot], p->gs));
+    ESN_CUDA_TRY(cudaEventRecord(p->g_out, p->gs));
+    ESN_CUDA_TRY(cudaStreamWaitEvent(p->st, p->g_out, 0));
+    return ESN_SUCCESS;
+}
+}  // extern "C++"
+
 int esn_spreader_create(int dim, const int64_t *nfine, int ntransf, const esn_opts *opts, esn_plan *out) {
     if (!out) return fail(ESN_SIZE_ERROR, "null plan pointer");
     *out = nullptr;
@@ -581,20 +684,24 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
         p->subcap = subneed;
     }
     p->M = M;
+    const bool graphed = graph_eligible(p);
+    const bool side = p->st2 && !graphed;  // (small, graphed sorts stay on the plan stream)
+    auto enqueue = [&]() -> int {
+    int rc;
     // side stream: ordered after everything queued on the plan stream so far
     // (the previous execute may still read the records this sort rewrites)
     cudaStream_t ss = p->st;
-    if (p->st2) {
+    if (side) {
         ESN_CUDA_TRY(cudaEventRecord(p->e_in, p->st));
         ESN_CUDA_TRY(cudaStreamWaitEvent(p->st2, p->e_in, 0));
         ss = p->st2;
     }
-    if (p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[0], ss));
+    if (p->have_events) ESN_CUDA_TRY(rec_ev(p, p->ev[0], ss));
     ESN_CUDA_TRY(cudaMemsetAsync(p->key_count, 0, sizeof(int) * p->nkeys, ss));
     // point flags [0..5] only when overlapped: flag 6 (data) belongs to the
     // concurrent execute on the plan stream
     if (!p->keep_flags)
-        ESN_CUDA_TRY(cudaMemsetAsync(p->flags, 0xff, sizeof(unsigned long long) * (p->st2 ? 6 : 8), ss));
+        ESN_CUDA_TRY(cudaMemsetAsync(p->flags, 0xff, sizeof(unsigned long long) * (side ? 6 : 8), ss));
     SetptsArgs a{};
     a.ibase = p->ibase;
     a.g = p->geom;
@@ -623,11 +730,22 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
     a.flags = p->flags;
     a.check_bounds = p->opts.check_bounds;
     if ((rc = launch_setpts(a, p->nbk, p->maxsub, p->subprob, p->nsub, p->subofs, ss))) return rc;
-    if (p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[1], ss));
-    if (p->st2) {
-        ESN_CUDA_TRY(cudaEventRecord(p->e_sorted, p->st2));
-        p->sort_pending = true;
+    if (p->have_events) ESN_CUDA_TRY(rec_ev(p, p->ev[1], ss));
+    if (side) ESN_CUDA_TRY(cudaEventRecord(p->e_sorted, p->st2));
+    return ESN_SUCCESS;
+    };
+    if (graphed) {
+        uint64_t sig = 0x5e7;
+        for (uint64_t v : {(uint64_t)M, (uint64_t)coord_dtype, (uint64_t)(uintptr_t)x, (uint64_t)(uintptr_t)y,
+                           (uint64_t)(uintptr_t)z, (uint64_t)p->keep_flags, (uint64_t)p->ibase,
+                           (uint64_t)p->have_events, (uint64_t)p->nkeys, (uint64_t)p->nbk, (uint64_t)p->chunk_len})
+            sig = mix(sig, v);
+        rc = run_graphed(p, 0, sig, enqueue);
+    } else {
+        rc = enqueue();
     }
+    if (rc) return rc;
+    p->sort_pending = side;
     p->points_set = true;
     return ESN_SUCCESS;
 }
@@ -673,15 +791,10 @@ bool esn::batched_owner(int dtype, int dim, int w, int ntransf, int method, cons
            bs[0] == Batch2Cfg<float, 2>::BX && bs[1] == Batch2Cfg<float, 2>::BY;
 }
 
-static int do_spread(esn_plan p, const void *c, void *grid, bool zero = true) {
-    if (int jr = join_sort(p)) return jr;
-    // the bin-structured spreaders need their own bin geometry and the
-    // geometric sort; a type-2 plan (interpolation bins, possibly a
-    // target-chunked order) spreads its adjoint with the order-agnostic
-    // spreader
-    const int method = p->type == 2 ? ESN_METHOD_GLOBAL : p->method;
+// scratch of the batched spreader: permuted strengths + per-point rows
+// table (<= 96 B per point)
+static int ensure_spread_scratch(esn_plan p, int method) {
     if (esn::batched_spread(p->dtype, p->dim, p->kp.w, p->ntransf, method)) {
-        // permuted strengths + per-point rows table (<= 96 B per point)
         const int64_t need = (int64_t)((p->ntransf + 31) / 32) * 32 * p->M * (int64_t)real_size(p->dtype) * 2 +
                              96 * p->M + 256;
         if (need > p->cperm_bytes) {
@@ -692,12 +805,23 @@ static int do_spread(esn_plan p, const void *c, void *grid, bool zero = true) {
             p->cperm_bytes = need;
         }
     }
+    return ESN_SUCCESS;
+}
+
+static int do_spread(esn_plan p, const void *c, void *grid, bool zero = true) {
+    if (int jr = join_sort(p)) return jr;
+    // the bin-structured spreaders need their own bin geometry and the
+    // geometric sort; a type-2 plan (interpolation bins, possibly a
+    // target-chunked order) spreads its adjoint with the order-agnostic
+    // spreader
+    const int method = p->type == 2 ? ESN_METHOD_GLOBAL : p->method;
+    if (int rc = ensure_spread_scratch(p, method)) return rc;
     // the owner-computes batched spreader writes every fine cell itself
     const bool owner = esn::batched_owner(p->dtype, p->dim, p->kp.w, p->ntransf, method, p->sbl, p->geom.bs);
     if (zero && !owner)
         ESN_CUDA_TRY(cudaMemsetAsync(grid, 0, real_size(p->dtype) * 2 * (size_t)p->G * p->ntransf, p->st));
     ESN_CUDA_TRY(cudaMemsetAsync(p->work, 0, sizeof(int), p->st));
-    if (p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[6], p->st));
+    if (p->have_events) ESN_CUDA_TRY(rec_ev(p, p->ev[6], p->st));
     int rc;
     if (p->dtype == ESN_F64) {
         SpreadArgs<double> a = make_spread_args<double>(p, c, grid);
@@ -708,20 +832,20 @@ static int do_spread(esn_plan p, const void *c, void *grid, bool zero = true) {
         a.accumulate = zero ? 0 : 1;
         rc = launch_spread<float>(a, method, p->nbins, p->pkey, p->cursor, (float *)p->cperm, p->st);
     }
-    if (!rc && p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[7], p->st));
+    if (!rc && p->have_events) ESN_CUDA_TRY(rec_ev(p, p->ev[7], p->st));
     return rc;
 }
 
 static int do_interp(esn_plan p, const void *grid, void *c) {
     if (int jr = join_sort(p)) return jr;
     ESN_CUDA_TRY(cudaMemsetAsync(p->work, 0, sizeof(int), p->st));
-    if (p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[6], p->st));
+    if (p->have_events) ESN_CUDA_TRY(rec_ev(p, p->ev[6], p->st));
     int rc = p->dtype == ESN_F64
                  ? launch_interp<double>(make_spread_args<double>(p, nullptr, nullptr), (double *)c,
                                          (const double *)grid, p->st)
                  : launch_interp<float>(make_spread_args<float>(p, nullptr, nullptr), (float *)c,
                                         (const float *)grid, p->st);
-    if (!rc && p->have_events) ESN_CUDA_TRY(cudaEventRecord(p->ev[7], p->st));
+    if (!rc && p->have_events) ESN_CUDA_TRY(rec_ev(p, p->ev[7], p->st));
     return rc;
 }
 
@@ -752,18 +876,33 @@ int esn_plan_interp(esn_plan p, const void *grid, void *c) {
     return do_interp(p, grid, c);
 }
 
+static int execute_body(esn_plan p, void *c, void *f);
+
 int esn_plan_execute(esn_plan p, void *c, void *f) {
     if (!p || !p->points_set) return fail(ESN_SIZE_ERROR, "plan has no points (call esn_plan_setpts first)");
     if (p->type != 1 && p->type != 2) return fail(ESN_SIZE_ERROR, "spreader plans have no execute");
+    if (!graph_eligible(p)) return execute_body(p, c, f);
+    // everything that allocates happens before a capture
+    int rc;
+    if ((rc = ensure_spread_scratch(p, p->type == 2 ? ESN_METHOD_GLOBAL : p->method))) return rc;
+    cufftHandle h;
+    if ((rc = get_fft_plan(p->dim, p->n, p->dtype, p->ntransf, &h))) return rc;
+    uint64_t sig = 0xe8ec;
+    for (uint64_t v : {(uint64_t)(uintptr_t)c, (uint64_t)(uintptr_t)f, (uint64_t)p->M, (uint64_t)p->have_events})
+        sig = mix(sig, v);
+    return run_graphed(p, 1, sig, [&]() { return execute_body(p, c, f); });
+}
+
+static int execute_body(esn_plan p, void *c, void *f) {
     int rc;
     const bool ev = p->have_events;
     ESN_CUDA_TRY(cudaMemsetAsync(p->flags + 6, 0xff, sizeof(unsigned long long), p->st));
     if (p->type == 1) {
-        if (ev) ESN_CUDA_TRY(cudaEventRecord(p->ev[2], p->st));
+        if (ev) ESN_CUDA_TRY(rec_ev(p, p->ev[2], p->st));
         if ((rc = do_spread(p, c, p->grid))) return rc;
-        if (ev) ESN_CUDA_TRY(cudaEventRecord(p->ev[3], p->st));
+        if (ev) ESN_CUDA_TRY(rec_ev(p, p->ev[3], p->st));
         if ((rc = run_fft(p->dim, p->n, p->dtype, p->ntransf, p->grid, p->isign, p->st))) return rc;
-        if (ev) ESN_CUDA_TRY(cudaEventRecord(p->ev[4], p->st));
+        if (ev) ESN_CUDA_TRY(rec_ev(p, p->ev[4], p->st));
         if (p->dtype == ESN_F64)
             rc = launch_deconv<double>(p->dim, p->ntransf, p->n, p->N, (const double *)p->grid, (const double *)p->pk[0],
                                        (const double *)p->pk[1], (const double *)p->pk[2], (double *)f, p->st);
@@ -771,9 +910,9 @@ int esn_plan_execute(esn_plan p, void *c, void *f) {
             rc = launch_deconv<float>(p->dim, p->ntransf, p->n, p->N, (const float *)p->grid, (const float *)p->pk[0],
                                       (const float *)p->pk[1], (const float *)p->pk[2], (float *)f, p->st);
         if (rc) return rc;
-        if (ev) ESN_CUDA_TRY(cudaEventRecord(p->ev[5], p->st));
+        if (ev) ESN_CUDA_TRY(rec_ev(p, p->ev[5], p->st));
     } else {
-        if (ev) ESN_CUDA_TRY(cudaEventRecord(p->ev[2], p->st));
+        if (ev) ESN_CUDA_TRY(rec_ev(p, p->ev[2], p->st));
         if (p->dtype == ESN_F64)
             rc = launch_amplify<double>(p->dim, p->ntransf, p->n, p->N, (const double *)f, (const double *)p->pk[0],
                                         (const double *)p->pk[1], (const double *)p->pk[2], (double *)p->grid,
@@ -783,11 +922,11 @@ int esn_plan_execute(esn_plan p, void *c, void *f) {
                                        (const float *)p->pk[1], (const float *)p->pk[2], (float *)p->grid,
                                        p->flags + 6, p->st);
         if (rc) return rc;
-        if (ev) ESN_CUDA_TRY(cudaEventRecord(p->ev[3], p->st));
+        if (ev) ESN_CUDA_TRY(rec_ev(p, p->ev[3], p->st));
         if ((rc = run_fft(p->dim, p->n, p->dtype, p->ntransf, p->grid, p->isign, p->st))) return rc;
-        if (ev) ESN_CUDA_TRY(cudaEventRecord(p->ev[4], p->st));
+        if (ev) ESN_CUDA_TRY(rec_ev(p, p->ev[4], p->st));
         if ((rc = do_interp(p, p->grid, c))) return rc;
-        if (ev) ESN_CUDA_TRY(cudaEventRecord(p->ev[5], p->st));
+        if (ev) ESN_CUDA_TRY(rec_ev(p, p->ev[5], p->st));
     }
     return ESN_SUCCESS;
 }

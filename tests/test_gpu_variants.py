@@ -89,3 +89,40 @@ def test_rows3_matches_first_row_spreader(tmp_path, default_out):
 def test_b2own_matches_tile_batched_spreader(tmp_path, default_out):
     alt = _run(str(tmp_path), {"ESN_B2": "tile"})
     assert _rel(default_out["t1_2d_batch"], alt["t1_2d_batch"]) <= 1e-6
+
+
+@pytest.mark.gpu
+def test_graph_replay_follows_new_data(esn):
+    """Small plans replay setpts / execute as captured CUDA graphs (keyed by
+    buffer pointers, M and the plan's allocation generation): new VALUES in
+    the same buffers, a different output buffer, a different M and a
+    different coordinate buffer must all give what a fresh plan gives."""
+    import torch
+    from paper_1808_06736_b200.plan import Plan
+    dev = torch.device("cuda", torch.cuda.current_device())
+    rng = np.random.default_rng(9)
+    nm = (40, 36)
+    p2 = Plan(2, 2, nmodes=nm, isign=-1, tol=1e-6, device=dev)
+    p1 = Plan(1, 2, nmodes=nm, isign=1, tol=1e-6, device=dev)
+    x = torch.empty(5000, dtype=torch.float64, device=dev)
+    y = torch.empty(5000, dtype=torch.float64, device=dev)
+    for rep, m in enumerate((5000, 5000, 3000, 5000)):
+        if rep == 3:  # a different coordinate buffer
+            x = torch.empty(5000, dtype=torch.float64, device=dev)
+        x[:m] = torch.from_numpy(rng.uniform(-np.pi, np.pi, m))
+        y[:m] = torch.from_numpy(rng.uniform(-np.pi, np.pi, m))
+        f = torch.from_numpy(rng.standard_normal(nm[::-1]) + 1j * rng.standard_normal(nm[::-1])).to(dev)
+        c = torch.from_numpy(rng.standard_normal(m) + 1j * rng.standard_normal(m)).to(dev)
+        out2 = torch.empty(m, dtype=torch.complex128, device=dev)
+        p2.setpts([x[:m], y[:m]])
+        p2.execute(out2, f)
+        out1 = torch.empty(nm[::-1], dtype=torch.complex128, device=dev)
+        p1.setpts([x[:m], y[:m]])
+        p1.execute(c, out1)
+        xs = (x[:m].cpu().numpy(), y[:m].cpu().numpy())
+        ref2, _ = esn.exec_type2(xs, f.cpu().numpy(), esn.TransformOptions(tolerance=1e-6, isign=-1))
+        ref1, _ = esn.exec_type1(xs, c.cpu().numpy(), nm, esn.TransformOptions(tolerance=1e-6))
+        assert np.array_equal(out2.cpu().numpy(), ref2), rep
+        assert _rel(out1.cpu().numpy(), ref1) <= 1e-13, rep
+    p1.close()
+    p2.close()
