@@ -126,3 +126,34 @@ def test_graph_replay_follows_new_data(esn):
         assert _rel(out1.cpu().numpy(), ref1) <= 1e-13, rep
     p1.close()
     p2.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype,tols", [
+    ("float64", (1e-2, 1e-3, 1e-5, 1e-7, 1e-8, 1e-10, 1e-11, 1e-12, 1e-13, 1e-14)),
+    ("float32", (1e-2, 1e-3, 1e-4, 1e-5, 1e-6)),
+])
+def test_every_width_3d_type1_and_batched_2d(esn, oracle, dtype, tols):
+    """Each kernel width instantiates its own spreader (w = 2 .. 15 here):
+    3D type 1 (k_spread_rows3) and float32 batched 2D type 1
+    (k_spread_b2own) against the oracle at small M."""
+    rng = np.random.default_rng(21)
+    m = 6000
+    for tol in tols:
+        xs = [rng.uniform(-np.pi, np.pi, m) for _ in range(3)]
+        c = rng.standard_normal(m) + 1j * rng.standard_normal(m)
+        o = esn.TransformOptions(tolerance=tol, dtype=dtype)
+        if dtype == "float32":
+            xs = [x.astype(np.float32) for x in xs]
+            c = c.astype(np.complex64)
+        got, _ = esn.exec_type1(xs, c, (20, 18, 16), o)
+        ref = oracle.exec_type1([x.astype(np.float64) for x in xs], c.astype(np.complex128), (20, 18, 16), tol=tol)
+        bound = 1e-3 * tol if dtype == "float64" else max(10 * tol, 1e-5)
+        assert _rel(got, ref) <= max(bound, 1e-13), (tol, _rel(got, ref))
+        if dtype == "float32":
+            cb = (rng.standard_normal((3, m)) + 1j * rng.standard_normal((3, m))).astype(np.complex64)
+            gotb, _ = esn.exec_type1(xs[:2], cb, (40, 34), o)
+            for t in range(3):
+                refb = oracle.exec_type1([x.astype(np.float64) for x in xs[:2]], cb[t].astype(np.complex128),
+                                         (40, 34), tol=tol)
+                assert _rel(gotb[t], refb) <= max(10 * tol, 1e-5), (tol, t, _rel(gotb[t], refb))
