@@ -166,6 +166,14 @@ int launch_amplify(int dim, int ntransf, const int *n, const int64_t *N, const T
 
 int device_sm_count();
 
+// 2D type 1 with a power-of-two n2: pruned y-FFT fused with the
+// deconvolution (after a 1D cuFFT x pass); twid = e^{isign 2 pi i k / n2},
+// k < n2 / 2, in the plan dtype
+bool colfft_eligible(int dtype, int dim, int n2);
+template <typename T>
+int launch_colfft_deconv(int ntransf, int n1, int n2, int N1, int N2, const T *grid, const T *twid, const T *p1,
+                         const T *p2, T *f, cudaStream_t st);
+
 }  // namespace esn
 
 #define ESN_CUDA_TRY(expr)                                                              \

@@ -99,6 +99,7 @@ struct esn_plan_s {
     void *pk[3] = {nullptr, nullptr, nullptr};
     Rec *rec = nullptr;  // sorted point records
     int *pkey = nullptr;  // per-point sorted position (batched plans: strength permutation)
+    void *twid = nullptr;                   // column-FFT twiddles (2D type 1, power-of-two n2)
     void *cperm = nullptr;                  // batched strengths in sorted order
     int64_t cperm_bytes = 0;
     int *cursor = nullptr, *key_count = nullptr, *block_sums = nullptr;
@@ -444,6 +445,7 @@ int esn_plan_destroy(esn_plan p) {
     }
     dfree(p->rec);
     dfree(p->pkey);
+    dfree(p->twid);
     dfree(p->cperm);
     dfree(p->cursor);
     dfree(p->key_count);
@@ -496,6 +498,31 @@ int esn_plan_create(int type, int dim, const int64_t *nmodes, int isign, int ntr
     if ((rc = plan_common_init(p, &o)) || (rc = upload_corrections(p))) {
         esn_plan_destroy(p);
         return rc;
+    }
+    if (type == 1 && esn::colfft_eligible(p->dtype, dim, p->n[1])) {
+        const int n2 = p->n[1];
+        std::vector<double> tw((size_t)n2);  // n2 / 2 complex
+        for (int k = 0; k < n2 / 2; ++k) {
+            const double a = 2.0 * M_PI * k / n2;
+            tw[2 * k] = std::cos(a);
+            tw[2 * k + 1] = isign * std::sin(a);
+        }
+        const size_t rs = real_size(p->dtype);
+        if ((rc = dmalloc(p, &p->twid, rs * n2))) {
+            esn_plan_destroy(p);
+            return rc;
+        }
+        cudaError_t e;
+        if (p->dtype == ESN_F64) {
+            e = cudaMemcpy(p->twid, tw.data(), sizeof(double) * n2, cudaMemcpyHostToDevice);
+        } else {
+            std::vector<float> twf(tw.begin(), tw.end());
+            e = cudaMemcpy(p->twid, twf.data(), sizeof(float) * n2, cudaMemcpyHostToDevice);
+        }
+        if (e != cudaSuccess) {
+            esn_plan_destroy(p);
+            return fail(ESN_INTERNAL_ERROR, "twiddle upload failed");
+        }
     }
     static const bool overlap = [] {
         const char *e = getenv("ESN_SORT_OVERLAP");
@@ -857,18 +884,46 @@ int esn_plan_spread(esn_plan p, const void *c, void *grid) {
     return do_spread(p, c, grid);
 }
 
+// type-1 tail: fine-grid FFT + deconvolution into the modes.  2D plans with
+// a power-of-two n2 run cuFFT along x only and the fused pruned y-FFT +
+// deconvolution kernel; others cuFFT (full) + k_deconv*.  `ev_mid` (may be
+// null) is recorded between the two halves.
+static int fft_deconv_type1(esn_plan p, void *grid, void *f, cudaStream_t st, cudaEvent_t ev_mid) {
+    int rc;
+    if (p->twid) {
+        const int n1 = p->n[0];
+        if ((rc = run_fft(1, &n1, p->dtype, p->ntransf * p->n[1], grid, p->isign, st))) return rc;
+        if (ev_mid) ESN_CUDA_TRY(rec_ev(p, ev_mid, st));
+        if (p->dtype == ESN_F64)
+            return launch_colfft_deconv<double>(p->ntransf, p->n[0], p->n[1], (int)p->N[0], (int)p->N[1],
+                                                (const double *)grid, (const double *)p->twid,
+                                                (const double *)p->pk[0], (const double *)p->pk[1], (double *)f, st);
+        return launch_colfft_deconv<float>(p->ntransf, p->n[0], p->n[1], (int)p->N[0], (int)p->N[1],
+                                           (const float *)grid, (const float *)p->twid, (const float *)p->pk[0],
+                                           (const float *)p->pk[1], (float *)f, st);
+    }
+    if ((rc = run_fft(p->dim, p->n, p->dtype, p->ntransf, grid, p->isign, st))) return rc;
+    if (ev_mid) ESN_CUDA_TRY(rec_ev(p, ev_mid, st));
+    if (p->dtype == ESN_F64)
+        return launch_deconv<double>(p->dim, p->ntransf, p->n, p->N, (const double *)grid, (const double *)p->pk[0],
+                                     (const double *)p->pk[1], (const double *)p->pk[2], (double *)f, st);
+    return launch_deconv<float>(p->dim, p->ntransf, p->n, p->N, (const float *)grid, (const float *)p->pk[0],
+                                (const float *)p->pk[1], (const float *)p->pk[2], (float *)f, st);
+}
+
+static int ensure_fft_plan(esn_plan p) {
+    cufftHandle h;
+    if (p->twid && p->type == 1) {
+        const int n1 = p->n[0];
+        return get_fft_plan(1, &n1, p->dtype, p->ntransf * p->n[1], &h);
+    }
+    return get_fft_plan(p->dim, p->n, p->dtype, p->ntransf, &h);
+}
+
 int esn_plan_finish_type1(esn_plan p, void *grid, void *f) {
     if (!p || p->type != 1) return fail(ESN_SIZE_ERROR, "finish_type1 needs a type-1 plan");
     if (!grid || !f) return fail(ESN_SIZE_ERROR, "null grid or mode array");
-    int rc;
-    if ((rc = run_fft(p->dim, p->n, p->dtype, p->ntransf, grid, p->isign, p->st))) return rc;
-    if (p->dtype == ESN_F64)
-        rc = launch_deconv<double>(p->dim, p->ntransf, p->n, p->N, (const double *)grid, (const double *)p->pk[0],
-                                   (const double *)p->pk[1], (const double *)p->pk[2], (double *)f, p->st);
-    else
-        rc = launch_deconv<float>(p->dim, p->ntransf, p->n, p->N, (const float *)grid, (const float *)p->pk[0],
-                                  (const float *)p->pk[1], (const float *)p->pk[2], (float *)f, p->st);
-    return rc;
+    return fft_deconv_type1(p, grid, f, p->st, nullptr);
 }
 
 int esn_plan_interp(esn_plan p, const void *grid, void *c) {
@@ -885,8 +940,7 @@ int esn_plan_execute(esn_plan p, void *c, void *f) {
     // everything that allocates happens before a capture
     int rc;
     if ((rc = ensure_spread_scratch(p, p->type == 2 ? ESN_METHOD_GLOBAL : p->method))) return rc;
-    cufftHandle h;
-    if ((rc = get_fft_plan(p->dim, p->n, p->dtype, p->ntransf, &h))) return rc;
+    if ((rc = ensure_fft_plan(p))) return rc;
     uint64_t sig = 0xe8ec;
     for (uint64_t v : {(uint64_t)(uintptr_t)c, (uint64_t)(uintptr_t)f, (uint64_t)p->M, (uint64_t)p->have_events})
         sig = mix(sig, v);
@@ -901,15 +955,7 @@ static int execute_body(esn_plan p, void *c, void *f) {
         if (ev) ESN_CUDA_TRY(rec_ev(p, p->ev[2], p->st));
         if ((rc = do_spread(p, c, p->grid))) return rc;
         if (ev) ESN_CUDA_TRY(rec_ev(p, p->ev[3], p->st));
-        if ((rc = run_fft(p->dim, p->n, p->dtype, p->ntransf, p->grid, p->isign, p->st))) return rc;
-        if (ev) ESN_CUDA_TRY(rec_ev(p, p->ev[4], p->st));
-        if (p->dtype == ESN_F64)
-            rc = launch_deconv<double>(p->dim, p->ntransf, p->n, p->N, (const double *)p->grid, (const double *)p->pk[0],
-                                       (const double *)p->pk[1], (const double *)p->pk[2], (double *)f, p->st);
-        else
-            rc = launch_deconv<float>(p->dim, p->ntransf, p->n, p->N, (const float *)p->grid, (const float *)p->pk[0],
-                                      (const float *)p->pk[1], (const float *)p->pk[2], (float *)f, p->st);
-        if (rc) return rc;
+        if ((rc = fft_deconv_type1(p, p->grid, f, p->st, ev ? p->ev[4] : nullptr))) return rc;
         if (ev) ESN_CUDA_TRY(rec_ev(p, p->ev[5], p->st));
     } else {
         if (ev) ESN_CUDA_TRY(rec_ev(p, p->ev[2], p->st));
@@ -1333,14 +1379,7 @@ static int pipelined(HostSlot *slot, int type, int dim, int64_t M, const double 
     ESN_CUDA_TRY(cudaEventRecord(slot->ev_down, down));
     ESN_CUDA_TRY(cudaStreamWaitEvent(st, slot->ev_down, 0));
     if (type == 1) {
-        if ((rc = run_fft(p->dim, p->n, p->dtype, p->ntransf, p->grid, p->isign, st))) return rc;
-        if (p->dtype == ESN_F64)
-            rc = launch_deconv<double>(p->dim, p->ntransf, p->n, p->N, (const double *)p->grid, (const double *)p->pk[0],
-                                       (const double *)p->pk[1], (const double *)p->pk[2], (double *)slot->df, st);
-        else
-            rc = launch_deconv<float>(p->dim, p->ntransf, p->n, p->N, (const float *)p->grid, (const float *)p->pk[0],
-                                      (const float *)p->pk[1], (const float *)p->pk[2], (float *)slot->df, st);
-        if (rc) return rc;
+        if ((rc = fft_deconv_type1(p, p->grid, slot->df, st, nullptr))) return rc;
         if (cudaMemcpyAsync(f, slot->df, cb * nm * T, cudaMemcpyDeviceToHost, st) != cudaSuccess)
             return fail(ESN_INTERNAL_ERROR, "D2H copy failed");
     }

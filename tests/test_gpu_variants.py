@@ -157,3 +157,22 @@ def test_every_width_3d_type1_and_batched_2d(esn, oracle, dtype, tols):
                 refb = oracle.exec_type1([x.astype(np.float64) for x in xs[:2]], cb[t].astype(np.complex128),
                                          (40, 34), tol=tol)
                 assert _rel(gotb[t], refb) <= max(10 * tol, 1e-5), (tol, t, _rel(gotb[t], refb))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nm,T,isign", [((37, 509), 1, 1), ((64, 512), 3, -1), ((1000, 505), 2, 1)])
+def test_fused_column_fft_deconv(esn, oracle, nm, T, isign):
+    """float32 2D type 1 with a 1024-point fine y axis (N2 in 501..512) runs
+    cuFFT along x and the fused 1024-point column FFT + deconvolution
+    (k_colfft1024_deconv): odd N1, partial column tiles, both signs, batches."""
+    rng = np.random.default_rng(31)
+    m = 30_000
+    xs = [rng.uniform(-np.pi, np.pi, m).astype(np.float32) for _ in range(2)]
+    c = (rng.standard_normal((T, m)) + 1j * rng.standard_normal((T, m))).astype(np.complex64)
+    o = esn.TransformOptions(tolerance=1e-5, isign=isign, dtype="float32")
+    got, _ = esn.exec_type1(xs, c if T > 1 else c[0], nm, o)
+    got = np.asarray(got).reshape(T, nm[1], nm[0])
+    for t in range(T):
+        ref = oracle.exec_type1([x.astype(np.float64) for x in xs], c[t].astype(np.complex128), nm, tol=1e-5,
+                                isign=isign)
+        assert _rel(got[t], ref) <= 1e-5, (t, _rel(got[t], ref))
