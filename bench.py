@@ -64,8 +64,22 @@ def hot_kernel_name(cfg):
     if cfg["dim"] == 1:
         return "k_spread_global"
     if cfg["dim"] == 2 and f32 and cfg.get("ntransf", 1) > 1:
-        return "k_spread_batch2d"
+        return "k_spread_batch2d" if os.environ.get("ESN_B2") == "tile" else "k_spread_b2own"
+    if cfg["dim"] == 3:
+        return "k_spread_rows" if os.environ.get("ESN_SPREAD3") == "rows" else "k_spread_rows3"
     return "k_spread_rows"
+
+
+# what actually bounds each config's hot kernel (ncu
+# pipe / shared-memory utilisation); roofline.frac stays the HBM fraction
+BINDING = {
+    "c1": "launch / latency (1e5 points; CUDA-graph replay)",
+    "c2": "shared-memory wavefronts (~75 % busy) + FP64 pipe (~37 %), not HBM",
+    "c3": "FP64 pipe (w^3 = 343 DFMA pairs per point), not HBM",
+    "c3f": "issue / FP32 pipe, not HBM",
+    "c4": "FP64 pipe (w^3 = 1000 DFMA pairs per point), not HBM",
+    "c5": "issue (per-point dispatch + staging), DRAM traffic = the algorithmic bytes",
+}
 
 
 def algorithmic_bytes(cfg, M, T):
@@ -466,7 +480,7 @@ def main():
         # scan + fill (7); type 2: amplify + interp; type 1: spread (batched:
         # permute + row table + spread) + deconv.  cuFFT's own kernels excluded.
         hk = hot_kernel_name(cfg)
-        n_launch = 7 + (2 if cfg["ttype"] == 2 else (3 if hk == "k_spread_batch2d" else 1) + 1)
+        n_launch = 7 + (2 if cfg["ttype"] == 2 else (3 if hk in ("k_spread_batch2d", "k_spread_b2own") else 1) + 1)
         cb = config_block(args.config, world, args.points, res["M"])
         if res["mode"] == "points":
             cb["parallelism"] = (f"points split x{world}, NCCL reduce of the partial "
@@ -481,7 +495,8 @@ def main():
                               "unit": "GB/s", "frac": frac, "traffic": traffic,
                               "kernel": f"{kern} ({hot_kernel_name(cfg)})",
                               "algorithmic_bytes": res["B"], "kernel_ms": res["hot_s"] * 1e3,
-                              "peak_source": f"{res['peak_kind']} MEASURED_PEAKS.json hbm_gbs"},
+                              "peak_source": f"{res['peak_kind']} MEASURED_PEAKS.json hbm_gbs",
+                              "binding": BINDING.get(args.config)},
                     stages_ms={k: v * 1e3 for k, v in res["stages"].items()},
                     clocks=res["clocks"], gpu_launches=n_launch * args.steps)
         if "e2e" in res:
