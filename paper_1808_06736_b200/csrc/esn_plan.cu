@@ -1271,11 +1271,12 @@ static int pipelined(HostSlot *slot, int type, int dim, int64_t M, const double 
     }
     if (trace) cudaEventRecord(tev[0][0], st);
     // type 1: every chunk's spread pays a full halo flush of every bin it
-    // touches, so few large chunks win (3D 1e7 points: K = 12 11.6 ms, K = 4
-    // 10.4 ms, K = 3 10.2 ms; c5 flat at 13.7 ms; c3 fp32 best at K = 4)
+    // touches, so few large chunks win (3D 1e7 points: K = 12 11.6 ms, K = 6
+    // 9.64, K = 5 9.60, K = 4 9.76 ms; c4: K = 5 10.1 ms, K = 4 11.1 ms;
+    // c5 flat at 13.7 ms)
     static const int KMAX1 = [] {
         const char *e = getenv("ESN_PIPE_CHUNKS");
-        return std::max(1, std::min(e ? atoi(e) : 4, HostSlot::KC));
+        return std::max(1, std::min(e ? atoi(e) : 5, HostSlot::KC));
     }();
     const int K = (int)std::min<int64_t>(type == 1 ? KMAX1 : KMAX, (M + (1 << 19) - 1) >> 19);
     // chunk boundaries: short first chunks (compute and the download start
@@ -1285,7 +1286,9 @@ static int pipelined(HostSlot *slot, int type, int dim, int64_t M, const double 
     {
         double w[HostSlot::KC], wsum = 0;
         for (int k = 0; k < K; ++k) w[k] = 1.0;
-        if (K >= 6) {
+        // (type 1 keeps equal chunks: a short last chunk was measured slower,
+        // its predecessors grow and their spreads stop hiding under the copies)
+        if (K >= 6 && type == 2) {
             w[0] = 0.25; w[1] = 0.5;
             w[K - 3] = 0.5; w[K - 2] = 0.25; w[K - 1] = 0.125;
         }
