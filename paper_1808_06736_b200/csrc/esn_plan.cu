@@ -765,7 +765,8 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
         uint64_t sig = 0x5e7;
         for (uint64_t v : {(uint64_t)M, (uint64_t)coord_dtype, (uint64_t)(uintptr_t)x, (uint64_t)(uintptr_t)y,
                            (uint64_t)(uintptr_t)z, (uint64_t)p->keep_flags, (uint64_t)p->ibase,
-                           (uint64_t)p->have_events, (uint64_t)p->nkeys, (uint64_t)p->nbk, (uint64_t)p->chunk_len})
+                           (uint64_t)p->have_events, (uint64_t)p->nkeys, (uint64_t)p->nbk, (uint64_t)p->chunk_len,
+                           (uint64_t)p->ntransf})
             sig = mix(sig, v);
         rc = run_graphed(p, 0, sig, enqueue);
     } else {
@@ -942,7 +943,8 @@ int esn_plan_execute(esn_plan p, void *c, void *f) {
     if ((rc = ensure_spread_scratch(p, p->type == 2 ? ESN_METHOD_GLOBAL : p->method))) return rc;
     if ((rc = ensure_fft_plan(p))) return rc;
     uint64_t sig = 0xe8ec;
-    for (uint64_t v : {(uint64_t)(uintptr_t)c, (uint64_t)(uintptr_t)f, (uint64_t)p->M, (uint64_t)p->have_events})
+    for (uint64_t v : {(uint64_t)(uintptr_t)c, (uint64_t)(uintptr_t)f, (uint64_t)p->M, (uint64_t)p->have_events,
+                       (uint64_t)p->ntransf, (uint64_t)p->keep_flags})
         sig = mix(sig, v);
     return run_graphed(p, 1, sig, [&]() { return execute_body(p, c, f); });
 }
@@ -950,7 +952,8 @@ int esn_plan_execute(esn_plan p, void *c, void *f) {
 static int execute_body(esn_plan p, void *c, void *f) {
     int rc;
     const bool ev = p->have_events;
-    ESN_CUDA_TRY(cudaMemsetAsync(p->flags + 6, 0xff, sizeof(unsigned long long), p->st));
+    // (keep_flags: a caller accumulating the data flag over several executes)
+    if (!p->keep_flags) ESN_CUDA_TRY(cudaMemsetAsync(p->flags + 6, 0xff, sizeof(unsigned long long), p->st));
     if (p->type == 1) {
         if (ev) ESN_CUDA_TRY(rec_ev(p, p->ev[2], p->st));
         if ((rc = do_spread(p, c, p->grid))) return rc;
@@ -1422,6 +1425,86 @@ static int pipelined(HostSlot *slot, int type, int dim, int64_t M, const double 
     return rc;
 }
 
+// Batched type 1 with points below the chunked-pipeline threshold (c5: 64
+// transforms of 1e6 points): the strengths dominate the transfer (512 MB),
+// so the pipeline runs over TRANSFORM groups instead of point chunks --
+// coordinates up and one sort, then per group of 32 transforms: strengths up
+// (transfer stream) -> batched spread + FFT + deconvolution on the plan
+// stream -> modes down (second transfer stream), so group g's compute and
+// download overlap group g + 1's upload.
+static int transform_pipelined(HostSlot *slot, int dim, int64_t M, const double *const *xs, int T, void *c, void *f,
+                               int64_t nm, size_t cb) {
+    esn_plan p = slot->plan;
+    cudaStream_t st = p->st;
+    if (!slot->up) {
+        ESN_CUDA_TRY(cudaStreamCreateWithFlags(&slot->up, cudaStreamNonBlocking));
+        ESN_CUDA_TRY(cudaStreamCreateWithFlags(&slot->down, cudaStreamNonBlocking));
+        ESN_CUDA_TRY(cudaEventCreateWithFlags(&slot->ev_grid, cudaEventDisableTiming));
+        ESN_CUDA_TRY(cudaEventCreateWithFlags(&slot->ev_in, cudaEventDisableTiming));
+        ESN_CUDA_TRY(cudaEventCreateWithFlags(&slot->ev_down, cudaEventDisableTiming));
+        for (int k = 0; k < HostSlot::KC; ++k) {
+            ESN_CUDA_TRY(cudaEventCreateWithFlags(&slot->ev_up[k], cudaEventDisableTiming));
+            ESN_CUDA_TRY(cudaEventCreateWithFlags(&slot->ev_comp[k], cudaEventDisableTiming));
+        }
+    }
+    cudaStream_t up = slot->up, down = slot->down;
+    // groups of 32 transforms (one lane group of the batched spreader); a
+    // remainder below 2 joins the previous group (a batch keeps >= 2)
+    int bounds[HostSlot::KC + 1], ng = 0;
+    for (int t0 = 0; t0 < T && ng < HostSlot::KC - 1; t0 += 32) bounds[ng++] = t0;
+    bounds[ng] = T;
+    if (ng > 1 && bounds[ng] - bounds[ng - 1] < 2) bounds[--ng] = T;
+    if (bounds[ng] != T) bounds[ng] = T;
+    ESN_CUDA_TRY(cudaEventRecord(slot->ev_in, st));
+    ESN_CUDA_TRY(cudaStreamWaitEvent(up, slot->ev_in, 0));
+    ESN_CUDA_TRY(cudaStreamWaitEvent(down, slot->ev_in, 0));
+    for (int d = 0; d < dim; ++d)
+        if (cudaMemcpyAsync(slot->dx[d], xs[d], sizeof(double) * M, cudaMemcpyHostToDevice, up) != cudaSuccess)
+            return fail(ESN_INTERNAL_ERROR, "H2D copy failed");
+    ESN_CUDA_TRY(cudaEventRecord(slot->ev_grid, up));
+    for (int g = 0; g < ng; ++g) {
+        const size_t off = (size_t)bounds[g] * M * cb, bytes = (size_t)(bounds[g + 1] - bounds[g]) * M * cb;
+        if (cudaMemcpyAsync((char *)slot->dc + off, (const char *)c + off, bytes, cudaMemcpyHostToDevice, up) !=
+            cudaSuccess)
+            return fail(ESN_INTERNAL_ERROR, "H2D copy failed");
+        ESN_CUDA_TRY(cudaEventRecord(slot->ev_up[g], up));
+    }
+    ESN_CUDA_TRY(cudaStreamWaitEvent(st, slot->ev_grid, 0));
+    int rc = esn_plan_setpts(p, M, ESN_F64, slot->dx[0], slot->dx[1], slot->dx[2]);  // (resets every flag)
+    const int T0 = p->ntransf;
+    p->keep_flags = true;  // the data flag accumulates over the groups
+    struct Restore {       // (every exit path restores the plan)
+        esn_plan p;
+        int T0;
+        ~Restore() {
+            p->keep_flags = false;
+            p->ntransf = T0;
+        }
+    } restore{p, T0};
+    for (int g = 0; g < ng && !rc; ++g) {
+        ESN_CUDA_TRY(cudaStreamWaitEvent(st, slot->ev_up[g], 0));
+        p->ntransf = bounds[g + 1] - bounds[g];  // (the plan's buffers are sized for all T)
+        rc = esn_plan_execute(p, (char *)slot->dc + (size_t)bounds[g] * M * cb,
+                              (char *)slot->df + (size_t)bounds[g] * nm * cb);
+        if (rc) break;
+        ESN_CUDA_TRY(cudaEventRecord(slot->ev_comp[g], st));
+        ESN_CUDA_TRY(cudaStreamWaitEvent(down, slot->ev_comp[g], 0));
+        const size_t off = (size_t)bounds[g] * nm * cb, bytes = (size_t)(bounds[g + 1] - bounds[g]) * nm * cb;
+        if (cudaMemcpyAsync((char *)f + off, (const char *)slot->df + off, bytes, cudaMemcpyDeviceToHost, down) !=
+            cudaSuccess)
+            return fail(ESN_INTERNAL_ERROR, "D2H copy failed");
+    }
+    p->keep_flags = false;
+    p->ntransf = T0;
+    ESN_CUDA_TRY(cudaEventRecord(slot->ev_down, down));
+    ESN_CUDA_TRY(cudaStreamWaitEvent(st, slot->ev_down, 0));
+    if (rc) {
+        cudaStreamSynchronize(st);
+        return rc;
+    }
+    return esn_plan_check(p, nullptr);
+}
+
 int esn_nufft_host(int type, int dim, int64_t M, const double *x, const double *y, const double *z, int ntransf,
                    void *c, int isign, double tol, const int64_t *nmodes, void *f, const esn_opts *opts) {
     // argument misuse -> SIZE_ERROR before any core work (esnufftpy __init__.py:54-122)
@@ -1500,6 +1583,14 @@ int esn_nufft_host(int type, int dim, int64_t M, const double *x, const double *
     if (nopipe && nopipe[0] == '1') pipe = false;
     if (pipe) {
         rc = pipelined(slot, type, dim, M, xs, ntransf, c, f, nm, cb);
+        if (transient) free_slot(*slot);
+        return rc;
+    }
+    bool tpipe = !rc && cacheable && type == 1 && ntransf > 32 && M > 0 && is_pinned(c) && is_pinned(f);
+    for (int d = 0; d < dim && tpipe; ++d) tpipe = is_pinned(xs[d]);
+    if (nopipe && nopipe[0] == '1') tpipe = false;
+    if (tpipe) {
+        rc = transform_pipelined(slot, dim, M, xs, ntransf, c, f, nm, cb);
         if (transient) free_slot(*slot);
         return rc;
     }

@@ -111,3 +111,20 @@ def test_host_type3_status_codes(esn):
     assert _lib.lib.esn_nufft1d3(2, P(x), P(c), 1, 1e-6, 2, P(s), P(f), None) == 5  # non-finite target
     assert "target" in _lib.last_error()
     assert _lib.lib.esn_nufft1d3(2, P(x), P(c), 1, 1e-6, 0, P(s), P(f), None) == 0  # no targets
+
+
+def test_host_batched_transform_pipeline(esn):
+    """ntransf > 32 with M below the point-chunk threshold runs the
+    transform-group pipeline (groups of 32 transforms: strengths up, spread +
+    FFT + deconvolution, modes down, overlapped): same result as the device
+    API, and a non-finite strength in the FIRST group is still reported."""
+    coords, c, cfg = cases.make_inputs("c5", M=300_000, ntransf=70)
+    st, out = _call_host(1, coords, c, cfg["nm"], cfg["tol"], cfg["isign"], dtype="float32", ntransf=70)
+    assert st == 0
+    ref, _ = esn.exec_type1([x.astype(np.float32) for x in coords], c.astype(np.complex64), cfg["nm"],
+                            esn.TransformOptions(tolerance=cfg["tol"], isign=cfg["isign"], dtype="float32"))
+    assert np.linalg.norm(out - ref) <= 1e-5 * np.linalg.norm(ref)
+    bad = c.copy()
+    bad[3, 1234] = np.nan
+    st, _ = _call_host(1, coords, bad, cfg["nm"], cfg["tol"], cfg["isign"], dtype="float32", ntransf=70)
+    assert st == 5  # DATA_ERROR (errors.py:13-20)
