@@ -116,6 +116,10 @@ typedef struct {
     void *stream;              /* cudaStream_t, NULL = legacy default       */
     const esn_kernel_params *params; /* override select_params (may be NULL) */
     const double *coeffs;      /* override Horner table w x (w+4) (NULL)    */
+    int strength_dtype;        /* host calls, type 1, float64 plans: ESN_F32 =
+                                  complex64 input strengths, upcast exactly on
+                                  the device (half the H2D bytes); 0 = the
+                                  plan dtype                                  */
 } esn_opts;
 
 void esn_default_opts(esn_opts *o);

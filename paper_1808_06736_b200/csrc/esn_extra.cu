@@ -231,3 +231,24 @@ template int launch_colfft_deconv<float>(int, int, int, int, int, const float *,
                                          const float *, float *, cudaStream_t);
 
 }  // namespace esn
+
+namespace esn {
+
+// complex64 -> complex128 (exact), for float64 type-1 host calls that take
+// complex64 strengths (esn_opts.strength_dtype)
+__global__ void k_upcast_c64(const float2 *in, double2 *out, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float2 v = in[i];
+        out[i] = make_double2((double)v.x, (double)v.y);
+    }
+}
+
+int launch_upcast_c64(const void *in, void *out, int64_t n, cudaStream_t st) {
+    if (n <= 0) return ESN_SUCCESS;
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, (int64_t)device_sm_count() * 16);
+    k_upcast_c64<<<blocks, 256, 0, st>>>((const float2 *)in, (double2 *)out, n);
+    ESN_CUDA_TRY(cudaGetLastError());
+    return ESN_SUCCESS;
+}
+
+}  // namespace esn

@@ -170,6 +170,8 @@ int device_sm_count();
 // deconvolution (after a 1D cuFFT x pass); twid = e^{isign 2 pi i k / n2},
 // k < n2 / 2, in the plan dtype
 bool colfft_eligible(int dtype, int dim, int n2);
+// complex64 -> complex128 (host calls with complex64 strengths for a float64 plan)
+int launch_upcast_c64(const void *in, void *out, int64_t n, cudaStream_t st);
 template <typename T>
 int launch_colfft_deconv(int ntransf, int n1, int n2, int N1, int N2, const T *grid, const T *twid, const T *p1,
                          const T *p2, T *f, cudaStream_t st);

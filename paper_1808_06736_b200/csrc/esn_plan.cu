@@ -1232,7 +1232,7 @@ static int copy_rows(void *dst, const void *src, int64_t M_dst, int64_t M_src, i
 }
 
 static int pipelined(HostSlot *slot, int type, int dim, int64_t M, const double *const *xs, int T, void *c, void *f,
-                     int64_t nm, size_t cb) {
+                     int64_t nm, size_t cb, bool c64in) {
     const auto t_start = std::chrono::steady_clock::now();
     esn_plan p = slot->plan;
     int rc;
@@ -1338,6 +1338,11 @@ static int pipelined(HostSlot *slot, int type, int dim, int64_t M, const double 
     auto block = [&](int64_t lo) {  // (T, cnt) staging block of chunk at lo
         return (char *)slot->dc + (T > 1 ? (size_t)M * T * cb + (size_t)lo * T * cb : (size_t)lo * cb);
     };
+    // complex64 input strengths land in the half of the staging buffer that
+    // block() leaves free, and are upcast into block() on the compute stream
+    auto stage64 = [&](int64_t lo) {
+        return (char *)slot->dc + (T > 1 ? (size_t)lo * T * 8 : (size_t)M * cb + (size_t)lo * 8);
+    };
     for (int k = 0; k < K; ++k) {
         const int64_t lo = bound[k], cnt = bound[k + 1] - lo;
         if (cnt <= 0) continue;
@@ -1345,7 +1350,8 @@ static int pipelined(HostSlot *slot, int type, int dim, int64_t M, const double 
             if (cudaMemcpyAsync((double *)slot->dx[d] + lo, xs[d] + lo, sizeof(double) * cnt, cudaMemcpyHostToDevice,
                                 up) != cudaSuccess)
                 return fail(ESN_INTERNAL_ERROR, "H2D copy failed");
-        if (type == 1 && (rc = copy_rows(block(lo), c, cnt, M, 0, lo, cnt, T, cb, cudaMemcpyHostToDevice, up)))
+        if (type == 1 && (rc = c64in ? copy_rows(stage64(lo), c, cnt, M, 0, lo, cnt, T, 8, cudaMemcpyHostToDevice, up)
+                                     : copy_rows(block(lo), c, cnt, M, 0, lo, cnt, T, cb, cudaMemcpyHostToDevice, up)))
             return rc;
         ESN_CUDA_TRY(cudaEventRecord(slot->ev_up[k], up));
         if (trace) cudaEventRecord(tev[1][k], up);
@@ -1367,6 +1373,7 @@ static int pipelined(HostSlot *slot, int type, int dim, int64_t M, const double 
         if ((rc = esn_plan_setpts(q, cnt, ESN_F64, cx[0], cx[1], cx[2]))) return rc;
         ESN_CUDA_TRY(cudaStreamWaitEvent(hs, slot->ev_grid, 0));
         if (type == 1) {
+            if (c64in && (rc = launch_upcast_c64(stage64(lo), blk, cnt * T, hs))) return rc;
             if ((rc = do_spread(q, blk, p->grid, false))) return rc;
         } else {
             if ((rc = do_interp(q, p->grid, blk))) return rc;
@@ -1433,7 +1440,7 @@ static int pipelined(HostSlot *slot, int type, int dim, int64_t M, const double 
 // stream -> modes down (second transfer stream), so group g's compute and
 // download overlap group g + 1's upload.
 static int transform_pipelined(HostSlot *slot, int dim, int64_t M, const double *const *xs, int T, void *c, void *f,
-                               int64_t nm, size_t cb) {
+                               int64_t nm, size_t cb, bool c64in) {
     esn_plan p = slot->plan;
     cudaStream_t st = p->st;
     if (!slot->up) {
@@ -1462,10 +1469,12 @@ static int transform_pipelined(HostSlot *slot, int dim, int64_t M, const double 
         if (cudaMemcpyAsync(slot->dx[d], xs[d], sizeof(double) * M, cudaMemcpyHostToDevice, up) != cudaSuccess)
             return fail(ESN_INTERNAL_ERROR, "H2D copy failed");
     ESN_CUDA_TRY(cudaEventRecord(slot->ev_grid, up));
+    // (complex64 input strengths: staged in the second half of dc, upcast per group)
+    const size_t cbi = c64in ? 8 : cb;
+    char *const stage = (char *)slot->dc + (c64in ? (size_t)M * T * cb : 0);
     for (int g = 0; g < ng; ++g) {
-        const size_t off = (size_t)bounds[g] * M * cb, bytes = (size_t)(bounds[g + 1] - bounds[g]) * M * cb;
-        if (cudaMemcpyAsync((char *)slot->dc + off, (const char *)c + off, bytes, cudaMemcpyHostToDevice, up) !=
-            cudaSuccess)
+        const size_t off = (size_t)bounds[g] * M * cbi, bytes = (size_t)(bounds[g + 1] - bounds[g]) * M * cbi;
+        if (cudaMemcpyAsync(stage + off, (const char *)c + off, bytes, cudaMemcpyHostToDevice, up) != cudaSuccess)
             return fail(ESN_INTERNAL_ERROR, "H2D copy failed");
         ESN_CUDA_TRY(cudaEventRecord(slot->ev_up[g], up));
     }
@@ -1483,6 +1492,9 @@ static int transform_pipelined(HostSlot *slot, int dim, int64_t M, const double 
     } restore{p, T0};
     for (int g = 0; g < ng && !rc; ++g) {
         ESN_CUDA_TRY(cudaStreamWaitEvent(st, slot->ev_up[g], 0));
+        if (c64in && (rc = launch_upcast_c64(stage + (size_t)bounds[g] * M * 8, (char *)slot->dc + (size_t)bounds[g] * M * cb,
+                                              (int64_t)(bounds[g + 1] - bounds[g]) * M, st)))
+            break;
         p->ntransf = bounds[g + 1] - bounds[g];  // (the plan's buffers are sized for all T)
         rc = esn_plan_execute(p, (char *)slot->dc + (size_t)bounds[g] * M * cb,
                               (char *)slot->df + (size_t)bounds[g] * nm * cb);
@@ -1577,12 +1589,15 @@ int esn_nufft_host(int type, int dim, int64_t M, const double *x, const double *
         slot->Mcap = M;
     }
     if (!rc && !slot->df) rc = dmalloc(p, &slot->df, cb * nm * ntransf);
+    const bool c64in = type == 1 && dtype == ESN_F64 && o.strength_dtype == ESN_F32;
+    if (o.strength_dtype && o.strength_dtype != dtype && !c64in)
+        return fail(ESN_SIZE_ERROR, "strength_dtype: only complex64 strengths for a float64 type-1 transform");
     bool pipe = !rc && cacheable && M >= (int64_t)(2 << 20) && is_pinned(c) && is_pinned(f);
     for (int d = 0; d < dim && pipe; ++d) pipe = is_pinned(xs[d]);
     static const char *nopipe = getenv("ESN_NO_PIPELINE");
     if (nopipe && nopipe[0] == '1') pipe = false;
     if (pipe) {
-        rc = pipelined(slot, type, dim, M, xs, ntransf, c, f, nm, cb);
+        rc = pipelined(slot, type, dim, M, xs, ntransf, c, f, nm, cb, c64in);
         if (transient) free_slot(*slot);
         return rc;
     }
@@ -1590,7 +1605,7 @@ int esn_nufft_host(int type, int dim, int64_t M, const double *x, const double *
     for (int d = 0; d < dim && tpipe; ++d) tpipe = is_pinned(xs[d]);
     if (nopipe && nopipe[0] == '1') tpipe = false;
     if (tpipe) {
-        rc = transform_pipelined(slot, dim, M, xs, ntransf, c, f, nm, cb);
+        rc = transform_pipelined(slot, dim, M, xs, ntransf, c, f, nm, cb, c64in);
         if (transient) free_slot(*slot);
         return rc;
     }
@@ -1598,9 +1613,13 @@ int esn_nufft_host(int type, int dim, int64_t M, const double *x, const double *
         for (int d = 0; d < dim && M > 0; ++d)
             if (cudaMemcpyAsync(slot->dx[d], xs[d], sizeof(double) * M, cudaMemcpyHostToDevice, st) != cudaSuccess)
                 rc = fail(ESN_INTERNAL_ERROR, "H2D copy failed");
-        if (!rc && type == 1 && M > 0)
-            if (cudaMemcpyAsync(slot->dc, c, cb * M * ntransf, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        if (!rc && type == 1 && M > 0) {
+            // (complex64 strengths: staged in the second half of dc, upcast into the first)
+            char *dst = (char *)slot->dc + (c64in ? cb * M * ntransf : 0);
+            if (cudaMemcpyAsync(dst, c, (c64in ? 8 : cb) * M * ntransf, cudaMemcpyHostToDevice, st) != cudaSuccess)
                 rc = fail(ESN_INTERNAL_ERROR, "H2D copy failed");
+            if (!rc && c64in) rc = launch_upcast_c64(dst, slot->dc, M * ntransf, st);
+        }
         if (!rc && type == 2)
             if (cudaMemcpyAsync(slot->df, f, cb * nm * ntransf, cudaMemcpyHostToDevice, st) != cudaSuccess)
                 rc = fail(ESN_INTERNAL_ERROR, "H2D copy failed");

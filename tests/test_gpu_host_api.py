@@ -128,3 +128,31 @@ def test_host_batched_transform_pipeline(esn):
     bad[3, 1234] = np.nan
     st, _ = _call_host(1, coords, bad, cfg["nm"], cfg["tol"], cfg["isign"], dtype="float32", ntransf=70)
     assert st == 5  # DATA_ERROR (errors.py:13-20)
+
+
+@pytest.mark.parametrize("M,T", [(2_300_000, 1), (50_000, 1), (40_000, 40)])
+def test_host_complex64_strengths_for_float64(esn, M, T):
+    """esn_opts.strength_dtype = float32: complex64 host strengths for a
+    float64 type-1 transform (c3's inputs) are upcast exactly on the device,
+    through the point-chunk pipeline, the plain path and the transform-group
+    pipeline: the same modes as complex128 strengths of the same values."""
+    from paper_1808_06736_b200 import _lib
+    from paper_1808_06736_b200.plan import make_opts
+    rng = np.random.default_rng(41)
+    coords = [rng.uniform(-np.pi, np.pi, M) for _ in range(3)]
+    c = (rng.standard_normal((T, M)) + 1j * rng.standard_normal((T, M))).astype(np.complex64)
+    if T == 1:
+        c = c[0]
+    nm = (24, 20, 18)
+    ref_st, ref = _call_host(1, coords, c.astype(np.complex128), nm, 1e-6, 1, ntransf=T)
+    assert ref_st == 0
+    hx = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for x in coords]
+    hc = torch.from_numpy(np.ascontiguousarray(c)).pin_memory()
+    hout = torch.empty(((T,) if T > 1 else ()) + tuple(reversed(nm)), dtype=torch.complex128).pin_memory()
+    o, keep = make_opts(dtype="float64", timing=False, strength_dtype="float32")
+    st = _lib.lib.esn_nufft_host(1, 3, M, *[ctypes.c_void_p(x.data_ptr()) for x in hx], T,
+                                 ctypes.c_void_p(hc.data_ptr()), 1, 1e-6, _lib.i64_array(nm),
+                                 ctypes.c_void_p(hout.data_ptr()), ctypes.byref(o))
+    assert st == 0
+    out = hout.numpy()
+    assert np.linalg.norm(out - ref) <= 1e-13 * np.linalg.norm(ref)
