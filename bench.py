@@ -365,7 +365,10 @@ def e2e_run(args, cfg, coords, data, M, T, dev):
     from paper_1808_06736_b200 import _lib
     from paper_1808_06736_b200.plan import make_opts
     cplx = torch.complex128 if cfg["dtype"] == "float64" else torch.complex64
-    hx = [torch.from_numpy(x).pin_memory() for x in coords]
+    # float32 configs take float32 coordinates (the values are float32-exact,
+    # cases.make_inputs); the host routine reads them as such (coord_dtype)
+    f32c = cfg["dtype"] == "float32"
+    hx = [torch.from_numpy(x.astype(np.float32) if f32c else x).pin_memory() for x in coords]
     # a config whose strengths ARE complex64 (c3: "c_j complex64", computed in
     # float64) hands them over as such: upcast exactly on the device
     c64in = cfg["ttype"] == 1 and cfg["dtype"] == "float64" and cfg.get("cdtype") == "complex64"
@@ -373,15 +376,16 @@ def e2e_run(args, cfg, coords, data, M, T, dev):
     if cfg["ttype"] == 1:
         hout = torch.empty((T,) + tuple(reversed(cfg["nm"])), dtype=cplx).pin_memory()
         cptr, fptr = hd.data_ptr(), hout.data_ptr()
-        h2d = sum(x.numel() * 8 for x in hx) + hd.numel() * hd.element_size()
+        h2d = sum(x.numel() * x.element_size() for x in hx) + hd.numel() * hd.element_size()
         d2h = hout.numel() * hout.element_size()
     else:
         hout = torch.empty((T, M) if T > 1 else (M,), dtype=cplx).pin_memory()
         cptr, fptr = hout.data_ptr(), hd.data_ptr()
-        h2d = sum(x.numel() * 8 for x in hx) + hd.numel() * hd.element_size()
+        h2d = sum(x.numel() * x.element_size() for x in hx) + hd.numel() * hd.element_size()
         d2h = hout.numel() * hout.element_size()
     o, keep = make_opts(dtype=cfg["dtype"], method=args.method, timing=False,
-                        strength_dtype="float32" if c64in else None)
+                        strength_dtype="float32" if c64in else None,
+                        coord_dtype="float32" if f32c else None)
     nm = _lib.i64_array(cfg["nm"])
     xp = [ctypes.c_void_p(x.data_ptr()) for x in hx] + [None] * (3 - len(hx))
 

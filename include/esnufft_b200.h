@@ -120,6 +120,8 @@ typedef struct {
                                   complex64 input strengths, upcast exactly on
                                   the device (half the H2D bytes); 0 = the
                                   plan dtype                                  */
+    int coord_dtype;           /* host calls: ESN_F32 = the x / y / z arrays
+                                  hold float32 (read as float*); 0 = float64 */
 } esn_opts;
 
 void esn_default_opts(esn_opts *o);

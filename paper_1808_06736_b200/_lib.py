@@ -35,7 +35,7 @@ class OptsC(ctypes.Structure):
         ("max_grid_values", i64), ("dtype", i32), ("method", i32),
         ("bin_size", i32 * 3), ("max_subprob", i32), ("timing", i32),
         ("stream", vp), ("params", ctypes.POINTER(KernelParamsC)), ("coeffs", P_dbl),
-        ("strength_dtype", i32),
+        ("strength_dtype", i32), ("coord_dtype", i32),
     ]
 
 

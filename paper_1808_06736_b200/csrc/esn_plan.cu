@@ -1232,7 +1232,8 @@ static int copy_rows(void *dst, const void *src, int64_t M_dst, int64_t M_src, i
 }
 
 static int pipelined(HostSlot *slot, int type, int dim, int64_t M, const double *const *xs, int T, void *c, void *f,
-                     int64_t nm, size_t cb, bool c64in) {
+                     int64_t nm, size_t cb, bool c64in, int cdt) {
+    const size_t xsz = cdt == ESN_F32 ? 4 : 8;  // coordinate element size (esn_opts.coord_dtype)
     const auto t_start = std::chrono::steady_clock::now();
     esn_plan p = slot->plan;
     int rc;
@@ -1347,7 +1348,7 @@ static int pipelined(HostSlot *slot, int type, int dim, int64_t M, const double 
         const int64_t lo = bound[k], cnt = bound[k + 1] - lo;
         if (cnt <= 0) continue;
         for (int d = 0; d < dim; ++d)
-            if (cudaMemcpyAsync((double *)slot->dx[d] + lo, xs[d] + lo, sizeof(double) * cnt, cudaMemcpyHostToDevice,
+            if (cudaMemcpyAsync((char *)slot->dx[d] + lo * xsz, (const char *)xs[d] + lo * xsz, xsz * cnt, cudaMemcpyHostToDevice,
                                 up) != cudaSuccess)
                 return fail(ESN_INTERNAL_ERROR, "H2D copy failed");
         if (type == 1 && (rc = c64in ? copy_rows(stage64(lo), c, cnt, M, 0, lo, cnt, T, 8, cudaMemcpyHostToDevice, up)
@@ -1369,8 +1370,8 @@ static int pipelined(HostSlot *slot, int type, int dim, int64_t M, const double 
         ESN_CUDA_TRY(cudaStreamWaitEvent(hs, slot->ev_up[k], 0));
         q->ibase = lo;
         const void *cx[3] = {nullptr, nullptr, nullptr};
-        for (int d = 0; d < dim; ++d) cx[d] = (const double *)slot->dx[d] + lo;
-        if ((rc = esn_plan_setpts(q, cnt, ESN_F64, cx[0], cx[1], cx[2]))) return rc;
+        for (int d = 0; d < dim; ++d) cx[d] = (const char *)slot->dx[d] + lo * xsz;
+        if ((rc = esn_plan_setpts(q, cnt, cdt, cx[0], cx[1], cx[2]))) return rc;
         ESN_CUDA_TRY(cudaStreamWaitEvent(hs, slot->ev_grid, 0));
         if (type == 1) {
             if (c64in && (rc = launch_upcast_c64(stage64(lo), blk, cnt * T, hs))) return rc;
@@ -1440,7 +1441,8 @@ static int pipelined(HostSlot *slot, int type, int dim, int64_t M, const double 
 // stream -> modes down (second transfer stream), so group g's compute and
 // download overlap group g + 1's upload.
 static int transform_pipelined(HostSlot *slot, int dim, int64_t M, const double *const *xs, int T, void *c, void *f,
-                               int64_t nm, size_t cb, bool c64in) {
+                               int64_t nm, size_t cb, bool c64in, int cdt) {
+    const size_t xsz = cdt == ESN_F32 ? 4 : 8;
     esn_plan p = slot->plan;
     cudaStream_t st = p->st;
     if (!slot->up) {
@@ -1466,7 +1468,7 @@ static int transform_pipelined(HostSlot *slot, int dim, int64_t M, const double 
     ESN_CUDA_TRY(cudaStreamWaitEvent(up, slot->ev_in, 0));
     ESN_CUDA_TRY(cudaStreamWaitEvent(down, slot->ev_in, 0));
     for (int d = 0; d < dim; ++d)
-        if (cudaMemcpyAsync(slot->dx[d], xs[d], sizeof(double) * M, cudaMemcpyHostToDevice, up) != cudaSuccess)
+        if (cudaMemcpyAsync(slot->dx[d], xs[d], xsz * M, cudaMemcpyHostToDevice, up) != cudaSuccess)
             return fail(ESN_INTERNAL_ERROR, "H2D copy failed");
     ESN_CUDA_TRY(cudaEventRecord(slot->ev_grid, up));
     // (complex64 input strengths: staged in the second half of dc, upcast per group)
@@ -1479,7 +1481,7 @@ static int transform_pipelined(HostSlot *slot, int dim, int64_t M, const double 
         ESN_CUDA_TRY(cudaEventRecord(slot->ev_up[g], up));
     }
     ESN_CUDA_TRY(cudaStreamWaitEvent(st, slot->ev_grid, 0));
-    int rc = esn_plan_setpts(p, M, ESN_F64, slot->dx[0], slot->dx[1], slot->dx[2]);  // (resets every flag)
+    int rc = esn_plan_setpts(p, M, cdt, slot->dx[0], slot->dx[1], slot->dx[2]);  // (resets every flag)
     const int T0 = p->ntransf;
     p->keep_flags = true;  // the data flag accumulates over the groups
     struct Restore {       // (every exit path restores the plan)
@@ -1590,6 +1592,8 @@ int esn_nufft_host(int type, int dim, int64_t M, const double *x, const double *
     }
     if (!rc && !slot->df) rc = dmalloc(p, &slot->df, cb * nm * ntransf);
     const bool c64in = type == 1 && dtype == ESN_F64 && o.strength_dtype == ESN_F32;
+    const int cdt = o.coord_dtype == ESN_F32 ? ESN_F32 : ESN_F64;  // (host coordinates as float32)
+    const size_t xsz = cdt == ESN_F32 ? 4 : 8;
     if (o.strength_dtype && o.strength_dtype != dtype && !c64in)
         return fail(ESN_SIZE_ERROR, "strength_dtype: only complex64 strengths for a float64 type-1 transform");
     bool pipe = !rc && cacheable && M >= (int64_t)(2 << 20) && is_pinned(c) && is_pinned(f);
@@ -1597,7 +1601,7 @@ int esn_nufft_host(int type, int dim, int64_t M, const double *x, const double *
     static const char *nopipe = getenv("ESN_NO_PIPELINE");
     if (nopipe && nopipe[0] == '1') pipe = false;
     if (pipe) {
-        rc = pipelined(slot, type, dim, M, xs, ntransf, c, f, nm, cb, c64in);
+        rc = pipelined(slot, type, dim, M, xs, ntransf, c, f, nm, cb, c64in, cdt);
         if (transient) free_slot(*slot);
         return rc;
     }
@@ -1605,13 +1609,13 @@ int esn_nufft_host(int type, int dim, int64_t M, const double *x, const double *
     for (int d = 0; d < dim && tpipe; ++d) tpipe = is_pinned(xs[d]);
     if (nopipe && nopipe[0] == '1') tpipe = false;
     if (tpipe) {
-        rc = transform_pipelined(slot, dim, M, xs, ntransf, c, f, nm, cb, c64in);
+        rc = transform_pipelined(slot, dim, M, xs, ntransf, c, f, nm, cb, c64in, cdt);
         if (transient) free_slot(*slot);
         return rc;
     }
     if (!rc) {
         for (int d = 0; d < dim && M > 0; ++d)
-            if (cudaMemcpyAsync(slot->dx[d], xs[d], sizeof(double) * M, cudaMemcpyHostToDevice, st) != cudaSuccess)
+            if (cudaMemcpyAsync(slot->dx[d], xs[d], xsz * M, cudaMemcpyHostToDevice, st) != cudaSuccess)
                 rc = fail(ESN_INTERNAL_ERROR, "H2D copy failed");
         if (!rc && type == 1 && M > 0) {
             // (complex64 strengths: staged in the second half of dc, upcast into the first)
@@ -1624,7 +1628,7 @@ int esn_nufft_host(int type, int dim, int64_t M, const double *x, const double *
             if (cudaMemcpyAsync(slot->df, f, cb * nm * ntransf, cudaMemcpyHostToDevice, st) != cudaSuccess)
                 rc = fail(ESN_INTERNAL_ERROR, "H2D copy failed");
     }
-    if (!rc) rc = esn_plan_setpts(p, M, ESN_F64, slot->dx[0], slot->dx[1], slot->dx[2]);
+    if (!rc) rc = esn_plan_setpts(p, M, cdt, slot->dx[0], slot->dx[1], slot->dx[2]);
     if (!rc) rc = esn_plan_execute(p, slot->dc, slot->df);
     if (!rc) {
         if (type == 1) {

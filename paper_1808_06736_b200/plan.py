@@ -25,7 +25,7 @@ METHODS = {"auto": _lib.METHOD_AUTO, "global": _lib.METHOD_GLOBAL, "tile": _lib.
 def make_opts(*, sigma=2.0, check_bounds=False, use_exact_kernel=False,
               max_grid_values=2 ** 31, dtype="float64", method="auto", bin_size=None,
               max_subprob=0, timing=True, stream=None, params: KernelParams | None = None,
-              coeffs=None, strength_dtype=None):
+              coeffs=None, strength_dtype=None, coord_dtype=None):
     o = _lib.OptsC()
     _lib.lib.esn_default_opts(ctypes.byref(o))
     o.sigma = float(sigma)
@@ -41,6 +41,7 @@ def make_opts(*, sigma=2.0, check_bounds=False, use_exact_kernel=False,
     o.timing = int(bool(timing))
     o.stream = ctypes.c_void_p(stream) if stream else None
     o.strength_dtype = DTYPES[strength_dtype] if strength_dtype else 0
+    o.coord_dtype = DTYPES[coord_dtype] if coord_dtype else 0
     keep = []
     if params is not None:
         kp = params.to_c()

@@ -156,3 +156,29 @@ def test_host_complex64_strengths_for_float64(esn, M, T):
     assert st == 0
     out = hout.numpy()
     assert np.linalg.norm(out - ref) <= 1e-13 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("M,T", [(2_300_000, 1), (60_000, 1), (40_000, 40)])
+def test_host_float32_coordinates(esn, M, T):
+    """esn_opts.coord_dtype = float32: a float32 plan's host coordinates go
+    over as float32 (the device sort reads them directly) -- identical modes
+    to float64 copies of the same values, in every host path."""
+    from paper_1808_06736_b200 import _lib
+    from paper_1808_06736_b200.plan import make_opts
+    rng = np.random.default_rng(43)
+    coords = [rng.uniform(-np.pi, np.pi, M).astype(np.float32) for _ in range(2)]
+    c = (rng.standard_normal((T, M)) + 1j * rng.standard_normal((T, M))).astype(np.complex64)
+    if T == 1:
+        c = c[0]
+    nm = (48, 40)
+    ref_st, ref = _call_host(1, [x.astype(np.float64) for x in coords], c, nm, 1e-4, 1, dtype="float32", ntransf=T)
+    assert ref_st == 0
+    hx = [torch.from_numpy(np.ascontiguousarray(x)).pin_memory() for x in coords]
+    hc = torch.from_numpy(np.ascontiguousarray(c)).pin_memory()
+    hout = torch.empty(((T,) if T > 1 else ()) + tuple(reversed(nm)), dtype=torch.complex64).pin_memory()
+    o, keep = make_opts(dtype="float32", timing=False, coord_dtype="float32")
+    st = _lib.lib.esn_nufft_host(1, 2, M, *[ctypes.c_void_p(x.data_ptr()) for x in hx], None, T,
+                                 ctypes.c_void_p(hc.data_ptr()), 1, 1e-4, _lib.i64_array(nm),
+                                 ctypes.c_void_p(hout.data_ptr()), ctypes.byref(o))
+    assert st == 0
+    assert np.linalg.norm(hout.numpy() - ref) <= 1e-6 * np.linalg.norm(ref)
