@@ -133,6 +133,8 @@ struct Batch2Cfg {
 int launch_setpts(const SetptsArgs &a, int nbins, int max_subprob, int4 *subprob, int *nsub, int *subofs,
                   cudaStream_t st);
 constexpr int kScanTile = 4096;  // keys per scan block
+// records in original order, no sort (small 1D type-1 plans, global-atomic spreader)
+int launch_setpts_unsorted(const SetptsArgs &a, cudaStream_t st);
 int launch_sort_view(int dtype, const void *rec, const int *bin_start, int nbins, int64_t M, int *perm,
                      int *keys, cudaStream_t st);
 // Bin geometry the chosen spreader needs: (bx, by, bz); returns 0 if the

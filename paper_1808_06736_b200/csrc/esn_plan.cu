@@ -756,7 +756,19 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
     a.rec = p->rec;
     a.flags = p->flags;
     a.check_bounds = p->opts.check_bounds;
-    if ((rc = launch_setpts(a, p->nbk, p->maxsub, p->subprob, p->nsub, p->subofs, ss))) return rc;
+    // small 1D type-1 plans spread point-parallel with global atomics: the
+    // records need no order (ESN_SORT1D=1 forces the sort)
+    static const bool sort1d = [] {
+        const char *e = getenv("ESN_SORT1D");
+        return e && e[0] == '1';
+    }();
+    const bool unsorted = p->type == 1 && p->dim == 1 && M <= ((int64_t)1 << 20) && !sort1d &&
+                          p->method == ESN_METHOD_GLOBAL;
+    if (unsorted) {
+        if ((rc = launch_setpts_unsorted(a, ss))) return rc;
+    } else if ((rc = launch_setpts(a, p->nbk, p->maxsub, p->subprob, p->nsub, p->subofs, ss))) {
+        return rc;
+    }
     if (p->have_events) ESN_CUDA_TRY(rec_ev(p, p->ev[1], ss));
     if (side) ESN_CUDA_TRY(cudaEventRecord(p->e_sorted, p->st2));
     return ESN_SUCCESS;

@@ -13,6 +13,7 @@
 // guaranteed multithreaded").
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
 #include <cstring>
 #include <mutex>
@@ -364,6 +365,35 @@ int launch_sort_view(int dtype, const void *rec, const int *bin_start, int nbins
     if (M == 0) return ESN_SUCCESS;
     int fb = (nbins + 127) / 128;
     k_sort_view<<<fb, 128, 0, st>>>((const Rec *)rec, bin_start, nbins, perm, keys);
+    ESN_CUDA_TRY(cudaGetLastError());
+    return ESN_SUCCESS;
+}
+
+// Records in ORIGINAL order (fold + grid scale + checks, no sort): for
+// consumers that only need the records, not their order -- the small 1D
+// type-1 plans, whose point-parallel global-atomic spreader (k_spread_global)
+// sorts only for locality, which a 20000-cell grid in L2 does not need
+// (c1: 1 kernel instead of 7, the sort was ~35 us of a ~90 us step).
+template <typename XT>
+__global__ void __launch_bounds__(256) k_setpts_unsorted(SetptsArgs a) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.M; i += (int64_t)gridDim.x * blockDim.x) {
+        double x[3] = {0.0, 0.0, 0.0}, g[3] = {0.0, 0.0, 0.0};
+        for (int d = 0; d < a.g.dim; ++d) x[d] = (double)__ldg(reinterpret_cast<const XT *>(a.x[d]) + i);
+        point_key(a, i, x, g, true);
+        const unsigned long long j = (unsigned long long)(unsigned)i;
+        asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(a.rec + i), "l"(__double_as_longlong(g[0])),
+                     "l"(__double_as_longlong(g[1])), "l"(__double_as_longlong(g[2])), "l"(j)
+                     : "memory");
+    }
+}
+
+int launch_setpts_unsorted(const SetptsArgs &a, cudaStream_t st) {
+    if (a.M == 0) return ESN_SUCCESS;
+    const int64_t b = std::min<int64_t>((a.M + 255) / 256, (int64_t)device_sm_count() * 8);
+    if (a.coord_f32)
+        k_setpts_unsorted<float><<<(int)b, 256, 0, st>>>(a);
+    else
+        k_setpts_unsorted<double><<<(int)b, 256, 0, st>>>(a);
     ESN_CUDA_TRY(cudaGetLastError());
     return ESN_SUCCESS;
 }
