@@ -43,7 +43,7 @@ import cases  # noqa: E402
 
 METRIC = "NU points/sec (spread+interp, full type-1/2) at 1/2/4/8 B200; % HBM roofline"
 UNIT = "NU points/s"
-K_E2E = 5
+K_E2E = 20  # end-to-end calls timed (a few ms each: enough to average out PCIe jitter)
 
 
 def peaks():
