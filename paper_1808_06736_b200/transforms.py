@@ -340,17 +340,21 @@ def exec_type3(coords, strengths, targets, opts: TransformOptions):
         resc = [torch.empty_like(x) for x in xs]
         _lib.check(_lib.lib.esn_type3_prephase(dim, m, *p3([x.contiguous() for x in xs]), x0, s0, gam,
                                                int(opts.isign < 0), _ptr(c), _ptr(cph), *p3(resc), stream))
-        sp = Plan(0, dim, nfine=geo.sizes, device=dev, params=params, sigma=opts.sigma,
-                  use_exact_kernel=opts.use_exact_kernel, method=opts.method, dtype="float64",
-                  max_grid_values=opts.max_grid_values, timing=True)
+        # the spreader plan is cached like the type-1/2 plans (keyed by the
+        # fine grid the geometry picked): repeated calls skip its allocations
+        skey = (0, dim, tuple(geo.sizes), params, opts.sigma, opts.method, opts.use_exact_kernel,
+                opts.max_grid_values, str(dev), stream)
+        sp = PLANS.get(skey, lambda: Plan(0, dim, nfine=geo.sizes, device=dev, params=params, sigma=opts.sigma,
+                                          use_exact_kernel=opts.use_exact_kernel, method=opts.method,
+                                          dtype="float64", max_grid_values=opts.max_grid_values, timing=True))
         grid = torch.empty(tuple(reversed(geo.sizes)), dtype=torch.complex128, device=dev)
-        sp.setpts(resc)
-        sp.spread(cph, grid)
-        sp.check()
-        t1 = sp.stage_times()
+        with sp.lock:
+            sp.setpts(resc)
+            sp.spread(cph, grid)
+            sp.check()
+            t1 = sp.stage_times()
         timings["sort"] += t1["sort"]
         timings["spread"] += t1["spread"]
-        sp.close()
         b = torch.empty_like(grid)
         _lib.check(_lib.lib.esn_fftshift(dim, nf, _ptr(grid), _ptr(b), stream))
         del grid
