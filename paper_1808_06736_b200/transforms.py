@@ -311,15 +311,20 @@ def exec_type3(coords, strengths, targets, opts: TransformOptions):
                 raise SizeError(f"coordinate array {d + 1} has shape {tuple(xs[d].shape)}")
             if ss[d].dim() != 1 or ss[d].numel() != nk:
                 raise SizeError(f"target array {d + 1} has shape {tuple(ss[d].shape)}")
-            if not bool(torch.isfinite(xs[d]).all()):
-                raise DataError(f"non-finite coordinate in dimension {d + 1}")
-            if not bool(torch.isfinite(ss[d]).all()):
-                raise DataError(f"non-finite target in dimension {d + 1}")
         c = D.as_complex(strengths, dev, torch.complex128)
         if tuple(c.shape) != (m,):
             raise SizeError(f"strengths shape {tuple(c.shape)} does not match M={m}")
-        bad = ~(torch.isfinite(c.real) & torch.isfinite(c.imag))
-        if bool(bad.any()):
+        # every finiteness check in one device reduction (one host sync); the
+        # reference's messages are rebuilt only when something is non-finite
+        ok = torch.stack([torch.isfinite(t).all() for t in xs + ss] +
+                         [(torch.isfinite(c.real) & torch.isfinite(c.imag)).all()])
+        if not bool(ok.all()):
+            for d in range(dim):
+                if not bool(torch.isfinite(xs[d]).all()):
+                    raise DataError(f"non-finite coordinate in dimension {d + 1}")
+                if not bool(torch.isfinite(ss[d]).all()):
+                    raise DataError(f"non-finite target in dimension {d + 1}")
+            bad = ~(torch.isfinite(c.real) & torch.isfinite(c.imag))
             raise DataError(f"non-finite strength at index {int(torch.nonzero(bad)[0, 0])}")
         if nk == 0:
             out = torch.empty(0, dtype=torch.complex128, device=dev)
@@ -348,13 +353,13 @@ def exec_type3(coords, strengths, targets, opts: TransformOptions):
                                           use_exact_kernel=opts.use_exact_kernel, method=opts.method,
                                           dtype="float64", max_grid_values=opts.max_grid_values, timing=True))
         grid = torch.empty(tuple(reversed(geo.sizes)), dtype=torch.complex128, device=dev)
-        with sp.lock:
+        sp.lock.acquire()  # (held until the stage times are read below)
+        try:
             sp.setpts(resc)
             sp.spread(cph, grid)
-            sp.check()
-            t1 = sp.stage_times()
-        timings["sort"] += t1["sort"]
-        timings["spread"] += t1["spread"]
+        except BaseException:
+            sp.lock.release()
+            raise
         b = torch.empty_like(grid)
         _lib.check(_lib.lib.esn_fftshift(dim, nf, _ptr(grid), _ptr(b), stream))
         del grid
@@ -362,7 +367,15 @@ def exec_type3(coords, strengths, targets, opts: TransformOptions):
         _lib.check(_lib.lib.esn_type3_targets(dim, nk, *p3([s.contiguous() for s in ss]), s0, gam, nf,
                                               *p3(inner), stream))
         inner_opts = replace(opts, isign=1, check_bounds=False, params=params, dtype="float64")
-        out, tin = exec_type2(inner, b, inner_opts)
+        try:
+            out, tin = exec_type2(inner, b, inner_opts)
+            # (inputs were checked finite above, so the spreader plan's flags
+            # need no read; its stage events are read once, after the type 2)
+            t1 = sp.stage_times()
+        finally:
+            sp.lock.release()
+        timings["sort"] += t1["sort"]
+        timings["spread"] += t1["spread"]
         _merge_timings(timings, tin)
         # psi-hat correction, post-phase, final conjugation (transforms.py:333-351)
         kp = params.to_c()
