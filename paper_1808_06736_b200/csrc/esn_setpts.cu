@@ -215,12 +215,14 @@ __device__ __forceinline__ int block_scan_excl(int v, int *total, int *wsum) {
 
 __global__ void __launch_bounds__(1024) k_scan_reduce(const int *cnt, int n, int *block_sums) {
     __shared__ int wsum[32];
-    const int base = blockIdx.x * kScanTile;
+    static_assert(kScanTile == 4 * 1024, "one 16-byte vector per thread");
+    const int base = blockIdx.x * kScanTile + threadIdx.x * 4;
     int v = 0;
-#pragma unroll
-    for (int u = 0; u < kScanTile / 1024; ++u) {
-        const int i = base + u * 1024 + threadIdx.x;
-        if (i < n) v += cnt[i];
+    if (base + 4 <= n) {
+        const int4 q = *reinterpret_cast<const int4 *>(cnt + base);
+        v = q.x + q.y + q.z + q.w;
+    } else {
+        for (int i = base; i < n; ++i) v += cnt[i];
     }
     int total;
     block_scan_excl(v, &total, wsum);
@@ -253,23 +255,41 @@ __global__ void __launch_bounds__(1024) k_scan_down(int *cnt, int n, const int *
     __shared__ int wsum[32];
     constexpr int U = kScanTile / 1024;
     const int base = blockIdx.x * kScanTile + threadIdx.x * U;  // each thread owns U consecutive keys
+    static_assert(U == 4, "one 16-byte vector per thread");
+    // full vectors as int4 (the tile base is 16-byte aligned): one 128-bit
+    // load / store per thread instead of four strided 32-bit ones
+    const bool full = base + U <= n;
     int v[U], s = 0;
+    if (full) {
+        const int4 q = *reinterpret_cast<const int4 *>(cnt + base);
+        v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+    } else {
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-        v[u] = base + u < n ? cnt[base + u] : 0;
-        s += v[u];
+        for (int u = 0; u < U; ++u) v[u] = base + u < n ? cnt[base + u] : 0;
     }
+#pragma unroll
+    for (int u = 0; u < U; ++u) s += v[u];
     int total;
     int e = block_scan_excl(s, &total, wsum) + block_sums[blockIdx.x];
+    int o[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
+        o[u] = e;
         const int k = base + u;
-        if (k < n) {
-            cursor[k] = e;
-            cnt[k] = e;
-            if (k % spb == 0) bin_start[k / spb] = e;
-        }
+        if (k < n && k % spb == 0) bin_start[k / spb] = e;
         e += v[u];
+    }
+    if (full) {
+        const int4 q = make_int4(o[0], o[1], o[2], o[3]);
+        *reinterpret_cast<int4 *>(cursor + base) = q;
+        *reinterpret_cast<int4 *>(cnt + base) = q;
+    } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (base + u < n) {
+                cursor[base + u] = o[u];
+                cnt[base + u] = o[u];
+            }
     }
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
         bin_start[nbins] = block_sums[gridDim.x];
