@@ -65,6 +65,7 @@ struct SetptsArgs {
     int nkeys;              // nchunk * nbins * spb
     int nbins_geo;          // geometric bins
     int64_t chunk_len;      // > 0: points per target chunk (key major part)
+    double inv_chunk;       // 1 / chunk_len
     double inv_bs[3];       // 1 / bs (fast division, corrected exactly)
     int64_t M;
     int coord_f32;          // input coordinates are float (else double)

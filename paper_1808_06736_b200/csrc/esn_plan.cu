@@ -747,6 +747,7 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
     a.nkeys = p->nkeys;
     a.nbins_geo = p->nbins;
     a.chunk_len = p->chunk_len;
+    a.inv_chunk = p->chunk_len > 0 ? 1.0 / (double)p->chunk_len : 0.0;
     a.key_count = p->key_count;
     a.block_sums = p->block_sums;
     a.bin_start = p->bin_start;

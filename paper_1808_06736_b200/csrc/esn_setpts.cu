@@ -106,7 +106,8 @@ __device__ __forceinline__ int point_key(const SetptsArgs &a, int64_t i, const d
         loc += ((i0 - q * bs) >> a.sbl[d]) * lmul;
         lmul *= ((bs - 1) >> a.sbl[d]) + 1;
     }
-    if (a.chunk_len > 0) bin += (int)(i / a.chunk_len) * a.nbins_geo;
+    // (i < 2^31: a float64 reciprocal and one fix-up, not a 64-bit division)
+    if (a.chunk_len > 0) bin += fast_div((int)i, (int)a.chunk_len, a.inv_chunk) * a.nbins_geo;
     return bin * a.spb + loc;
 }
 
