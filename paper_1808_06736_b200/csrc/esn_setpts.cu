@@ -75,12 +75,14 @@ __device__ __forceinline__ int fast_div(int i, int d, double inv) {
     return q;
 }
 
-// Fine sort key of one point; g receives its grid coordinates.
+// Fine sort key of one point; g receives its grid coordinates.  DIM = 0:
+// the plan's dimension at run time (the unsorted path).
+template <int DIM = 0>
 __device__ __forceinline__ int point_key(const SetptsArgs &a, int64_t i, const double *xin, double *gout, bool check) {
     int bin = 0, loc = 0, bmul = 1, lmul = 1;
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
-        if (d >= a.g.dim) break;
+    for (int d = 0; d < (DIM ? DIM : 3); ++d) {
+        if (!DIM && d >= a.g.dim) break;
         const double x = xin[d];
         double g = 0.0;
         if (!isfinite(x)) {
@@ -114,7 +116,7 @@ __device__ __forceinline__ int point_key(const SetptsArgs &a, int64_t i, const d
 constexpr int kILP = 4;   // points in flight per thread (independent loads / atomics)
 constexpr int kSILP = 8;  // record scatter: points in flight per thread
 
-template <typename XT, int U = kILP>
+template <typename XT, int DIM, int U = kILP>
 __device__ __forceinline__ void load_coords(const SetptsArgs &a, int64_t base, double (*x)[3]) {
     // all loads first (independent, read-only), compute afterwards
 #pragma unroll
@@ -123,7 +125,7 @@ __device__ __forceinline__ void load_coords(const SetptsArgs &a, int64_t base, d
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
             x[u][d] = 0.0;
-            if (d < a.g.dim && i < a.M) x[u][d] = (double)__ldg(reinterpret_cast<const XT *>(a.x[d]) + i);
+            if (d < DIM && i < a.M) x[u][d] = (double)__ldg(reinterpret_cast<const XT *>(a.x[d]) + i);
         }
     }
 }
@@ -131,18 +133,18 @@ __device__ __forceinline__ void load_coords(const SetptsArgs &a, int64_t base, d
 // Pass 1: key histogram (fire-and-forget REDs: no return trip, no per-point
 // state written) plus the finite / bounds flags.  The ranks come from the
 // scatter pass's fill cursors.
-template <typename XT>
+template <typename XT, int DIM>
 __global__ void __launch_bounds__(256, 4) k_setpts_count(SetptsArgs a) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * kILP;
     for (int64_t base = (int64_t)blockIdx.x * blockDim.x * kILP + threadIdx.x; base < a.M; base += stride) {
         double x[kILP][3];
-        load_coords<XT>(a, base, x);
+        load_coords<XT, DIM>(a, base, x);
         int key[kILP];
 #pragma unroll
         for (int u = 0; u < kILP; ++u) {
             const int64_t i = base + (int64_t)u * blockDim.x;
             double g[3];
-            key[u] = i < a.M ? point_key(a, i, x[u], g, true) : -1;
+            key[u] = i < a.M ? point_key<DIM>(a, i, x[u], g, true) : -1;
         }
 #pragma unroll
         for (int u = 0; u < kILP; ++u)
@@ -156,19 +158,19 @@ __global__ void __launch_bounds__(256, 4) k_setpts_count(SetptsArgs a) {
 // record {g, j} at pos with one 256-bit store (a whole L2 sector).  Batched
 // fp32 plans keep pos in key[] for the strength permutation.  kSILP points
 // per thread, all loads issued before the dependent gather.
-template <typename XT>
+template <typename XT, int DIM>
 __global__ void __launch_bounds__(256) k_setpts_scatter(SetptsArgs a) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * kSILP;
     for (int64_t base = (int64_t)blockIdx.x * blockDim.x * kSILP + threadIdx.x; base < a.M; base += stride) {
         int pos[kSILP];
         double x[kSILP][3];
-        load_coords<XT, kSILP>(a, base, x);
+        load_coords<XT, DIM, kSILP>(a, base, x);
         double g[kSILP][3];
 #pragma unroll
         for (int u = 0; u < kSILP; ++u) {
             const int64_t i = base + (int64_t)u * blockDim.x;
             g[u][0] = g[u][1] = g[u][2] = 0.0;
-            pos[u] = i < a.M ? point_key(a, i, x[u], g[u], false) : -1;
+            pos[u] = i < a.M ? point_key<DIM>(a, i, x[u], g[u], false) : -1;
         }
 #pragma unroll
         for (int u = 0; u < kSILP; ++u)
@@ -348,7 +350,7 @@ __global__ void k_fill_subprob(const int *bin_start, const int *subofs, int nbin
     }
 }
 
-template <typename XT>
+template <typename XT, int DIM>
 static int setpts_impl(const SetptsArgs &a, int nbins, int maxsub, int4 *subprob, int *nsub, int *subofs,
                        cudaStream_t st) {
     const int threads = 256;
@@ -363,12 +365,12 @@ static int setpts_impl(const SetptsArgs &a, int nbins, int maxsub, int4 *subprob
         return (int64_t)device_sm_count() * occ;
     };
     static const int64_t cap_count = (int64_t)device_sm_count() * 8;  // (atomics: oversubscribed is faster)
-    static const int64_t cap_scatter = resident(k_setpts_scatter<XT>);
+    static const int64_t cap_scatter = resident(k_setpts_scatter<XT, DIM>);
     int64_t blocks = (a.M + threads * kILP - 1) / (threads * kILP);
     if (blocks > cap_count) blocks = cap_count;
     if (blocks < 1) blocks = 1;
     if (a.M > 0) {
-        k_setpts_count<XT><<<(int)blocks, threads, 0, st>>>(a);
+        k_setpts_count<XT, DIM><<<(int)blocks, threads, 0, st>>>(a);
         ESN_CUDA_TRY(cudaGetLastError());
     }
     const int nsb = (a.nkeys + kScanTile - 1) / kScanTile;
@@ -379,7 +381,7 @@ static int setpts_impl(const SetptsArgs &a, int nbins, int maxsub, int4 *subprob
     if (a.M > 0) {
         int64_t sb = (a.M + threads * kSILP - 1) / (threads * kSILP);
         if (sb > cap_scatter) sb = cap_scatter;
-        k_setpts_scatter<XT><<<(int)sb, threads, 0, st>>>(a);
+        k_setpts_scatter<XT, DIM><<<(int)sb, threads, 0, st>>>(a);
         ESN_CUDA_TRY(cudaGetLastError());
     }
     k_scan_subprob<<<1, 1024, 0, st>>>(a.bin_start, nbins, maxsub, subofs, nsub);
@@ -440,8 +442,15 @@ int launch_setpts_unsorted(const SetptsArgs &a, cudaStream_t st) {
 
 int launch_setpts(const SetptsArgs &a, int nbins, int max_subprob, int4 *subprob, int *nsub, int *subofs,
                   cudaStream_t st) {
-    return a.coord_f32 ? setpts_impl<float>(a, nbins, max_subprob, subprob, nsub, subofs, st)
-                       : setpts_impl<double>(a, nbins, max_subprob, subprob, nsub, subofs, st);
+    auto run = [&](auto xt) {
+        using XT = decltype(xt);
+        switch (a.g.dim) {
+            case 1: return setpts_impl<XT, 1>(a, nbins, max_subprob, subprob, nsub, subofs, st);
+            case 2: return setpts_impl<XT, 2>(a, nbins, max_subprob, subprob, nsub, subofs, st);
+            default: return setpts_impl<XT, 3>(a, nbins, max_subprob, subprob, nsub, subofs, st);
+        }
+    };
+    return a.coord_f32 ? run(0.0f) : run(0.0);
 }
 
 }  // namespace esn
