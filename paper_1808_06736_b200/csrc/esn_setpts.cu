@@ -75,31 +75,53 @@ __device__ __forceinline__ int fast_div(int i, int d, double inv) {
     return q;
 }
 
+// Grid coordinate of one coordinate value on the rare paths: non-finite
+// (flag d), |x| > 3 pi (flag 3 + d, when checked), |x| >= 2 pi (fmod fold)
+// or caller-folded grid units.  (Out of line it cost 20-30 registers for
+// the call; inline it is only a branch target.)
+__device__ __forceinline__ double grid_coord_slow(unsigned long long *flags, unsigned long long idx, double x, int d,
+                                              bool check, int check_bounds, int grid_units, double n, double scale) {
+    double g = 0.0;
+    if (!isfinite(x)) {
+        if (check) atomicMin(&flags[d], idx);
+    } else {
+        if (check && check_bounds && fabs(x) > 3.0 * 3.141592653589793) atomicMin(&flags[3 + d], idx);
+        if (grid_units) {
+            g = x;  // caller already folded (bin_sort on grid coordinates, grid.py:202)
+            if (g >= n) g -= n;
+            if (g < 0.0) g = 0.0;
+        } else {
+            g = fold_scale(x, n, scale);
+        }
+    }
+    return g;
+}
+
 // Fine sort key of one point; g receives its grid coordinates.  DIM = 0:
-// the plan's dimension at run time (the unsorted path).
+// the plan's dimension at run time (the unsorted path).  The common case
+// |x| < 2 pi (finite, inside the 3 pi bound, fmod the identity) is
+// fold_scale's arithmetic as selects, bit-identical, no branches.
 template <int DIM = 0>
 __device__ __forceinline__ int point_key(const SetptsArgs &a, int64_t i, const double *xin, double *gout, bool check) {
     int bin = 0, loc = 0, bmul = 1, lmul = 1;
+    const double two_pi = 6.283185307179586;
 #pragma unroll
     for (int d = 0; d < (DIM ? DIM : 3); ++d) {
         if (!DIM && d >= a.g.dim) break;
         const double x = xin[d];
-        double g = 0.0;
-        if (!isfinite(x)) {
-            if (check) atomicMin(&a.flags[d], (unsigned long long)(i + a.ibase));
+        const double n = (double)a.g.n[d];
+        double g;
+        if (fabs(x) < two_pi && !a.grid_units) {
+            double r = x < 0.0 ? x + two_pi : x;
+            r = r >= two_pi ? 0.0 : r;
+            g = r * a.scale[d];
+            g = g >= n ? g - n : g;
         } else {
-            if (check && a.check_bounds && fabs(x) > 3.0 * 3.141592653589793)
-                atomicMin(&a.flags[3 + d], (unsigned long long)(i + a.ibase));
-            if (a.grid_units) {
-                g = x;  // caller already folded (bin_sort on grid coordinates, grid.py:202)
-                if (g >= (double)a.g.n[d]) g -= (double)a.g.n[d];
-                if (g < 0.0) g = 0.0;
-            } else {
-                g = fold_scale(x, (double)a.g.n[d], a.scale[d]);
-            }
+            g = grid_coord_slow(a.flags, (unsigned long long)(i + a.ibase), x, d, check, a.check_bounds, a.grid_units,
+                                n, a.scale[d]);
         }
-        gout[d] = g;
-        int i0 = (int)floor(g - 0.5 * a.g.w + 1.0);  // spreadinterp.py:117-120
+    gout[d] = g;
+        int i0 = __double2int_rd(g - 0.5 * a.g.w + 1.0);  // floor (spreadinterp.py:117-120)
         if (i0 < 0) i0 += a.g.n[d];
         const int bs = a.g.bs[d];
         const int q = fast_div(i0, bs, a.inv_bs[d]);
