@@ -82,6 +82,7 @@ struct SetptsArgs {
     int64_t ibase;          // index offset of this point chunk (error reports)
     unsigned long long *flags;  // [0..2] first non-finite per dim, [3..5] first |x|>3pi
     int check_bounds;
+    int hints;              // L2 cache hints in the record scatter (ESN_SCATTER_HINTS=0: off)
 };
 
 template <typename T>

@@ -183,6 +183,11 @@ __global__ void __launch_bounds__(256, 4) k_setpts_count(SetptsArgs a) {
 template <typename XT, int DIM>
 __global__ void __launch_bounds__(256) k_setpts_scatter(SetptsArgs a) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * kSILP;
+    uint64_t pol_first = 0, pol_last = 0;
+    if (a.hints) {
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
+    }
     for (int64_t base = (int64_t)blockIdx.x * blockDim.x * kSILP + threadIdx.x; base < a.M; base += stride) {
         int pos[kSILP];
         double x[kSILP][3];
@@ -194,19 +199,38 @@ __global__ void __launch_bounds__(256) k_setpts_scatter(SetptsArgs a) {
             g[u][0] = g[u][1] = g[u][2] = 0.0;
             pos[u] = i < a.M ? point_key<DIM>(a, i, x[u], g[u], false) : -1;
         }
+        if (a.hints) {
+            // the fill cursors (L2-resident key array) evict-last, the
+            // streaming record stores evict-first: without the hints about
+            // half of the cursor atomics missed the near L2 (ncu, c2)
 #pragma unroll
-        for (int u = 0; u < kSILP; ++u)
-            if (pos[u] >= 0) pos[u] = atomicAdd(a.key_count + pos[u], 1);  // fill cursor of the key
+            for (int u = 0; u < kSILP; ++u)
+                if (pos[u] >= 0)
+                    asm volatile("atom.global.add.L2::cache_hint.u32 %0, [%1], 1, %2;"
+                                 : "=r"(pos[u])
+                                 : "l"(a.key_count + pos[u]), "l"(pol_last)
+                                 : "memory");
+        } else {
+#pragma unroll
+            for (int u = 0; u < kSILP; ++u)
+                if (pos[u] >= 0) pos[u] = atomicAdd(a.key_count + pos[u], 1);  // fill cursor of the key
+        }
 #pragma unroll
         for (int u = 0; u < kSILP; ++u) {
             if (pos[u] < 0) continue;
             const int64_t i = base + (int64_t)u * blockDim.x;
             if (a.store_pos) a.key[i] = pos[u];
             const unsigned long long j = (unsigned long long)(unsigned)i;
-            asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(a.rec + pos[u]),
-                         "l"(__double_as_longlong(g[u][0])), "l"(__double_as_longlong(g[u][1])),
-                         "l"(__double_as_longlong(g[u][2])), "l"(j)
-                         : "memory");
+            if (a.hints)
+                asm volatile("st.global.L2::cache_hint.v4.u64 [%0], {%1,%2,%3,%4}, %5;" ::"l"(a.rec + pos[u]),
+                             "l"(__double_as_longlong(g[u][0])), "l"(__double_as_longlong(g[u][1])),
+                             "l"(__double_as_longlong(g[u][2])), "l"(j), "l"(pol_first)
+                             : "memory");
+            else
+                asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(a.rec + pos[u]),
+                             "l"(__double_as_longlong(g[u][0])), "l"(__double_as_longlong(g[u][1])),
+                             "l"(__double_as_longlong(g[u][2])), "l"(j)
+                             : "memory");
         }
     }
 }
