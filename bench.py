@@ -10,13 +10,20 @@ Other configs (--config c1/c3/c3f/c4/c5) exist for parity-shape timing.
 
 A "step" is one full transform (setpts sort + amplify/spread + cuFFT +
 interp/deconv) over one batch of synthetic seeded input already resident in
-HBM.  Under torchrun (N > 1) every rank runs its own independent shard of
-the same size (weak scaling, no data-path collective): type 2 targets are
-independent outputs.  Times are CUDA events on the launching stream, max
-over ranks.  e2e = the same metric through the C ABI one-shot routine
-(esn_nufft_host) with pinned HOST buffers, H2D + D2H inside the timed
-region.  --impl reference times the CPU restatement of the reference
-(oracle/, "port") with all host threads on the same config.
+HBM.  `--gpus N` with N > 1 re-launches itself under torch.distributed.run
+(N ranks, NCCL, 127.0.0.1) unless already under torchrun; it exits 2 when
+fewer than N GPUs are visible or WORLD_SIZE != N.  At N > 1 every rank runs
+its own independent shard of c2 (weak scaling, no data-path collective:
+type-2 targets are independent outputs), and the line carries
+`sharded_configs`: c3 with its points split across the ranks and the
+fine grids NCCL-reduced to rank 0 (north_star; plus the mode-array reduce
+variant) and c5 with its 64 transforms split (strong scaling).  Times are
+CUDA events on the launching stream, max over ranks.  e2e = the same metric
+end to end with pinned HOST buffers, H2D + D2H inside the timed region:
+through the C ABI one-shot routine (esn_nufft_host) for replicas, through
+the package's distributed API for the sharded paths.  --impl reference
+times the CPU restatement of the reference (oracle/, "port") with all host
+threads on the same config.
 """
 
 from __future__ import annotations
@@ -226,29 +233,35 @@ def cpu_sample_size(name):
 # ---------------------------------------------------------------------------
 # GPU arm
 
-def gpu_run(args, rank, world, local_rank):
+def run_mode(cfg, world, reduce):
+    """Multi-GPU mode of a config."""
+    if world > 1 and cfg["ttype"] == 1 and cfg["ntransf"] == 1 and cfg["dim"] == 3:
+        return "points"
+    if world > 1 and cfg["ntransf"] > 1:
+        return "transforms"
+    return "replica"
+
+
+def gpu_run(args, name, rank, world, local_rank, *, steps, warmup, reduce, e2e, points="uniform"):
+    """Device-resident timing of one config (+ the end-to-end leg).
+
+    replica    : every rank its own independent M points (weak scaling);
+    points     : one transform, its points split across ranks, the partial
+                 fine grids (reduce="grid", north_star) or mode arrays
+                 (reduce="modes") NCCL-reduced to rank 0 (strong scaling);
+    transforms : a batch split across ranks, results all-gathered (strong)."""
     import torch
     import torch.distributed as dist
-    import paper_1808_06736_b200 as E
-    from paper_1808_06736_b200 import _lib
+    from paper_1808_06736_b200.distributed import shard_range
     from paper_1808_06736_b200.plan import Plan
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    name = args.config
     cfg = cases.CONFIGS[name]
     M, T = cfg["M_full"], cfg["ntransf"]
-    # multi-GPU mode: one large type 1 splits its points
-    # (NCCL reduce of the partial modes), a batch splits its transforms
-    # (all-gather of the results); type 2 / 1D run independent replicas
-    mode = "replica"
-    if world > 1 and cfg["ttype"] == 1 and T == 1 and cfg["dim"] == 3:
-        mode = "points"
-    elif world > 1 and T > 1:
-        mode = "transforms"
-    coords, data, cfg = cases.make_inputs(name, M=M, ntransf=T, dist=args.points)
+    mode = run_mode(cfg, world, reduce)
+    coords, data, cfg = cases.make_inputs(name, M=M, ntransf=T, dist=points)
     M = cfg["M_actual"]
-    from paper_1808_06736_b200.distributed import shard_range
     Mr, Tr = M, T
     if mode == "points":
         lo, hi = shard_range(M, rank, world)
@@ -259,7 +272,7 @@ def gpu_run(args, rank, world, local_rank):
         lo, hi = shard_range(T, rank, world)
         data = data[lo:hi]
         Tr = hi - lo
-    elif rank > 0 and args.points == "uniform":
+    elif rank > 0 and points == "uniform":
         # replicas: every rank owns an independent shard (its own seed)
         rng = np.random.default_rng(cfg["seed"] + 7919 * rank)
         coords = [rng.uniform(cfg["lo"], cfg["hi"], M) for _ in range(cfg["dim"])]
@@ -267,6 +280,8 @@ def gpu_run(args, rank, world, local_rank):
     cplx = torch.complex128 if cfg["dtype"] == "float64" else torch.complex64
     xs = [torch.from_numpy(x).to(dev, real).contiguous() for x in coords]
     d = torch.from_numpy(np.ascontiguousarray(data)).to(dev, cplx).contiguous()
+    if Tr < 1:
+        raise SystemExit(f"rank {rank}: no transforms for world {world} (T={T})")
     plan = Plan(cfg["ttype"], cfg["dim"], nmodes=cfg["nm"], isign=cfg["isign"], ntransf=Tr,
                 tol=cfg["tol"], device=dev, dtype=cfg["dtype"], method=args.method, timing=True)
     if cfg["ttype"] == 1:
@@ -281,16 +296,15 @@ def gpu_run(args, rank, world, local_rank):
         width = max(h - l for l, h in (shard_range(T, r, world) for r in range(world)))
         gathered = [torch.empty((width,) + tuple(out.shape[1:]), dtype=cplx, device=dev) for _ in range(world)]
         padded = torch.zeros_like(gathered[0])
-
     fine = None
-    if mode == "points" and args.reduce == "grid":
+    if mode == "points" and reduce == "grid":
         fine = torch.empty(tuple(reversed(plan.nfine)), dtype=cplx, device=dev)
 
     def step():
         plan.setpts(xs)
         if fine is not None:
-            # fine-grid reduce variant: spread, NCCL-reduce the fine grids,
-            # root alone runs FFT + deconvolution
+            # fine-grid reduce (north_star): spread, NCCL-reduce the fine
+            # grids, root alone runs FFT + deconvolution
             plan.spread(cin, fine)
             dist.reduce(torch.view_as_real(fine), dst=0, op=dist.ReduceOp.SUM)
             if rank == 0:
@@ -303,7 +317,7 @@ def gpu_run(args, rank, world, local_rank):
             padded[: out.shape[0]].copy_(out)
             dist.all_gather([torch.view_as_real(g) for g in gathered], torch.view_as_real(padded))
 
-    for _ in range(max(args.warmup, 0)):
+    for _ in range(max(warmup, 0)):
         step()
     plan.check()
     torch.cuda.synchronize(dev)
@@ -314,10 +328,7 @@ def gpu_run(args, rank, world, local_rank):
     with ClockSampler(local_rank) as clk:
         torch.cuda.synchronize(dev)
         ev0.record(stream)
-        # per-step stage events are recorded by the plan on the same stream;
-        # they are read after each step's own events complete (no host sync
-        # between steps except the event query of the previous step)
-        for k in range(args.steps):
+        for k in range(steps):
             step()
             if args.stage_sync:
                 st = plan.stage_times()
@@ -326,10 +337,12 @@ def gpu_run(args, rank, world, local_rank):
                 hot.append(plan.hot_kernel_seconds())
         ev1.record(stream)
         torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
     elapsed = ev0.elapsed_time(ev1) / 1e3
     if not args.stage_sync:
         st = plan.stage_times()
-        stages = {k: v * args.steps for k, v in st.items()}
+        stages = {k: v * steps for k, v in st.items()}
         hot = [plan.hot_kernel_seconds()]
     plan.check()
     t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
@@ -337,30 +350,39 @@ def gpu_run(args, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     elapsed = float(t.item())
     Tn = T if cfg["ttype"] == 1 else 1
+    # units processed by the whole job per step: replicas each own M points;
+    # a split transform / batch is M * T in total
     total_units = M * Tn * (world if mode == "replica" else 1)
-    value = total_units * args.steps / elapsed
+    value = total_units * steps / elapsed
     B, G = algorithmic_bytes(cfg, Mr, Tr)
     hot_s = statistics.mean(hot)
     peak, peak_kind = peaks()
-    achieved = B / hot_s / 1e9
-    res = dict(value=value, elapsed=elapsed, hot_s=hot_s, achieved=achieved, peak=peak, mode=mode, M=M,
-               peak_kind=peak_kind, B=B, G=G, clocks=clk.summary(),
-               stages={k: v / args.steps for k, v in stages.items()})
-    # e2e through the C ABI with pinned host buffers
-    if args.e2e:
-        e2 = e2e_run(args, cfg, coords, data, M, T, dev)
+    res = dict(value=value, elapsed=elapsed, steps=steps, hot_s=hot_s, achieved=B / hot_s / 1e9, peak=peak,
+               mode=mode, M=M, peak_kind=peak_kind, B=B, G=G, clocks=clk.summary(), reduce=reduce,
+               stages={k: v / steps for k, v in st.items()} if not args.stage_sync
+               else {k: v / steps for k, v in stages.items()})
+    plan.close()
+    del xs, d, out, fine, gathered
+    torch.cuda.empty_cache()
+    if e2e:
+        if mode == "replica":
+            e2 = e2e_host_abi(args, cfg, coords, data, M, T, dev, warmup)
+        else:
+            e2 = e2e_sharded(cfg, coords, data, M, Mr, T, Tr, mode, reduce, rank, world, dev, warmup)
         te = torch.tensor([e2.pop("elapsed")], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2["value"] = M * (T if cfg["ttype"] == 1 else 1) * world * e2.pop("calls") / float(te.item())
-        e2["note"] = "independent replica per rank" if world > 1 else "1 GPU"
-        e2["ms_per_step"] = float(te.item()) / K_E2E * 1e3
+        units = M * (T if cfg["ttype"] == 1 else 1) * (world if mode == "replica" else 1)
+        e2["value"] = units * e2.pop("calls") / float(te.item())
+        e2["ms_per_step"] = float(te.item()) / e2["calls_timed"] * 1e3
         res["e2e"] = e2
-    plan.close()
     return res
 
 
-def e2e_run(args, cfg, coords, data, M, T, dev):
+def e2e_host_abi(args, cfg, coords, data, M, T, dev, warmup):
+    """End to end through the C ABI one-shot routine esn_nufft_host with
+    pinned HOST buffers: H2D of the inputs and D2H of the result inside the
+    timed region (this rank's own M points / T transforms)."""
     import torch
     from paper_1808_06736_b200 import _lib
     from paper_1808_06736_b200.plan import make_opts
@@ -372,17 +394,17 @@ def e2e_run(args, cfg, coords, data, M, T, dev):
     # a config whose strengths ARE complex64 (c3: "c_j complex64", computed in
     # float64) hands them over as such: upcast exactly on the device
     c64in = cfg["ttype"] == 1 and cfg["dtype"] == "float64" and cfg.get("cdtype") == "complex64"
-    hd = torch.from_numpy(data).to(torch.complex64 if c64in else cplx).pin_memory()
+    hd = torch.from_numpy(np.ascontiguousarray(data)).to(torch.complex64 if c64in else cplx).pin_memory()
+    assert hx[0].numel() == M, "e2e buffers must hold exactly this rank's M points"
     if cfg["ttype"] == 1:
-        hout = torch.empty((T,) + tuple(reversed(cfg["nm"])), dtype=cplx).pin_memory()
+        assert hd.numel() == M * T
+        hout = torch.empty(((T,) if T > 1 else ()) + tuple(reversed(cfg["nm"])), dtype=cplx).pin_memory()
         cptr, fptr = hd.data_ptr(), hout.data_ptr()
-        h2d = sum(x.numel() * x.element_size() for x in hx) + hd.numel() * hd.element_size()
-        d2h = hout.numel() * hout.element_size()
     else:
         hout = torch.empty((T, M) if T > 1 else (M,), dtype=cplx).pin_memory()
         cptr, fptr = hout.data_ptr(), hd.data_ptr()
-        h2d = sum(x.numel() * x.element_size() for x in hx) + hd.numel() * hd.element_size()
-        d2h = hout.numel() * hout.element_size()
+    h2d = sum(x.numel() * x.element_size() for x in hx) + hd.numel() * hd.element_size()
+    d2h = hout.numel() * hout.element_size()
     o, keep = make_opts(dtype=cfg["dtype"], method=args.method, timing=False,
                         strength_dtype="float32" if c64in else None,
                         coord_dtype="float32" if f32c else None)
@@ -394,31 +416,177 @@ def e2e_run(args, cfg, coords, data, M, T, dev):
                                            ctypes.c_void_p(cptr), cfg["isign"], cfg["tol"], nm,
                                            ctypes.c_void_p(fptr), ctypes.byref(o)))
 
-    for _ in range(max(1, args.warmup)):
+    for _ in range(max(1, warmup)):
         call()
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
     for _ in range(K_E2E):
         call()
     el = time.perf_counter() - t0
-    return {"elapsed": el, "calls": K_E2E, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+    return {"elapsed": el, "calls": K_E2E, "calls_timed": K_E2E, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "api": "esn_nufft_host (C ABI, pinned host buffers)"}
 
 
-def config_block(name, world, dist="uniform", M=None):
+def e2e_sharded(cfg, coords, data, M, Mr, T, Tr, mode, reduce, rank, world, dev, warmup):
+    """End to end of the sharded paths through the package's public
+    distributed API (paper_1808_06736_b200.distributed) with pinned HOST
+    buffers: each rank's shard goes H2D, is spread (and, for the modes
+    reduce / transform split, FFT'd + deconvolved), the NCCL reduce /
+    all-gather runs, and rank 0 reads the result back D2H."""
+    import torch
+    import torch.distributed as dist
+    import paper_1808_06736_b200 as E
+    from paper_1808_06736_b200 import distributed as DD
+    cplx = torch.complex128 if cfg["dtype"] == "float64" else torch.complex64
+    real = torch.float64 if cfg["dtype"] == "float64" else torch.float32
+    hx = [torch.from_numpy(np.ascontiguousarray(x)).to(real).pin_memory() for x in coords]
+    opts = E.TransformOptions(tolerance=cfg["tol"], isign=cfg["isign"], dtype=cfg["dtype"], device=dev)
+    if mode == "points":
+        hd = torch.from_numpy(np.ascontiguousarray(data)).to(cplx).pin_memory()
+        assert hx[0].numel() == Mr and hd.numel() == Mr
+
+        def call():
+            if reduce == "grid":
+                r = DD.exec_type1_grid_reduced(hx, hd, cfg["nm"], opts, dst=0)
+            else:
+                r = DD.exec_type1_point_sharded(hx, hd, cfg["nm"], opts, dst=0)
+            return r.cpu() if rank == 0 else None
+        h2d = sum(x.numel() * x.element_size() for x in hx) + hd.numel() * hd.element_size()
+        d2h = int(np.prod(cfg["nm"])) * hd.element_size() if rank == 0 else 0
+    else:
+        # the transform split reads only this rank's rows of the (T, M)
+        # host batch; the other rows are never touched
+        from paper_1808_06736_b200.distributed import shard_range
+        lo, hi = shard_range(T, rank, world)
+        hd = torch.empty((T, M), dtype=cplx).pin_memory()
+        hd[lo:hi].copy_(torch.from_numpy(np.ascontiguousarray(data)).to(cplx))
+
+        def call():
+            r = DD.exec_type1_transform_sharded(hx, hd, cfg["nm"], opts)
+            return r.cpu() if rank == 0 else None
+        h2d = sum(x.numel() * x.element_size() for x in hx) + (hi - lo) * M * hd.element_size()
+        d2h = T * int(np.prod(cfg["nm"])) * hd.element_size() if rank == 0 else 0
+    for _ in range(max(1, warmup)):
+        call()
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    k = 5
+    t0 = time.perf_counter()
+    for _ in range(k):
+        call()
+    torch.cuda.synchronize(dev)
+    el = time.perf_counter() - t0
+    return {"elapsed": el, "calls": k, "calls_timed": k, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h),
+            "api": ("distributed.exec_type1_grid_reduced" if mode == "points" and reduce == "grid" else
+                    "distributed.exec_type1_point_sharded" if mode == "points" else
+                    "distributed.exec_type1_transform_sharded")
+                   + " (pinned host shards; H2D, spread/FFT, NCCL, D2H on rank 0)"}
+
+
+def config_block(name, world, dist="uniform", M=None, mode="replica", reduce="grid"):
     cfg = cases.CONFIGS[name]
     nm = "x".join(str(v) for v in cfg["nm"])
     M = cfg["M_full"] if M is None else M
     pts = "iid uniform, seeded" if dist == "uniform" else f"{dist} quadrature cloud (clustered)"
+    per = " per GPU" if mode == "replica" else " total"
+    par = "1 GPU"
+    if world > 1:
+        par = {"replica": f"replica shards x{world} (independent points per GPU)",
+               "points": f"points split x{world}, NCCL reduce of the partial "
+                         + ("fine grids, root FFT + deconv" if reduce == "grid" else "mode arrays"),
+               "transforms": f"transforms split x{world}, all-gather of the results"}[mode]
     return {
-        "workload": f"{name}: {cfg['dim']}D type-{cfg['ttype']}, modes {nm}, M={M:.0e}"
-                    f" per GPU, eps={cfg['tol']:g}, isign={cfg['isign']:+d}, ntransf={cfg['ntransf']}"
+        "workload": f"{name}: {cfg['dim']}D type-{cfg['ttype']}, modes {nm}, M={M:.0e}{per}, "
+                    f"eps={cfg['tol']:g}, isign={cfg['isign']:+d}, ntransf={cfg['ntransf']}"
                     + ("" if dist == "uniform" else f", points {dist}"),
-        "dim": cfg["dim"], "type": cfg["ttype"], "modes": list(cfg["nm"]), "M_per_gpu": M,
-        "tol": cfg["tol"], "ntransf": cfg["ntransf"], "points": pts,
-        "parallelism": f"replica shards x{world} (independent points per GPU)" if world > 1 else "1 GPU",
+        "dim": cfg["dim"], "type": cfg["ttype"], "modes": list(cfg["nm"]),
+        ("M_per_gpu" if mode == "replica" else "M_total"): M,
+        "tol": cfg["tol"], "ntransf": cfg["ntransf"], "points": pts, "parallelism": par,
         "l2": "inputs larger than L2 (coords + outputs > 126 MB), no explicit flush",
     }
+
+
+def cpu_info():
+    """CPU model and core counts of this host."""
+    info = {"logical_cores": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        kv = {}
+        for line in out.splitlines():
+            if ":" in line:
+                k, v = line.split(":", 1)
+                kv[k.strip()] = v.strip()
+        info["cpu_model"] = kv.get("Model name")
+        sockets = int(kv.get("Socket(s)", "1") or 1)
+        cps = int(kv.get("Core(s) per socket", "0") or 0)
+        info["physical_cores"] = sockets * cps if cps else None
+        info["threads_per_core"] = int(kv.get("Thread(s) per core", "1") or 1)
+    except Exception:
+        pass
+    try:
+        info["affinity_cores"] = len(os.sched_getaffinity(0))
+    except Exception:
+        pass
+    return info
+
+
+def n_launches(cfg):
+    """Our kernels per step: setpts = count, scan x3, scatter, subproblem
+    scan + fill (7); type 2: amplify + interp; type 1: spread (batched:
+    permute + row table + spread) + deconv.  cuFFT's own kernels excluded."""
+    hk = hot_kernel_name(cfg)
+    return 7 + (2 if cfg["ttype"] == 2 else (3 if hk in ("k_spread_batch2d", "k_spread_b2own") else 1) + 1)
+
+
+def line_for(args, name, res, world, base):
+    cfg = cases.CONFIGS[name]
+    frac = res["achieved"] / res["peak"]
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(name)
+        except Exception:
+            traffic = None
+    kern = "interp" if cfg["ttype"] == 2 else "spread"
+    b = dict(base)
+    if res["mode"] != "replica":
+        b["scaling"] = "strong"
+    line = dict(b, value=res["value"], ms_per_step=res["elapsed"] / res["steps"] * 1e3,
+                config=config_block(name, world, args.points, res["M"], res["mode"], res["reduce"]),
+                roofline={"bound": "hbm", "achieved": res["achieved"], "peak": res["peak"],
+                          "unit": "GB/s", "frac": frac, "traffic": traffic,
+                          "kernel": f"{kern} ({hot_kernel_name(cfg)})",
+                          "algorithmic_bytes": res["B"], "kernel_ms": res["hot_s"] * 1e3,
+                          "peak_source": f"{res['peak_kind']} MEASURED_PEAKS.json hbm_gbs",
+                          "binding": BINDING.get(name)},
+                stages_ms={k: v * 1e3 for k, v in res["stages"].items()},
+                clocks=res["clocks"], gpu_launches=n_launches(cfg) * res["steps"])
+    if traffic is not None:
+        line["roofline"]["traffic_source"] = "profiles/traffic.json (ncu dram__bytes_read+write of this kernel)"
+    if "e2e" in res:
+        line["e2e"] = res["e2e"]
+    return line
+
+
+def self_launch(args):
+    """`python bench.py --gpus N` (N > 1) outside torchrun: re-run this
+    script under torch.distributed.run with N ranks on 127.0.0.1."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible", file=sys.stderr)
+        sys.exit(2)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    print("bench.py: launching " + " ".join(cmd), file=sys.stderr, flush=True)
+    sys.exit(subprocess.call(cmd))
 
 
 def main():
@@ -429,25 +597,29 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=list(cases.CONFIGS))
     ap.add_argument("--method", default="auto")
-    ap.add_argument("--reduce", default="modes", choices=["modes", "grid"],
-                    help="multi-GPU single 3D type 1: NCCL-reduce the per-rank mode arrays (each rank "
-                         "FFTs + deconvolves) or the fine grids (root alone finishes)")
+    ap.add_argument("--reduce", default="grid", choices=["modes", "grid"],
+                    help="multi-GPU single 3D type 1: NCCL-reduce the fine grids (north_star; root alone "
+                         "runs FFT + deconv) or the per-rank mode arrays (each rank FFTs + deconvolves)")
     ap.add_argument("--points", default="uniform", choices=list(cases.DISTRIBUTIONS),
                     help="point cloud: the config's iid uniform points, or the paper's clustered "
                          "disc-quad (2D) / sph-quad (3D) quadrature clouds of about M points")
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu", dest="cpu", action="store_false")
+    ap.add_argument("--no-sharded", dest="sharded", action="store_false",
+                    help="skip the sharded-config measurements (c3 point split, c5 transform split) "
+                         "attached to the default c2 line")
     ap.add_argument("--stage-sync", action="store_true",
                     help="read stage events after every step (adds a host sync per step)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
+    in_torchrun = "WORLD_SIZE" in os.environ
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     cfg = cases.CONFIGS[args.config]
-    base = {"metric": METRIC, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+    base = {"metric": METRIC, "unit": UNIT, "n_gpus": world if in_torchrun else args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64" if cfg["dtype"] == "float64" else "f32",
             "data": "synthetic (seeded " + ("iid uniform" if args.points == "uniform" else args.points)
                     + " points, N(0,1) complex data; BASELINE.json shapes)"}
@@ -459,63 +631,68 @@ def main():
         v, per, cores = cpu_run(args.config, Ms, Ts, max(1, args.steps), args.warmup, args.points)
         line = dict(base, value=v, ms_per_step=per * 1e3, impl="reference",
                     config=config_block(args.config, 1, args.points),
-                    cpu_baseline={"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                                  "sample": f"{args.config} with M={Ms:.0e}, ntransf={Ts} per step "
-                                            "(oracle/ C+OpenMP restatement of the reference path, "
-                                            "scipy pocketfft)"},
+                    cpu_baseline=dict({"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                                       "sample": f"{args.config} with M={Ms:.0e}, ntransf={Ts} per step "
+                                                 "(oracle/ C+OpenMP restatement of the reference path, "
+                                                 "scipy pocketfft)"}, **cpu_info()),
                     e2e={"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
+        line["n_gpus"] = args.gpus
         print(json.dumps(line), flush=True)
         return
 
+    if not in_torchrun and args.gpus > 1:
+        self_launch(args)
     import torch
     import torch.distributed as dist
-    if world > 1:
+    if in_torchrun and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
+    if torch.cuda.device_count() < (local_rank + 1):
+        print(f"bench.py: rank {rank} needs cuda:{local_rank}, {torch.cuda.device_count()} visible",
+              file=sys.stderr)
+        sys.exit(2)
+    if in_torchrun:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    res = gpu_run(args, rank, world, local_rank)
+        print(f"bench.py: rank {rank}/{world} on cuda:{local_rank} "
+              f"({torch.cuda.get_device_name(local_rank)}), NCCL {torch.cuda.nccl.version()}",
+              file=sys.stderr, flush=True)
+    res = gpu_run(args, args.config, rank, world, local_rank, steps=args.steps, warmup=args.warmup,
+                  reduce=args.reduce, e2e=args.e2e, points=args.points)
+    sharded = {}
+    if args.sharded and args.config == "c2" and args.points == "uniform":
+        # north_star: the sharded configs at every N -- c3 one transform with
+        # its points split (fine-grid reduce, and the mode-array variant)
+        # and c5's batch split; printed inside the same line
+        runs = [("c3_grid_reduce", "c3", "grid"), ("c3_modes_reduce", "c3", "modes"),
+                ("c5_transform_split", "c5", "grid")]
+        if world == 1:  # (one GPU: no reduce, the two c3 variants coincide)
+            runs = [("c3", "c3", "grid"), ("c5", "c5", "grid")]
+        for key, name, red in runs:
+            r = gpu_run(args, name, rank, world, local_rank, steps=5, warmup=3, reduce=red,
+                        e2e=args.e2e and red == "grid")
+            if rank == 0:
+                ln = line_for(args, name, r, world, base)
+                sharded[key] = {k: ln[k] for k in ("value", "ms_per_step", "scaling", "config", "roofline",
+                                                   "stages_ms") if k in ln}
+                sharded[key]["n_gpus"] = world
+                sharded[key]["gpu_launches"] = n_launches(cases.CONFIGS[name]) * 5
+                if "e2e" in ln:
+                    sharded[key]["e2e"] = ln["e2e"]
     if world > 1:
         dist.barrier()
     if rank == 0:
-        frac = res["achieved"] / res["peak"]
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "traffic.json")
-        if os.path.exists(tp):
-            try:
-                traffic = json.load(open(tp)).get(args.config)
-            except Exception:
-                traffic = None
-        kern = "interp" if cfg["ttype"] == 2 else "spread"
-        # our kernels per step: setpts = count, scan x3, scatter, subproblem
-        # scan + fill (7); type 2: amplify + interp; type 1: spread (batched:
-        # permute + row table + spread) + deconv.  cuFFT's own kernels excluded.
-        hk = hot_kernel_name(cfg)
-        n_launch = 7 + (2 if cfg["ttype"] == 2 else (3 if hk in ("k_spread_batch2d", "k_spread_b2own") else 1) + 1)
-        cb = config_block(args.config, world, args.points, res["M"])
-        if res["mode"] == "points":
-            cb["parallelism"] = (f"points split x{world}, NCCL reduce of the partial "
-                                 + ("fine grids, root FFT + deconv" if args.reduce == "grid" else "modes"))
-            base["scaling"] = "strong"
-        elif res["mode"] == "transforms":
-            cb["parallelism"] = f"transforms split x{world}, all-gather of the results"
-            base["scaling"] = "strong"
-        line = dict(base, value=res["value"], ms_per_step=res["elapsed"] / args.steps * 1e3,
-                    config=cb,
-                    roofline={"bound": "hbm", "achieved": res["achieved"], "peak": res["peak"],
-                              "unit": "GB/s", "frac": frac, "traffic": traffic,
-                              "kernel": f"{kern} ({hot_kernel_name(cfg)})",
-                              "algorithmic_bytes": res["B"], "kernel_ms": res["hot_s"] * 1e3,
-                              "peak_source": f"{res['peak_kind']} MEASURED_PEAKS.json hbm_gbs",
-                              "binding": BINDING.get(args.config)},
-                    stages_ms={k: v * 1e3 for k, v in res["stages"].items()},
-                    clocks=res["clocks"], gpu_launches=n_launch * args.steps)
-        if "e2e" in res:
-            line["e2e"] = res["e2e"]
+        line = line_for(args, args.config, res, world, base)
+        if sharded:
+            line["sharded_configs"] = sharded
+            line["gpu_launches"] += sum(v["gpu_launches"] for v in sharded.values())
         if args.cpu and world == 1:
             try:
                 Ms, Ts = cpu_sample_size(args.config)
                 v, per, cores = cpu_run(args.config, Ms, Ts, 1, 0, args.points)
-                line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                                        "sample": f"{args.config} with M={Ms:.0e}, ntransf={Ts}, one "
-                                                  "full transform (oracle/ C+OpenMP port, scipy FFT)"}
+                line["cpu_baseline"] = dict({"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                                             "sample": f"{args.config} with M={Ms:.0e}, ntransf={Ts}, one "
+                                                       "full transform (oracle/ C+OpenMP port, scipy FFT)"},
+                                            **cpu_info())
             except Exception as exc:  # the baseline must never sink the GPU line
                 line["cpu_baseline"] = {"value": None, "error": str(exc)[:200]}
         print(json.dumps(line), flush=True)

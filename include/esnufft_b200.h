@@ -142,7 +142,14 @@ int esn_plan_create(int type, int dim, const int64_t *nmodes, int isign,
 int esn_spreader_create(int dim, const int64_t *nfine, int ntransf,
                         const esn_opts *opts, esn_plan *out);
 /* Fold, grid-scale and bin-sort M points (device arrays of coord_dtype);
- * replaces build_point_set + ensure_sorted (spreadinterp.py:79-114). */
+ * replaces build_point_set + ensure_sorted (spreadinterp.py:79-114).
+ * Stream contract: a type-2 plan sorts on a private side stream that first
+ * waits for the work already queued on opts.stream; the coordinate arrays
+ * are read by that side stream until the next call on this plan
+ * (execute / interp / spread / check / setpts), which orders opts.stream
+ * after the sort.  Do not modify or free x / y / z before that call (or a
+ * stream synchronisation).  Each setpts first joins any earlier pending
+ * sort of the plan. */
 int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x,
                     const void *y, const void *z);
 /* Run the transform (device arrays).  type 1: c (ntransf, M) -> f

@@ -65,7 +65,8 @@ struct SpreadRowsOp {
             }();
             if (!old_rows) {
                 using Cfg3 = Rows3Cfg<T, W>;
-                static int grid3 = 0;
+                static PerDev<int> grid3_;
+                int &grid3 = grid3_();
                 if (grid3 == 0) {
                     int rc = persistent_launch(k_spread_rows3<T, W>, Cfg3::NT, Cfg3::SMEM, st, nullptr, &grid3);
                     if (rc) return rc;
@@ -82,7 +83,8 @@ struct SpreadRowsOp {
                              (Cfg::NT / 32) * Cfg::CH;
         const size_t tile = (size_t)Cfg::RY * Cfg::RZ * Cfg::X * sizeof(C);
         const size_t smem = stage > tile ? stage : tile;
-        static int grid = 0;
+        static PerDev<int> grid_;
+        int &grid = grid_();
         if (grid == 0) {
             int rc = persistent_launch(k_spread_rows<T, D, W>, Cfg::NT, smem, st, nullptr, &grid);
             if (rc) return rc;
@@ -114,21 +116,24 @@ struct SpreadBatchOp {
             // cell-resolution sort keys -> static x-offset sweep; else per-point dispatch
             if (batched_owner(ESN_F32, 2, W, a.ntransf, ESN_METHOD_TILE, a.sbl, a.g.bs)) {
                 constexpr size_t osmem = b2own_smem_bytes<T, W>();
-                static int grid = 0;
+                static PerDev<int> grid_;
+                int &grid = grid_();
                 if (grid == 0) {
                     int rc = persistent_launch(k_spread_b2own<T, W>, 128, osmem, st, nullptr, &grid);
                     if (rc) return rc;
                 }
                 k_spread_b2own<T, W><<<grid, 128, osmem, st>>>(a, cperm, tab);
             } else if (a.sbl[0] == 0 && a.sbl[1] == 0 && a.g.bs[0] == Cfg::BX) {
-                static int grid = 0;
+                static PerDev<int> grid_;
+                int &grid = grid_();
                 if (grid == 0) {
                     int rc = persistent_launch(k_spread_batch2d<T, W, true>, 128, smem, st, nullptr, &grid);
                     if (rc) return rc;
                 }
                 k_spread_batch2d<T, W, true><<<grid, 128, smem, st>>>(a, cperm, tab);
             } else {
-                static int grid = 0;
+                static PerDev<int> grid_;
+                int &grid = grid_();
                 if (grid == 0) {
                     int rc = persistent_launch(k_spread_batch2d<T, W, false>, 128, smem, st, nullptr, &grid);
                     if (rc) return rc;
@@ -165,7 +170,8 @@ struct InterpOp {
             const int slice = sl ? atoi(sl) : 512;
             const size_t bsmem = 2 * cells * sizeof(C) + 2 * (size_t)slice * sizeof(Rec);
             if (bsmem <= 112 * 1024) {
-                static size_t bconfigured = 0;
+                static PerDev<size_t> bconf_;
+                size_t &bconfigured = bconf_();
                 if (bsmem > bconfigured) {
                     ESN_CUDA_TRY(cudaFuncSetAttribute(k_interp_bulk<T, D, W>,
                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem));
@@ -185,7 +191,8 @@ struct InterpOp {
             ESN_CUDA_TRY(cudaGetLastError());
             return ESN_SUCCESS;
         }
-        static size_t configured = 0;
+        static PerDev<size_t> conf_;
+        size_t &configured = conf_();
         if (smem > configured) {
             ESN_CUDA_TRY(cudaFuncSetAttribute(k_interp_tile<T, D, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               (int)smem));

@@ -169,6 +169,16 @@ int launch_amplify(int dim, int ntransf, const int *n, const int64_t *N, const T
                    const T *p2, const T *p3, T *grid, unsigned long long *flag, cudaStream_t st);
 
 int device_sm_count();
+// index of the calling thread's current CUDA device, clamped to [0, 64)
+int current_device();
+// a launcher setting cached per device: kernel attributes (the dynamic
+// shared-memory limit) and occupancy-derived grid sizes are per-device
+// properties, so a process driving several GPUs keeps one slot for each
+template <typename V>
+struct PerDev {
+    V v[64] = {};
+    V &operator()() { return v[current_device()]; }
+};
 
 // 2D type 1 with a power-of-two n2: pruned y-FFT fused with the
 // deconvolution (after a 1D cuFFT x pass); twid = e^{isign 2 pi i k / n2},

@@ -32,28 +32,25 @@ using namespace esn;
 static inline size_t real_size(int dtype) { return dtype == ESN_F64 ? 8 : 4; }
 
 // ---------------------------------------------------------------------------
-// cuFFT plan cache keyed by (dim, n, dtype, batch) -- the fft.py:87-111 analog.
+// cuFFT handles.  A cuFFT handle owns one work area, so two FFTs may run
+// concurrently only on different handles: every esn_plan owns its handle
+// (created on first use, destroyed with the plan; captured graphs of the
+// plan bake in the plan's own work area), and the plan-less esn_fft keeps a
+// cache keyed by (shape, dtype, batch, device, STREAM) -- work on one stream
+// is serialised by the stream itself.  The fft.py:87-111 analog.
 namespace {
 struct FftKey {
     int dim, n1, n2, n3, dtype, batch, device;
+    uintptr_t stream;
     bool operator<(const FftKey &o) const {
-        return std::tie(dim, n1, n2, n3, dtype, batch, device) <
-               std::tie(o.dim, o.n1, o.n2, o.n3, o.dtype, o.batch, o.device);
+        return std::tie(dim, n1, n2, n3, dtype, batch, device, stream) <
+               std::tie(o.dim, o.n1, o.n2, o.n3, o.dtype, o.batch, o.device, o.stream);
     }
 };
 std::mutex g_fft_mu;
 std::map<FftKey, cufftHandle> g_fft_cache;
 
-int get_fft_plan(int dim, const int *n, int dtype, int batch, cufftHandle *out) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    FftKey key{dim, n[0], dim > 1 ? n[1] : 1, dim > 2 ? n[2] : 1, dtype, batch, dev};
-    std::lock_guard<std::mutex> lk(g_fft_mu);
-    auto it = g_fft_cache.find(key);
-    if (it != g_fft_cache.end()) {
-        *out = it->second;
-        return ESN_SUCCESS;
-    }
+int make_fft_plan(int dim, const int *n, int dtype, int batch, cufftHandle *out) {
     int dims[3];
     for (int d = 0; d < dim; ++d) dims[d] = n[dim - 1 - d];  // slowest first
     int64_t dist = 1;
@@ -62,16 +59,11 @@ int get_fft_plan(int dim, const int *n, int dtype, int batch, cufftHandle *out) 
     cufftResult r = cufftPlanMany(&h, dim, dims, nullptr, 1, (int)dist, nullptr, 1, (int)dist,
                                   dtype == ESN_F64 ? CUFFT_Z2Z : CUFFT_C2C, batch);
     if (r != CUFFT_SUCCESS) return fail(ESN_INTERNAL_ERROR, "cufftPlanMany failed (%d)", (int)r);
-    g_fft_cache[key] = h;
     *out = h;
     return ESN_SUCCESS;
 }
 
-int run_fft(int dim, const int *n, int dtype, int batch, void *data, int sign, cudaStream_t st) {
-    cufftHandle h;
-    int rc = get_fft_plan(dim, n, dtype, batch, &h);
-    if (rc) return rc;
-    std::lock_guard<std::mutex> lk(g_fft_mu);  // SetStream + enqueue as one unit
+int exec_fft(cufftHandle h, int dtype, void *data, int sign, cudaStream_t st) {
     if (cufftSetStream(h, st) != CUFFT_SUCCESS) return fail(ESN_INTERNAL_ERROR, "cufftSetStream failed");
     // reference FORWARD = e^{+2 pi i lk/n} = CUFFT_INVERSE (fft.py:3-6, 52-59)
     const int dir = sign > 0 ? CUFFT_INVERSE : CUFFT_FORWARD;
@@ -80,6 +72,23 @@ int run_fft(int dim, const int *n, int dtype, int batch, void *data, int sign, c
                         : cufftExecC2C(h, (cufftComplex *)data, (cufftComplex *)data, dir);
     if (r != CUFFT_SUCCESS) return fail(ESN_INTERNAL_ERROR, "cufftExec failed (%d)", (int)r);
     return ESN_SUCCESS;
+}
+
+// plan-less FFT (esn_fft): one handle per (shape, stream)
+int run_fft_cached(int dim, const int *n, int dtype, int batch, void *data, int sign, cudaStream_t st) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    FftKey key{dim, n[0], dim > 1 ? n[1] : 1, dim > 2 ? n[2] : 1, dtype, batch, dev, (uintptr_t)st};
+    std::lock_guard<std::mutex> lk(g_fft_mu);
+    cufftHandle h;
+    auto it = g_fft_cache.find(key);
+    if (it != g_fft_cache.end()) {
+        h = it->second;
+    } else {
+        if (int rc = make_fft_plan(dim, n, dtype, batch, &h)) return rc;
+        g_fft_cache[key] = h;
+    }
+    return exec_fft(h, dtype, data, sign, st);
 }
 }  // namespace
 
@@ -140,7 +149,31 @@ struct esn_plan_s {
     bool capturing = false;
     bool graphs_off = false;  // a capture failed once: run directly from then on
     float last_ms[4] = {0, 0, 0, 0};  // sort, spread, fft, correct
+    // this plan's own cuFFT handle (no work area shared with other plans)
+    cufftHandle fft_h = 0;
+    bool fft_made = false;
 };
+
+// the plan's FFT shape: 2D type 1 with the fused column FFT runs cuFFT along
+// x only (batch ntransf * n2); everything else the full d-dimensional FFT
+static int ensure_fft_plan(esn_plan p) {
+    if (p->fft_made) return ESN_SUCCESS;
+    int rc;
+    if (p->twid && p->type == 1) {
+        const int n1 = p->n[0];
+        rc = make_fft_plan(1, &n1, p->dtype, p->ntransf * p->n[1], &p->fft_h);
+    } else {
+        rc = make_fft_plan(p->dim, p->n, p->dtype, p->ntransf, &p->fft_h);
+    }
+    if (rc) return rc;
+    p->fft_made = true;
+    return ESN_SUCCESS;
+}
+
+static int plan_fft(esn_plan p, void *data, cudaStream_t st) {
+    if (int rc = ensure_fft_plan(p)) return rc;
+    return exec_fft(p->fft_h, p->dtype, data, p->isign, st);
+}
 
 // timing events: inside a graph capture they become EXTERNAL event-record
 // nodes (plain captured records cannot be timed)
@@ -458,6 +491,7 @@ int esn_plan_destroy(esn_plan p) {
     dfree(p->flags);
     if (p->have_events)
         for (int i = 0; i < 8; ++i) cudaEventDestroy(p->ev[i]);
+    if (p->fft_made) cufftDestroy(p->fft_h);
     delete p;
     return ESN_SUCCESS;
 }
@@ -659,6 +693,10 @@ int esn_spreader_create(int dim, const int64_t *nfine, int ntransf, const esn_op
 
 int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const void *y, const void *z) {
     if (!p) return fail(ESN_SIZE_ERROR, "null plan");
+    // an earlier side-stream sort may still be writing the records / key
+    // arrays this call reallocates or rewrites (and a graphed setpts would
+    // not wait for it): order the plan stream after it first
+    if (int jr = join_sort(p)) return jr;
     if (M < 0 || M > INT_MAX) return fail(ESN_SIZE_ERROR, "point count %lld outside [0, 2^31)", (long long)M);
     const void *xs[3] = {x, y, z};
     for (int d = 0; d < p->dim; ++d)
@@ -911,7 +949,7 @@ static int fft_deconv_type1(esn_plan p, void *grid, void *f, cudaStream_t st, cu
     int rc;
     if (p->twid) {
         const int n1 = p->n[0];
-        if ((rc = run_fft(1, &n1, p->dtype, p->ntransf * p->n[1], grid, p->isign, st))) return rc;
+        if ((rc = plan_fft(p, grid, st))) return rc;
         if (ev_mid) ESN_CUDA_TRY(rec_ev(p, ev_mid, st));
         if (p->dtype == ESN_F64)
             return launch_colfft_deconv<double>(p->ntransf, p->n[0], p->n[1], (int)p->N[0], (int)p->N[1],
@@ -921,7 +959,7 @@ static int fft_deconv_type1(esn_plan p, void *grid, void *f, cudaStream_t st, cu
                                            (const float *)grid, (const float *)p->twid, (const float *)p->pk[0],
                                            (const float *)p->pk[1], (float *)f, st);
     }
-    if ((rc = run_fft(p->dim, p->n, p->dtype, p->ntransf, grid, p->isign, st))) return rc;
+    if ((rc = plan_fft(p, grid, st))) return rc;
     if (ev_mid) ESN_CUDA_TRY(rec_ev(p, ev_mid, st));
     if (p->dtype == ESN_F64)
         return launch_deconv<double>(p->dim, p->ntransf, p->n, p->N, (const double *)grid, (const double *)p->pk[0],
@@ -930,14 +968,6 @@ static int fft_deconv_type1(esn_plan p, void *grid, void *f, cudaStream_t st, cu
                                 (const float *)p->pk[1], (const float *)p->pk[2], (float *)f, st);
 }
 
-static int ensure_fft_plan(esn_plan p) {
-    cufftHandle h;
-    if (p->twid && p->type == 1) {
-        const int n1 = p->n[0];
-        return get_fft_plan(1, &n1, p->dtype, p->ntransf * p->n[1], &h);
-    }
-    return get_fft_plan(p->dim, p->n, p->dtype, p->ntransf, &h);
-}
 
 int esn_plan_finish_type1(esn_plan p, void *grid, void *f) {
     if (!p || p->type != 1) return fail(ESN_SIZE_ERROR, "finish_type1 needs a type-1 plan");
@@ -990,7 +1020,7 @@ static int execute_body(esn_plan p, void *c, void *f) {
                                        p->flags + 6, p->st);
         if (rc) return rc;
         if (ev) ESN_CUDA_TRY(rec_ev(p, p->ev[3], p->st));
-        if ((rc = run_fft(p->dim, p->n, p->dtype, p->ntransf, p->grid, p->isign, p->st))) return rc;
+        if ((rc = plan_fft(p, p->grid, p->st))) return rc;
         if (ev) ESN_CUDA_TRY(rec_ev(p, p->ev[4], p->st));
         if ((rc = do_interp(p, p->grid, c))) return rc;
         if (ev) ESN_CUDA_TRY(rec_ev(p, p->ev[5], p->st));
@@ -1118,8 +1148,8 @@ int esn_fft(int dim, int dtype, int ntransf, const int64_t *nfine, void *data, i
         if (nfine[d] < 1 || nfine[d] > INT_MAX) return fail(ESN_SIZE_ERROR, "invalid transform shape");
         n[d] = (int)nfine[d];
     }
-    return run_fft(dim, n, dtype == ESN_F32 ? ESN_F32 : ESN_F64, ntransf < 1 ? 1 : ntransf, data, sign,
-                   (cudaStream_t)stream);
+    return run_fft_cached(dim, n, dtype == ESN_F32 ? ESN_F32 : ESN_F64, ntransf < 1 ? 1 : ntransf, data, sign,
+                          (cudaStream_t)stream);
 }
 
 // ---------------------------------------------------------------------------
@@ -1178,6 +1208,7 @@ static int clone_point_plan(esn_plan main, cudaStream_t st, esn_plan *out) {
 namespace {
 struct HostSlot {
     int type, dim, isign, ntransf, dtype;
+    int device;  // the slot's plan, streams and buffers live on this device
     int64_t N[3];
     double tol, sigma;
     int method;
@@ -1201,6 +1232,9 @@ std::mutex g_host_mu;
 std::vector<HostSlot> g_slots;
 
 void free_slot(HostSlot &s) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != s.device) cudaSetDevice(s.device);
     for (int h = 0; h < HostSlot::NH; ++h) {
         if (s.helper[h]) esn_plan_destroy(s.helper[h]);
         if (s.hst[h]) cudaStreamDestroy(s.hst[h]);
@@ -1220,6 +1254,7 @@ void free_slot(HostSlot &s) {
     dfree(s.dc);
     dfree(s.df);
     if (s.st) cudaStreamDestroy(s.st);
+    if (cur != s.device) cudaSetDevice(cur);
 }
 
 bool is_pinned(const void *ptr) {
@@ -1347,7 +1382,7 @@ static int pipelined(HostSlot *slot, int type, int dim, int64_t M, const double 
                                        (const float *)p->pk[1], (const float *)p->pk[2], (float *)p->grid, p->flags + 6,
                                        st);
         if (rc) return rc;
-        if ((rc = run_fft(p->dim, p->n, p->dtype, p->ntransf, p->grid, p->isign, st))) return rc;
+        if ((rc = plan_fft(p, p->grid, st))) return rc;
     } else {
         ESN_CUDA_TRY(cudaMemsetAsync(p->grid, 0, real_size(p->dtype) * 2 * (size_t)p->G * p->ntransf, st));
     }
@@ -1555,9 +1590,10 @@ int esn_nufft_host(int type, int dim, int64_t M, const double *x, const double *
     std::lock_guard<std::mutex> lk(g_host_mu);
     const bool cacheable = !o.params && !o.coeffs && !o.check_bounds && !o.use_exact_kernel && !o.stream;
     HostSlot *slot = nullptr;
+    const int device = current_device();
     if (cacheable) {
         for (auto &s : g_slots) {
-            bool same = s.type == type && s.dim == dim && s.isign == isign && s.ntransf == ntransf &&
+            bool same = s.device == device && s.type == type && s.dim == dim && s.isign == isign && s.ntransf == ntransf &&
                         s.dtype == dtype && s.tol == tol && s.sigma == o.sigma && s.method == o.method;
             for (int d = 0; d < dim && same; ++d) same = s.N[d] == nmodes[d];
             if (same) {
@@ -1570,7 +1606,7 @@ int esn_nufft_host(int type, int dim, int64_t M, const double *x, const double *
     bool transient = false;
     if (!slot) {
         tmp.type = type; tmp.dim = dim; tmp.isign = isign; tmp.ntransf = ntransf; tmp.dtype = dtype;
-        tmp.tol = tol; tmp.sigma = o.sigma; tmp.method = o.method;
+        tmp.tol = tol; tmp.sigma = o.sigma; tmp.method = o.method; tmp.device = device;
         for (int d = 0; d < 3; ++d) tmp.N[d] = d < dim ? nmodes[d] : 1;
         if (!o.stream) {
             ESN_CUDA_TRY(cudaStreamCreateWithFlags(&tmp.st, cudaStreamNonBlocking));

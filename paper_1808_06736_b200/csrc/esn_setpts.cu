@@ -39,11 +39,15 @@ int fail(int code, const char *fmt, ...) {
 
 const char *last_error() { return g_errbuf; }
 
+int current_device() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    return (dev < 0 || dev >= 64) ? 0 : dev;
+}
+
 int device_sm_count() {
     static int cached[64] = {0};
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
-    if (dev < 0 || dev >= 64) dev = 0;
+    const int dev = current_device();
     if (cached[dev] == 0) {
         int v = 0;
         if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
@@ -410,8 +414,10 @@ static int setpts_impl(const SetptsArgs &a, int nbins, int maxsub, int4 *subprob
         }
         return (int64_t)device_sm_count() * occ;
     };
-    static const int64_t cap_count = (int64_t)device_sm_count() * 8;  // (atomics: oversubscribed is faster)
-    static const int64_t cap_scatter = resident(k_setpts_scatter<XT, DIM>);
+    const int64_t cap_count = (int64_t)device_sm_count() * 8;  // (atomics: oversubscribed is faster)
+    static PerDev<int64_t> cap_scatter_;
+    int64_t &cap_scatter = cap_scatter_();
+    if (cap_scatter == 0) cap_scatter = resident(k_setpts_scatter<XT, DIM>);
     int64_t blocks = (a.M + threads * kILP - 1) / (threads * kILP);
     if (blocks > cap_count) blocks = cap_count;
     if (blocks < 1) blocks = 1;

@@ -9,9 +9,11 @@ SURVEY.md section 8(e):
   of spreading, FFT and the diagonal correction; the mode array is
   sigma^d = 8x smaller than the fine grid); exec_type1_grid_reduced --
   the partial FINE GRIDS are reduced and only the root runs FFT + deconv;
-* batched transforms (config c5) split their TRANSFORMS across ranks: every
-  rank sorts the shared point set itself and runs its slice of strength
-  vectors -- no data-path collective; the slices are gathered at the end;
+* batched transforms (config c5, and batched type 2) split their
+  TRANSFORMS across ranks: every rank sorts the shared point set itself and
+  runs its slice of strength / mode vectors -- no data-path collective; the
+  slices are gathered at the end (exec_type1_transform_sharded,
+  exec_type2_transform_sharded);
 * type 2 and single-GPU configs run as independent replicas (each rank owns
   its own targets; type-2 outputs are independent per point).
 
@@ -111,24 +113,69 @@ def exec_type1_grid_reduced(coords, strengths, num_modes, opts, *, group=None, d
     return finish(state, grid, num_modes, opts)
 
 
-def exec_type1_transform_sharded(coords, strengths_all, num_modes, opts, *, group=None, compute=None):
-    """Batched type 1 (strengths (T, M)) with the T transforms split across
-    ranks; every rank returns the full (T, N_d..N_1) result (all-gather)."""
-    compute = compute or _gpu_type1
-    rank, world = _world(group)
-    T = strengths_all.shape[0]
-    lo, hi = shard_range(T, rank, world)
-    mine = strengths_all[lo:hi]
-    if hi <= lo:
-        raise ValueError(f"rank {rank} has no transforms (T={T} < world={world})")
-    part = compute(coords, mine, num_modes, opts)
-    if world == 1:
-        return part
+def _gather_transform_slices(part, T, rank, world, group, tail_shape, dtype, device):
+    """All-gather per-rank (T_r, ...) slices into the full (T, ...) array.
+    Every rank joins the collective, including ranks whose slice is empty
+    (T < world): they contribute a zero pad, so no rank can block."""
     shapes = [shard_range(T, r, world) for r in range(world)]
     width = max(h - l for l, h in shapes)
-    ref = part if isinstance(part, torch.Tensor) else torch.as_tensor(part)
-    pad = torch.zeros((width,) + tuple(ref.shape[1:]), dtype=ref.dtype, device=ref.device)
-    pad[: ref.shape[0]] = ref
+    pad = torch.zeros((width,) + tuple(tail_shape), dtype=dtype, device=device)
+    if part is not None and part.shape[0]:
+        pad[: part.shape[0]] = part
     slabs = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather([_as_real_view(s) for s in slabs], _as_real_view(pad), group=group)
     return torch.cat([s[: h - l] for s, (l, h) in zip(slabs, shapes)], dim=0)
+
+
+def exec_type1_transform_sharded(coords, strengths_all, num_modes, opts, *, group=None, compute=None):
+    """Batched type 1 (strengths (T, M)) with the T transforms split across
+    ranks; every rank returns the full (T, N_d..N_1) result (all-gather).
+    T and world are the same on every rank, so argument errors are raised
+    on all ranks before any collective; ranks left without a transform
+    (T < world) still join the all-gather with an empty slice."""
+    compute = compute or _gpu_type1
+    rank, world = _world(group)
+    if strengths_all.ndim != 2 or strengths_all.shape[0] < 1:
+        raise ValueError(f"batched strengths must be (T >= 1, M), got {tuple(strengths_all.shape)}")
+    T = strengths_all.shape[0]
+    lo, hi = shard_range(T, rank, world)
+    part = compute(coords, strengths_all[lo:hi], num_modes, opts) if hi > lo else None
+    if world == 1:
+        return part
+    nm = tuple(num_modes) if not isinstance(num_modes, int) else (num_modes,)
+    tail = tuple(reversed(nm))
+    ref = strengths_all if isinstance(strengths_all, torch.Tensor) else torch.as_tensor(strengths_all)
+    part = None if part is None else (part if isinstance(part, torch.Tensor) else torch.as_tensor(part))
+    dtype = part.dtype if part is not None else ref.dtype
+    device = part.device if part is not None else ref.device
+    return _gather_transform_slices(part, T, rank, world, group, tail, dtype, device)
+
+
+def _gpu_type2(coords, modes, opts):
+    from .transforms import exec_type2
+    return exec_type2(coords, modes, opts)[0]
+
+
+def exec_type2_transform_sharded(coords, modes_all, opts, *, group=None, compute=None):
+    """Batched type 2 (mode arrays (T, N_d..N_1)) with the T transforms split
+    across ranks (north_star: batched transforms shard across the GPUs):
+    every rank interpolates its slice at the shared targets -- no
+    data-path collective -- and the (T_r, M) slices are all-gathered, so
+    every rank returns the full (T, M) result."""
+    compute = compute or _gpu_type2
+    rank, world = _world(group)
+    if modes_all.ndim < 2 or modes_all.shape[0] < 1:
+        raise ValueError(f"batched modes must be (T >= 1, N_d..N_1), got {tuple(modes_all.shape)}")
+    T = modes_all.shape[0]
+    M = int(coords[0].shape[0])
+    lo, hi = shard_range(T, rank, world)
+    part = compute(coords, modes_all[lo:hi], opts) if hi > lo else None
+    if world == 1:
+        return part
+    ref = modes_all if isinstance(modes_all, torch.Tensor) else torch.as_tensor(modes_all)
+    part = None if part is None else (part if isinstance(part, torch.Tensor) else torch.as_tensor(part))
+    if part is not None and part.ndim == 1:
+        part = part[None]
+    dtype = part.dtype if part is not None else ref.dtype
+    device = part.device if part is not None else ref.device
+    return _gather_transform_slices(part, T, rank, world, group, (M,), dtype, device)

@@ -32,6 +32,14 @@ def _oracle_compute(coords, c, nm, opts):
     return torch.from_numpy(np.ascontiguousarray(out))
 
 
+def _oracle_compute2(coords, f, opts):
+    import esn_oracle as O
+    f = f.numpy() if isinstance(f, torch.Tensor) else np.asarray(f)
+    cs = [np.asarray(x) for x in coords]
+    out = np.stack([O.exec_type2(cs, fi, tol=opts["tol"], isign=-1) for fi in f])
+    return torch.from_numpy(np.ascontiguousarray(out))
+
+
 def _oracle_spread(coords, c, nm, opts):
     """First half of the oracle's type 1 (esn_oracle.exec_type1 up to the
     spread), returning (grid tensor, state) like spread_type1_grid."""
@@ -63,7 +71,8 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_1808_06736_b200.distributed import (exec_type1_grid_reduced, exec_type1_point_sharded,
-                                                       exec_type1_transform_sharded, shard_range)
+                                                       exec_type1_transform_sharded,
+                                                       exec_type2_transform_sharded, shard_range)
         rng = np.random.default_rng(5)
         M, nm = 3000, (12, 10)
         coords = [rng.uniform(-np.pi, np.pi, M) for _ in range(2)]
@@ -80,8 +89,13 @@ def _worker(rank, world, port, q):
                                         finish=_oracle_finish)
         gall = exec_type1_grid_reduced(mine, c[lo:hi], nm, opts, dst=None, spread=_oracle_spread,
                                        finish=_oracle_finish)
+        # batched type 2: transforms split, (T, M) all-gathered
+        fb = rng.standard_normal((3,) + tuple(reversed(nm))) + 1j * rng.standard_normal((3,) + tuple(reversed(nm)))
+        batched2 = exec_type2_transform_sharded(coords, torch.from_numpy(fb), opts, compute=_oracle_compute2)
+        # T < world: the rank without a transform still joins the gather
+        one = exec_type1_transform_sharded(coords, torch.from_numpy(cb[:1]), nm, opts, compute=_oracle_compute)
         q.put((rank, None if full is None else full.numpy(), allr.numpy(), batched.numpy(),
-               None if gfull is None else gfull.numpy(), gall.numpy()))
+               None if gfull is None else gfull.numpy(), gall.numpy(), batched2.numpy(), one.numpy()))
     finally:
         dist.destroy_process_group()
 
@@ -107,8 +121,8 @@ def test_point_and_transform_sharding_world2(oracle):
         p.start()
     res = {}
     for _ in procs:
-        r, full, allr, batched, gfull, gall = q.get(timeout=300)
-        res[r] = (full, allr, batched, gfull, gall)
+        r, *vals = q.get(timeout=300)
+        res[r] = tuple(vals)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -131,3 +145,8 @@ def test_point_and_transform_sharding_world2(oracle):
     refb = np.stack([O.exec_type1(coords, ci, nm, tol=1e-9) for ci in cb])
     for r in (0, 1):
         np.testing.assert_array_equal(res[r][2], refb)
+        np.testing.assert_array_equal(res[r][6], refb[:1])
+    fb = rng.standard_normal((3,) + tuple(reversed(nm))) + 1j * rng.standard_normal((3,) + tuple(reversed(nm)))
+    refb2 = np.stack([O.exec_type2(coords, fi, tol=1e-9, isign=-1) for fi in fb])
+    for r in (0, 1):
+        np.testing.assert_array_equal(res[r][5], refb2)
