@@ -44,36 +44,48 @@ DISTRIBUTIONS = ("uniform", "disc-quad", "sph-quad")
 
 
 def quad_points(dist: str, m: int, dim: int):
-    """Clustered quadrature point clouds of the paper's benchmark section
-    (esnufft bench.py:100-139 describes them; restated here):
+    """Clustered quadrature point clouds of the paper's benchmark section:
+    the reference's gen_points (esnufft bench.py:100-139) as restated by
+    the product's benchrows.gen_points, bit-identical to the reference
+    (pinned by tests/test_benchrows.py against ref_bench.npz).  disc-quad
+    (2D) / sph-quad (3D); the returned count is close to, not equal to, m."""
+    from paper_1808_06736_b200.benchrows import gen_points
+    if dist not in ("disc-quad", "sph-quad"):
+        raise ValueError(f"unknown distribution {dist!r}")
+    if (dist == "disc-quad") != (dim == 2):
+        raise ValueError(f"{dist} is {'2D' if dist == 'disc-quad' else '3D'}")
+    return list(gen_points(dist, m, dim, 0))
 
-    disc-quad (2D): a polar product grid on the disc of radius pi --
-      round(sqrt(m)) Gauss-Legendre radii on (0, pi) times as many
-      equispaced angles;
-    sph-quad (3D): round(sqrt(m)/2) Gauss-Legendre radial shells on
-      (0, pi), each an (n_lat colatitude midpoints) x (2 n_lat equispaced
-      longitudes) grid with n_lat = round(sqrt(m / (2 n_shells))).
-    The returned count is close to, not equal to, m."""
-    if dist == "disc-quad":
-        if dim != 2:
-            raise ValueError("disc-quad is 2D")
-        k = max(1, round(np.sqrt(m)))
-        r = (np.polynomial.legendre.leggauss(k)[0] + 1.0) * (PI / 2.0)
-        th = 2.0 * PI * np.arange(k) / k
-        rr, tt = np.meshgrid(r, th, indexing="ij")
-        return [(rr * np.cos(tt)).ravel(), (rr * np.sin(tt)).ravel()]
-    if dist == "sph-quad":
-        if dim != 3:
-            raise ValueError("sph-quad is 3D")
-        nr = max(1, round(np.sqrt(m) / 2.0))
-        nlat = max(1, round(np.sqrt(m / (2.0 * nr))))
-        r = (np.polynomial.legendre.leggauss(nr)[0] + 1.0) * (PI / 2.0)
-        colat = PI * (np.arange(nlat) + 0.5) / nlat
-        lon = PI * np.arange(2 * nlat) / nlat
-        rr, cc, ll = np.meshgrid(r, colat, lon, indexing="ij")
-        return [(rr * np.sin(cc) * np.cos(ll)).ravel(), (rr * np.sin(cc) * np.sin(ll)).ravel(),
-                (rr * np.cos(cc)).ravel()]
-    raise ValueError(f"unknown distribution {dist!r}")
+
+# esnufftpy binding fixtures: the reference's make_fixtures.py recipe
+# (bindings/tests/make_fixtures.py:19-60) -- seeds 8800 + 10 type + dim
+BIND_M, BIND_K, BIND_TOL = 300, 200, 1e-9
+BIND_NM = {1: (50,), 2: (12, 10), 3: (6, 5, 4)}
+BIND_ISIGN = {1: 1, 2: -1, 3: 1}
+
+
+def binding_case(ttype: int, dim: int):
+    """Seeded inputs of one binding fixture: dict with coords, isign, tol and
+    c / f / targets / n_modes as the (type, dim) needs."""
+    rng = np.random.default_rng(8800 + 10 * ttype + dim)
+    nm = BIND_NM[dim]
+    out = dict(isign=BIND_ISIGN[dim], tol=BIND_TOL, nm=nm)
+    out["coords"] = [rng.uniform(-np.pi, np.pi, BIND_M) for _ in range(dim)]
+    if ttype == 1:
+        out["c"] = rng.standard_normal(BIND_M) + 1j * rng.standard_normal(BIND_M)
+    elif ttype == 2:
+        n = int(np.prod(nm))
+        out["f"] = (rng.standard_normal(n) + 1j * rng.standard_normal(n)).reshape(tuple(reversed(nm)))
+    else:
+        out["c"] = rng.standard_normal(BIND_M) + 1j * rng.standard_normal(BIND_M)
+        out["targets"] = [rng.uniform(-20.0, 20.0, BIND_K) for _ in range(dim)]
+    return out
+
+
+# reference gen_points pins: (dist, m, dim, seed)
+BENCH_POINT_CASES = [("rand-uniform", 1000, 2, 3), ("rand-uniform", 500, 3, 9), ("disc-quad", 1000, 2, 0),
+                     ("disc-quad", 20000, 2, 5), ("sph-quad", 1000, 3, 0), ("sph-quad", 30000, 3, 1)]
+BENCH_POINT_BIG = [("disc-quad", 10_000_000, 2), ("sph-quad", 10_000_000, 3)]
 
 
 def make_inputs(name: str, M: int | None = None, ntransf: int | None = None, dist: str = "uniform"):

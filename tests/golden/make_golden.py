@@ -171,6 +171,42 @@ def gen_north_star():
     np.savez_compressed(os.path.join(HERE, "ref_northstar.npz"), **out)
 
 
+def gen_bindings():
+    """The reference binding fixtures (bindings/tests/make_fixtures.py
+    recipe, core output at one thread) for the nine esnufftpy routines."""
+    out = {}
+    for tt in (1, 2, 3):
+        for dim in (1, 2, 3):
+            b = cases.binding_case(tt, dim)
+            opts = TransformOptions(tolerance=b["tol"], isign=b["isign"], threads=1)
+            if tt == 1:
+                r = exec_type1(b["coords"], b["c"], b["nm"], opts)[0]
+            elif tt == 2:
+                r = exec_type2(b["coords"], b["f"], opts)[0]
+            else:
+                r = exec_type3(b["coords"], b["c"], b["targets"], opts)[0]
+            out[f"t{tt}d{dim}"] = r
+    np.savez_compressed(os.path.join(HERE, "ref_bindings.npz"), **out)
+
+
+def gen_bench():
+    """The reference's benchmark clouds (esnufft.bench.gen_points): small
+    cases in full, the north-star-sized quadrature clouds as count + sums."""
+    from esnufft.bench import gen_points
+    out = {}
+    for i, (dist, m, dim, seed) in enumerate(cases.BENCH_POINT_CASES):
+        pts = gen_points(dist, m, dim, seed)
+        for d, x in enumerate(pts):
+            out[f"p{i}_{d}"] = np.asarray(x)
+    for i, (dist, m, dim) in enumerate(cases.BENCH_POINT_BIG):
+        pts = gen_points(dist, m, dim, 0)
+        out[f"big{i}_n"] = np.int64(len(pts[0]))
+        out[f"big{i}_sum"] = np.array([np.sum(x) for x in pts])
+        out[f"big{i}_sumsq"] = np.array([np.sum(x * x) for x in pts])
+        out[f"big{i}_sample"] = np.stack([np.asarray(x)[:: max(1, len(x) // 4096)] for x in pts])
+    np.savez_compressed(os.path.join(HERE, "ref_bench.npz"), **out)
+
+
 if __name__ == "__main__":
     print("reference esnufft", esnufft.__version__)
     gen_params()
@@ -178,4 +214,6 @@ if __name__ == "__main__":
     gen_spread()
     gen_transforms()
     gen_north_star()
+    gen_bindings()
+    gen_bench()
     print("ok")

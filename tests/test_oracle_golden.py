@@ -117,3 +117,18 @@ def test_direct_sums_closed_forms(oracle):
     modes = np.zeros(9, complex)
     modes[4] = 1.0
     np.testing.assert_allclose(oracle.direct_type2([x], modes), np.ones(25), atol=1e-15)
+
+
+@pytest.mark.parametrize("tt", (1, 2, 3))
+@pytest.mark.parametrize("dim", (1, 2, 3))
+def test_binding_fixtures_bitwise(oracle, golden, tt, dim):
+    """The esnufftpy binding fixtures (reference make_fixtures.py recipe,
+    regenerated from the reference core by make_golden.gen_bindings)."""
+    b = cases.binding_case(tt, dim)
+    if tt == 1:
+        out = oracle.exec_type1(b["coords"], b["c"], b["nm"], b["tol"], b["isign"])
+    elif tt == 2:
+        out = oracle.exec_type2(b["coords"], b["f"], b["tol"], b["isign"])
+    else:
+        out = oracle.exec_type3(b["coords"], b["c"], b["targets"], b["tol"], b["isign"])
+    np.testing.assert_array_equal(out, golden("bindings")[f"t{tt}d{dim}"])
