@@ -565,6 +565,13 @@ def line_for(args, name, res, world, base):
                 clocks=res["clocks"], gpu_launches=n_launches(cfg) * res["steps"])
     if traffic is not None:
         line["roofline"]["traffic_source"] = "profiles/traffic.json (ncu dram__bytes_read+write of this kernel)"
+        try:  # was it measured on the library being benched? (tools/kernel_table.py)
+            stamp = json.load(open(tp)).get("_so", {}).get(name)
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            import kernel_table
+            line["roofline"]["traffic_same_build"] = stamp == kernel_table.so_sha()
+        except Exception:
+            line["roofline"]["traffic_same_build"] = None
     if "e2e" in res:
         line["e2e"] = res["e2e"]
     return line
