@@ -71,7 +71,8 @@ def hot_kernel_name(cfg):
     if cfg["dim"] == 1:
         return "k_spread_global"
     if cfg["dim"] == 2 and f32 and cfg.get("ntransf", 1) > 1:
-        return "k_spread_batch2d" if os.environ.get("ESN_B2") == "tile" else "k_spread_b2own"
+        b2 = os.environ.get("ESN_B2")
+        return {"tile": "k_spread_batch2d", "own": "k_spread_b2own"}.get(b2, "k_spread_b2roll")
     if cfg["dim"] == 3:
         return "k_spread_rows" if os.environ.get("ESN_SPREAD3") == "rows" else "k_spread_rows3"
     return "k_spread_rows"
@@ -85,7 +86,7 @@ BINDING = {
     "c3": "FP64 pipe (w^3 = 343 DFMA pairs per point), not HBM",
     "c3f": "issue / FP32 pipe, not HBM",
     "c4": "FP64 pipe (w^3 = 1000 DFMA pairs per point), not HBM",
-    "c5": "issue (per-point dispatch + staging), DRAM traffic = the algorithmic bytes",
+    "c5": "issue (~80 instructions per point-strip visit, 45 % issue efficiency), DRAM ~ algorithmic bytes",
 }
 
 

@@ -151,6 +151,21 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *g) {
                  "l"(g)
                  : "memory");
 }
+// the same with an L2 eviction-policy hint (createpolicy): records that
+// stream through once go evict-first, gathered strengths evict-last so the
+// other values of each 32-byte sector are still in L2 when their points come
+__device__ __forceinline__ void cp_async16_hint(void *smem, const void *g, uint64_t pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+                 "l"(g), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async8_hint(void *smem, const void *g, uint64_t pol) {
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+                 "l"(g), "l"(pol)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -534,6 +549,9 @@ __global__ void __launch_bounds__(Rows3Cfg<T, W>::NT, Rows3Cfg<T, W>::MINB) k_sp
     const int n1 = a.g.n[0], n2 = a.g.n[1], n3 = a.g.n[2];
     const int nsub = *a.nsub;
     unsigned *mylist = s_list + warp * CH;
+    uint64_t pol_first, pol_last;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
     for (;;) {
         if (tid == 0) s_sub = atomicAdd(a.work, 1);
         __syncthreads();
@@ -557,8 +575,9 @@ __global__ void __launch_bounds__(Rows3Cfg<T, W>::NT, Rows3Cfg<T, W>::MINB) k_sp
                 if (pt < nch_of(ci)) {
                     const Rec *src = a.rec + start + ci * CH + pt;
                     Rec *dst = s_ring + (st & 1) * CH + pt;
-                    cp_async16(dst, src);
-                    cp_async16(reinterpret_cast<char *>(dst) + 16, reinterpret_cast<const char *>(src) + 16);
+                    cp_async16_hint(dst, src, pol_first);
+                    cp_async16_hint(reinterpret_cast<char *>(dst) + 16, reinterpret_cast<const char *>(src) + 16,
+                                    pol_first);
                 }
             }
             cp_async_commit();
@@ -570,12 +589,9 @@ __global__ void __launch_bounds__(Rows3Cfg<T, W>::NT, Rows3Cfg<T, W>::MINB) k_sp
                     const int j = s_ring[(st & 1) * CH + pt].j;
                     const C *src = reinterpret_cast<const C *>(a.c) + (int64_t)t * a.M + j;
                     if constexpr (sizeof(C) == 16) {
-                        cp_async16(s_c + pt, src);
+                        cp_async16_hint(s_c + pt, src, pol_last);
                     } else {
-                        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                                         static_cast<uint32_t>(__cvta_generic_to_shared(s_c + pt))),
-                                     "l"(src)
-                                     : "memory");
+                        cp_async8_hint(s_c + pt, src, pol_last);
                     }
                 }
             }
@@ -1503,6 +1519,301 @@ __device__ __forceinline__ void st_keep(double2 *p, double2 v, uint64_t policy) 
 __device__ __forceinline__ void st_keep(float2 *p, float2 v, uint64_t policy) {
     asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(p), "f"(v.x), "f"(v.y), "l"(policy)
                  : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Batched 2D spreader, y-rolling owner-computes (ntransf > 1, float32): lanes
+// are transforms.  A warp item is (strip of kRollBX owned columns, segment of
+// kRollSeg owned rows, 32-transform group).  It walks the ORIGIN rows
+// y0 - (w - 1) .. y0 + SEG - 1 in order; the points of one origin row whose
+// origin column lies in [x0 - (w - 1), x0 + BX) come from <= 3 contiguous
+// key ranges (the window crosses at most one bin edge and the wrap), listed
+// once per item.  They are staged in pieces of kRollNB points (kernel rows
+// + the group's 32 strengths, cp.async.bulk on an mbarrier, one piece
+// ahead, pieces spanning rows) and each adds its w x w footprint into a ring
+// of w output rows held in registers (acc[dy][col], owned columns only, one
+// static dispatch per point on the origin column).  When the origin row
+// advances past row y, row y is complete: its owned cells are stored once
+// (no memset, no atomics) and the ring shifts.  Per point this is one warp
+// visit per strip it reaches (1 + (w - 1) / BX) and (SEG + w - 1) / SEG row
+// passes, against w / 2 + 1 item visits of k_spread_b2own.  Same sort keys
+// and scratch as k_spread_b2own (cell-resolution keys over 16 x 16 bins,
+// cperm, tab).  Reference: spreadinterp.py:354-368 (_spread_sub_2d), one
+// pass per transform there (bench.py c5 runs 64 single transforms).
+constexpr int kRollBX = 8;    // owned columns per strip
+constexpr int kRollSeg = 32;  // owned rows per segment
+constexpr int kRollNB = 16;   // staged points per piece
+template <int W>
+struct RollCfg {
+    static constexpr int R = kRollSeg + W - 1;  // origin rows per item
+    static constexpr int NC = kRollBX + W - 1;  // window cells per row
+    static constexpr int RUNS = 4;              // run slots per row (<= 3 used)
+    static constexpr uint32_t I1OFF = 2 * W * sizeof(float);  // PtRows2<W>::i1
+    static constexpr size_t STAGE = (size_t)kRollNB * (sizeof(PtRows2<W>) + 32 * sizeof(float2));
+    static constexpr size_t TABLE = (size_t)R * RUNS * 2 * sizeof(int) + (size_t)R * sizeof(int);
+    static constexpr size_t WARP = 2 * STAGE + (TABLE + 127) / 128 * 128;
+    static_assert((size_t)R * NC * 2 * sizeof(int) <= 2 * STAGE, "key ranges alias the stages");
+};
+template <int W>
+constexpr size_t b2roll_smem_bytes() { return 4 * RollCfg<W>::WARP; }
+__device__ __forceinline__ int lds_s32(uint32_t a) {
+    int v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float2 lds_f2(uint32_t a) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+// r1[W], r2[W] of one staged PtRows2<W> (16-byte aligned, 16-byte vectors)
+template <int W>
+__device__ __forceinline__ void lds_rows(uint32_t a, float *r1, float *r2) {
+    constexpr int NV = (2 * W + 3) / 4;
+    static_assert(NV * 16 <= (int)sizeof(PtRows2<W>), "vector loads stay inside the entry");
+    float f[NV * 4];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+        const float4 q = lds_f4(a + 16 * i);
+        f[4 * i] = q.x;
+        f[4 * i + 1] = q.y;
+        f[4 * i + 2] = q.z;
+        f[4 * i + 3] = q.w;
+    }
+#pragma unroll
+    for (int m = 0; m < W; ++m) {
+        r1[m] = f[m];
+        r2[m] = f[W + m];
+    }
+}
+// grids this kernel handles: the window of one strip / segment must not wrap
+// onto itself
+template <int W>
+__host__ __device__ inline bool b2roll_fits(int n1, int n2) { return n1 >= kRollBX + W - 1 && n2 >= kRollSeg + W - 1; }
+
+template <typename T, int W>
+__global__ void __launch_bounds__(128, 3) k_spread_b2roll(SpreadArgs<T> a, const T *cperm, const PtRows2<W> *tab) {
+    static_assert(sizeof(T) == 4, "float32 plans");
+    using C = typename Cx<T>::type;
+    using Cfg = RollCfg<W>;
+    constexpr int BXS = kRollBX, NB = kRollNB, H = W - 1, NC = Cfg::NC, R = Cfg::R, RUNS = Cfg::RUNS;
+    constexpr uint32_t TB = sizeof(PtRows2<W>), CB = 32 * sizeof(C);
+    constexpr size_t STAGE = Cfg::STAGE;
+    static_assert(NC <= 32, "one lane per window column");
+    static_assert(TB % 16 == 0 && CB % 16 == 0, "bulk copies move 16-byte multiples");
+    extern __shared__ __align__(128) unsigned char roll_smem[];
+    __shared__ uint64_t s_bar[4][2];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned char *wbase = roll_smem + wid * Cfg::WARP;
+    int *run_src = reinterpret_cast<int *>(wbase + 2 * STAGE);  // [R * RUNS]
+    int *run_end = run_src + R * RUNS;                            // [R * RUNS]
+    int *rowend = run_end + R * RUNS;                             // [R] slots through row r
+    int *se = reinterpret_cast<int *>(wbase);                     // [R][NC][2] (item setup only)
+    uint64_t *bar = s_bar[wid];
+    if (lane == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    const int n1 = a.g.n[0], n2 = a.g.n[1], nb0 = a.g.nb[0];
+    // bins are 16 x 16 cells on this path (batched_owner checks bs)
+    constexpr int bx = Batch2Cfg<float, W>::BX, by = Batch2Cfg<float, W>::BY;
+    const int ngroups = (a.ntransf + 31) / 32;
+    const int nstrips = (n1 + BXS - 1) / BXS, nsegs = (n2 + kRollSeg - 1) / kRollSeg;
+    const int nitems = nstrips * nsegs * ngroups;
+    uint32_t par0 = 0, par1 = 0;  // mbarrier phase parity per buffer
+    int next = 0;
+    if (lane == 0) next = atomicAdd(a.work, 1);
+    for (;;) {
+        const int item = __shfl_sync(0xffffffffu, next, 0);
+        if (item >= nitems) break;
+        if (lane == 0) next = atomicAdd(a.work, 1);
+        const int tg = item % ngroups;
+        const int sid = item / ngroups;
+        const int strip = sid % nstrips, seg = sid / nstrips;
+        const int x0 = strip * BXS, y0 = seg * kRollSeg;
+        const int yend = min(y0 + kRollSeg, n2);  // owned rows y0 .. yend - 1
+        const int nrows = yend - (y0 - H);         // origin rows of this item (<= R)
+        int xb = x0 - H;
+        while (xb < 0) xb += n1;  // window column k: (xb + k) mod n1
+        int yb = y0 - H;
+        while (yb < 0) yb += n2;
+        // item setup 1: key range [s, e) of every (origin row, window cell),
+        // all loads in flight at once
+        for (int p = lane; p < nrows * NC; p += 32) {
+            const int r = p / NC, k = p - r * NC;
+            int yr = yb + r, xr = xb + k;
+            if (yr >= n2) yr -= n2;
+            if (xr >= n1) xr -= n1;
+            const int key = (((yr / by) * nb0 + xr / bx) * by + (yr % by)) * bx + (xr % bx);
+            se[2 * p] = a.kstart[key];
+            se[2 * p + 1] = a.kstart[key + 1];
+        }
+        __syncwarp();
+        // item setup 2: per row, its contiguous runs and the running slot count
+        int tot = 0;
+        for (int r = 0; r < nrows; ++r) {
+            int s = 0, e = 0;
+            if (lane < NC) {
+                s = se[2 * (r * NC + lane)];
+                e = se[2 * (r * NC + lane) + 1];
+            }
+            const int eprev = __shfl_up_sync(0xffffffffu, e, 1);
+            const bool start = lane < NC && (lane == 0 || s != eprev);
+            const unsigned smask = __ballot_sync(0xffffffffu, start);
+            const bool last = lane < NC && (lane == NC - 1 || ((smask >> (lane + 1)) & 1u));
+            const int idx = __popc(smask & ((2u << lane) - 1u)) - 1;  // run of this lane
+            if (start && idx < RUNS) run_src[r * RUNS + idx] = s;
+            if (last && idx < RUNS) run_end[r * RUNS + idx] = e;
+            int cnt = lane < NC ? e - s : 0;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+            const int nr = __popc(smask);
+            if (lane < RUNS && lane >= nr) {  // unused run slots are empty
+                run_src[r * RUNS + lane] = 0;
+                run_end[r * RUNS + lane] = 0;
+            }
+            tot += cnt;
+            if (lane == 0) rowend[r] = tot;
+        }
+        __syncwarp();
+        const C *cg = reinterpret_cast<const C *>(cperm) + (int64_t)tg * a.M * 32;
+        // producer state (lane 0): run pr (flat over rows), offset po in it
+        int pr = 0, po = 0, issued = 0;
+        auto issue = [&](int buf) -> int {  // next piece of up to NB slots into buf
+            const int n = min(NB, tot - issued);
+            if (lane == 0) {
+                unsigned char *dst = wbase + buf * STAGE;
+                mbar_expect_tx(&bar[buf], (uint32_t)n * (TB + CB));
+                int slot = 0;
+                while (slot < n) {
+                    const int s0 = run_src[pr], len = run_end[pr] - s0 - po;
+                    const int take = min(len, n - slot);
+                    if (take > 0) {
+                        const int src = s0 + po;
+                        bulk_g2s(dst + slot * TB, tab + src, (uint32_t)take * TB, &bar[buf]);
+                        bulk_g2s(dst + NB * TB + slot * CB, cg + (int64_t)src * 32, (uint32_t)take * CB, &bar[buf]);
+                        slot += take;
+                        po += take;
+                    }
+                    if (po >= run_end[pr] - s0) {
+                        ++pr;
+                        po = 0;
+                    }
+                }
+            }
+            issued += n;
+            return n;
+        };
+        C acc[W][BXS];
+#pragma unroll
+        for (int r = 0; r < W; ++r)
+#pragma unroll
+            for (int x = 0; x < BXS; ++x) acc[r][x] = C{(T)0, (T)0};
+        const bool vec = (n1 % 2) == 0 && x0 + BXS <= n1;
+        const int t = tg * 32 + lane;
+        int ycur = y0 - H;    // origin row of the next slot
+        int rnext = rowend[0];  // slots through row ycur
+        int rr = 0;
+        // origin row ycur done: output row ycur is complete -> store, shift
+        auto advance_row = [&]() {
+            if (ycur >= y0 && t < a.ntransf) {
+                C *dst = reinterpret_cast<C *>(a.grid) + (int64_t)t * a.gstride + (int64_t)ycur * n1 + x0;
+                if (a.accumulate) {
+#pragma unroll
+                    for (int x = 0; x < BXS; ++x)
+                        if (x0 + x < n1 && (acc[0][x].x != (T)0 || acc[0][x].y != (T)0)) red_add(dst + x, acc[0][x]);
+                } else if (vec) {
+#pragma unroll
+                    for (int x = 0; x < BXS; x += 2)
+                        *reinterpret_cast<float4 *>(dst + x) = make_float4(acc[0][x].x, acc[0][x].y, acc[0][x + 1].x,
+                                                                           acc[0][x + 1].y);
+                } else {
+#pragma unroll
+                    for (int x = 0; x < BXS; ++x)
+                        if (x0 + x < n1) dst[x] = acc[0][x];
+                }
+            }
+#pragma unroll
+            for (int r = 0; r + 1 < W; ++r)
+#pragma unroll
+                for (int x = 0; x < BXS; ++x) acc[r][x] = acc[r + 1][x];
+#pragma unroll
+            for (int x = 0; x < BXS; ++x) acc[W - 1][x] = C{(T)0, (T)0};
+            ++ycur;
+            ++rr;
+            rnext = rr < nrows ? rowend[rr] : 0x7fffffff;
+        };
+        int q = 0, buf = 0;
+        int cn = tot > 0 ? issue(0) : 0;
+        while (cn > 0) {
+            const int nn = issued < tot ? issue(buf ^ 1) : 0;  // the other buffer's reader is done
+            mbar_wait(&bar[buf], buf ? par1 : par0);
+            if (buf) par1 ^= 1u; else par0 ^= 1u;
+            // 32-bit shared addresses (explicit ld.shared): one register per
+            // pointer, nothing for the compiler to re-derive inside the loop
+            const uint32_t sb = smem_u32(wbase) + (uint32_t)(buf * STAGE);
+            const uint32_t cb = sb + NB * TB + lane * (uint32_t)sizeof(C);
+            // the piece in same-row segments: the hot loop carries no row logic
+            for (int k0 = 0; k0 < cn;) {
+                while (q >= rnext) advance_row();
+                const int k1 = min(cn, k0 + (rnext - q));
+                q += k1 - k0;
+                // the origin column of the next point is loaded one point ahead,
+                // so the dispatch of point k resolves while its rows load
+                int i1n = lds_s32(sb + k0 * TB + Cfg::I1OFF);
+#pragma unroll 1
+            for (int k = k0; k < k1; ++k) {
+                const int i1 = i1n;
+                if (k + 1 < k1) i1n = lds_s32(sb + (k + 1) * TB + Cfg::I1OFF);
+                T r1[W], r2[W];
+                lds_rows<W>(sb + k * TB, r1, r2);
+                const float2 cc = lds_f2(cb + k * CB);
+                C v[W];
+#pragma unroll
+                for (int dy = 0; dy < W; ++dy) v[dy] = C{cc.x * r2[dy], cc.y * r2[dy]};
+                int cs = i1 - xb;
+                if (cs < 0) cs += n1;
+#define ESN_ROLL_CASE(CS)                                                                 \
+    case CS:                                                                              \
+        if constexpr (CS < NC) {                                                          \
+            _Pragma("unroll") for (int m = 0; m < W; ++m) {                               \
+                constexpr int XL = CS - H;                                                \
+                if (XL + m >= 0 && XL + m < BXS) {                                        \
+                    _Pragma("unroll") for (int dy = 0; dy < W; ++dy) {                    \
+                        acc[dy][XL + m].x = fma(v[dy].x, r1[m], acc[dy][XL + m].x);       \
+                        acc[dy][XL + m].y = fma(v[dy].y, r1[m], acc[dy][XL + m].y);       \
+                    }                                                                     \
+                }                                                                         \
+            }                                                                             \
+        }                                                                                 \
+        break;
+                switch (cs) {
+                    ESN_ROLL_CASE(0) ESN_ROLL_CASE(1) ESN_ROLL_CASE(2) ESN_ROLL_CASE(3)
+                    ESN_ROLL_CASE(4) ESN_ROLL_CASE(5) ESN_ROLL_CASE(6) ESN_ROLL_CASE(7)
+                    ESN_ROLL_CASE(8) ESN_ROLL_CASE(9) ESN_ROLL_CASE(10) ESN_ROLL_CASE(11)
+                    ESN_ROLL_CASE(12) ESN_ROLL_CASE(13) ESN_ROLL_CASE(14) ESN_ROLL_CASE(15)
+                    ESN_ROLL_CASE(16) ESN_ROLL_CASE(17)
+                    default:
+                        break;
+                }
+#undef ESN_ROLL_CASE
+            }
+                k0 = k1;
+            }
+            __syncwarp();
+            buf ^= 1;
+            cn = nn;
+        }
+        while (rr < nrows) advance_row();  // trailing rows (and items with no points)
+        __syncwarp();  // setup of the next item overwrites the stages and tables
+    }
 }
 
 // One unit of interpolation work: a slice of one subproblem's point records.

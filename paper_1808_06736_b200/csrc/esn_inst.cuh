@@ -114,7 +114,24 @@ struct SpreadBatchOp {
             k_rows2d<T, W><<<grid_for(a.M, 256), 256, 0, st>>>(a, tab);
             constexpr size_t smem = batch2d_smem_bytes<T, W>();
             // cell-resolution sort keys -> static x-offset sweep; else per-point dispatch
-            if (batched_owner(ESN_F32, 2, W, a.ntransf, ESN_METHOD_TILE, a.sbl, a.g.bs)) {
+            bool rolled = false;
+            // y-rolling owner-computes for w <= 6 (the w x 8 register ring fits 128 registers)
+            if constexpr (W <= 6) {
+                if (batched_owner(ESN_F32, 2, W, a.ntransf, ESN_METHOD_TILE, a.sbl, a.g.bs) &&
+                    b2roll_fits<W>(a.g.n[0], a.g.n[1]) && !batched_roll_off()) {
+                    constexpr size_t rsmem = b2roll_smem_bytes<W>();
+                    static PerDev<int> grid_;
+                    int &grid = grid_();
+                    if (grid == 0) {
+                        int rc = persistent_launch(k_spread_b2roll<T, W>, 128, rsmem, st, nullptr, &grid);
+                        if (rc) return rc;
+                    }
+                    k_spread_b2roll<T, W><<<grid, 128, rsmem, st>>>(a, cperm, tab);
+                    rolled = true;
+                }
+            }
+            if (rolled) {
+            } else if (batched_owner(ESN_F32, 2, W, a.ntransf, ESN_METHOD_TILE, a.sbl, a.g.bs)) {
                 constexpr size_t osmem = b2own_smem_bytes<T, W>();
                 static PerDev<int> grid_;
                 int &grid = grid_();

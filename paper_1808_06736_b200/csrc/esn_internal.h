@@ -150,6 +150,7 @@ bool batched_spread(int dtype, int dim, int w, int ntransf, int method);
 // does the batched 2D owner-computes spreader (writes every fine cell, no
 // memset needed) apply?  Needs cell-resolution keys over 16 x 16 bins.
 bool batched_owner(int dtype, int dim, int w, int ntransf, int method, const int *sbl, const int *bs);
+bool batched_roll_off();
 template <typename T>
 int launch_interp(const SpreadArgs<T> &a, T *cout, const T *grid, cudaStream_t st);
 // per-(dtype, dim, width part) instantiations, one translation unit each

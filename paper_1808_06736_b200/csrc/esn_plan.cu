@@ -866,6 +866,16 @@ bool esn::batched_spread(int dtype, int dim, int w, int ntransf, int method) {
     return method != ESN_METHOD_GLOBAL && dim == 2 && dtype == ESN_F32 && ntransf > 1 && w <= 10;
 }
 
+// ESN_B2=own: the per-item owner-computes kernel (k_spread_b2own) instead of
+// the y-rolling one (k_spread_b2roll)
+bool esn::batched_roll_off() {
+    static const bool off = [] {
+        const char *e = getenv("ESN_B2");
+        return e && std::string(e) == "own";
+    }();
+    return off;
+}
+
 bool esn::batched_owner(int dtype, int dim, int w, int ntransf, int method, const int *sbl, const int *bs) {
     static const bool off = [] {
         const char *e = getenv("ESN_B2");

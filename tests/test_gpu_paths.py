@@ -132,11 +132,14 @@ def test_spread_then_finish_equals_type1(esn, dim, nm, T):
     ((13, 9), 3, 4000, False),      # fine grid narrower than one 16 x 16 block: wrapped halo cells
     ((37, 21), 33, 20_000, False),  # partial last blocks in x and y, a partial second transform group
     ((64, 48), 4, 60_000, True),    # clustered: hundreds of points per cell, many pieces per source row
+    ((200, 150), 64, 80_000, False),  # two full transform groups, many strips / segments
 ])
 def test_batched_owner_spreader(esn, oracle, nm, T, m, clustered):
-    """float32 batched 2D type 1 goes through the owner-computes spreader
-    (k_spread_b2own: every fine cell written once by its block's warp); the
-    single transforms go through the row spreader, an independent kernel."""
+    """float32 batched 2D type 1 goes through an owner-computes spreader
+    (every fine cell written once by its owner warp: k_spread_b2roll, the
+    y-rolling strip kernel, when the fine grid is at least 8 + w - 1 by
+    32 + w - 1 cells and w <= 6, else k_spread_b2own -- the (13, 9) case);
+    the single transforms go through the row spreader, an independent kernel."""
     rng = np.random.default_rng(11)
     lo, hi = (-np.pi, -np.pi + 0.3) if clustered else (-np.pi, np.pi)
     coords = [rng.uniform(lo, hi, m).astype(np.float32) for _ in range(2)]
