@@ -179,6 +179,10 @@ int esn_plan_hot_kernel_seconds(esn_plan p, double *seconds);
 int esn_plan_info(esn_plan p, int64_t *nfine, esn_kernel_params *kp);
 /* Bin geometry of a plan: total bins, bin size and bins per dimension. */
 int esn_plan_bins(esn_plan p, int *nbins, int *bin_size, int *bins_per_dim);
+/* Work items (subproblems) of the last sort, the spread / interp kernels'
+ * unit of dynamic scheduling (the tasks count of spreadinterp.py:165-184).
+ * Waits for the plan stream. */
+int esn_plan_tasks(esn_plan p, int64_t *ntasks);
 /* Copy the plan's bin sort into caller device buffers (any may be NULL):
  * perm (M int32, sorted slot -> original index), keys (M int32, bin of each
  * original point), bin_start (nbins + 1 int32).  Replaces the
@@ -217,6 +221,19 @@ int esn_fftshift(int dim, const int64_t *n, const void *in, void *out, void *str
 
 int esn_fft(int dim, int dtype, int ntransf, const int64_t *nfine,
             void *data, int sign, void *stream);
+
+/* Explicit FFT plans: replace fft.py:79-84 (_build_plan), :87-96 (get_plan)
+ * and :99-106 (clear_plan_cache).  One cuFFT handle and work area per plan;
+ * executions of one plan are serialised (one stream at a time).  sign = +1
+ * is the reference FORWARD (e^{+2 pi i lk/n}), -1 BACKWARD; in place,
+ * unnormalised, (ntransf, n_d..n_1) C order. */
+typedef struct esn_fft_plan_s *esn_fft_plan;
+int esn_fft_plan_create(int dim, int dtype, int ntransf, const int64_t *nfine, esn_fft_plan *out);
+int esn_fft_plan_exec(esn_fft_plan plan, void *data, int sign, void *stream);
+int64_t esn_fft_plan_work_bytes(esn_fft_plan plan);
+int esn_fft_plan_destroy(esn_fft_plan plan);
+/* drop the handles esn_fft caches per (shape, dtype, batch, device, stream) */
+int esn_fft_cache_clear(void);
 
 /* fold_coords + grid scaling (grid.py:152-168, spreadinterp.py:90-101) on
  * device: g[i] = (x[i] mod 2 pi) * n / 2 pi in [0, n), float64 output,

@@ -69,8 +69,14 @@ SIGNATURES = {
     "esn_plan_finish_type1": (i32, [vp, vp, vp]),
     "esn_plan_target_chunks": (i32, [vp, vp]),
     "esn_plan_bins": (i32, [vp, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)]),
+    "esn_plan_tasks": (i32, [vp, P_i64]),
     "esn_fold_coords": (i32, [i64, i32, vp, i64, vp, vp]),
     "esn_fft": (i32, [i32, i32, i32, P_i64, vp, i32, vp]),
+    "esn_fft_plan_create": (i32, [i32, i32, i32, P_i64, ctypes.POINTER(vp)]),
+    "esn_fft_plan_exec": (i32, [vp, vp, i32, vp]),
+    "esn_fft_plan_work_bytes": (i64, [vp]),
+    "esn_fft_plan_destroy": (i32, [vp]),
+    "esn_fft_cache_clear": (i32, []),
     "esn_type3_prephase": (i32, [i32, i64, vp, vp, vp, P_dbl, P_dbl, P_dbl, i32, vp, vp, vp, vp, vp, vp]),
     "esn_type3_targets": (i32, [i32, i64, vp, vp, vp, P_dbl, P_dbl, P_i64, vp, vp, vp, vp]),
     "esn_type3_correct": (i32, [i32, i64, vp, vp, vp, P_dbl, P_dbl, P_dbl, P_i64,

@@ -1131,6 +1131,21 @@ int esn_plan_bins(esn_plan p, int *nbins, int *bin_size, int *bins_per_dim) {
     return ESN_SUCCESS;
 }
 
+// spreadinterp.py:165-184 (_run_tasks stats): the work items of the last
+// sort -- subproblems, the spread / interp kernels' unit of dynamic
+// scheduling -- read back after the plan stream drains
+int esn_plan_tasks(esn_plan p, int64_t *ntasks) {
+    if (!p || !p->points_set) return fail(ESN_SIZE_ERROR, "plan has no points");
+    if (int jr = join_sort(p)) return jr;
+    int v = 0;
+    if (p->nsub) {
+        ESN_CUDA_TRY(cudaMemcpyAsync(&v, p->nsub, sizeof(int), cudaMemcpyDeviceToHost, p->st));
+        ESN_CUDA_TRY(cudaStreamSynchronize(p->st));
+    }
+    if (ntasks) *ntasks = v;
+    return ESN_SUCCESS;
+}
+
 int esn_plan_sort_view(esn_plan p, void *perm, void *keys, void *bin_start) {
     if (!p || !p->points_set) return fail(ESN_SIZE_ERROR, "plan has no points");
     if (p->nchunk > 1) return fail(ESN_SIZE_ERROR, "sort view needs a spreader plan (this plan's order is target-chunked)");
@@ -1150,6 +1165,73 @@ int esn_plan_target_chunks(esn_plan p, int *nchunk) {
 }
 
 int64_t esn_plan_device_bytes(esn_plan p) { return p ? p->device_bytes : 0; }
+
+// Explicit cuFFT plans (fft.py:79-111 _build_plan / get_plan / clear_plan_cache):
+// one handle and work area per plan; executions of one plan are serialised
+// by its mutex (SetStream + Exec), so callers that run one plan from two
+// streams at once must use two plans.
+struct esn_fft_plan_s {
+    int dim = 1, dtype = ESN_F64, batch = 1, device = 0;
+    int n[3] = {1, 1, 1};
+    cufftHandle h = 0;
+    size_t work = 0;
+    std::mutex mu;
+};
+
+int esn_fft_plan_create(int dim, int dtype, int ntransf, const int64_t *nfine, esn_fft_plan *out) {
+    if (!out) return fail(ESN_SIZE_ERROR, "null plan pointer");
+    *out = nullptr;
+    if (dim < 1 || dim > 3) return fail(ESN_SIZE_ERROR, "dimension must be 1, 2, or 3");
+    auto *p = new (std::nothrow) esn_fft_plan_s;
+    if (!p) return fail(ESN_RESOURCE_ERROR, "out of host memory");
+    p->dim = dim;
+    p->dtype = dtype == ESN_F32 ? ESN_F32 : ESN_F64;
+    p->batch = ntransf < 1 ? 1 : ntransf;
+    cudaGetDevice(&p->device);
+    for (int d = 0; d < dim; ++d) {
+        if (nfine[d] < 1 || nfine[d] > INT_MAX) {
+            delete p;
+            return fail(ESN_SIZE_ERROR, "invalid transform shape");
+        }
+        p->n[d] = (int)nfine[d];
+    }
+    if (int rc = make_fft_plan(dim, p->n, p->dtype, p->batch, &p->h)) {
+        delete p;
+        return rc;
+    }
+    cufftGetSize(p->h, &p->work);
+    *out = p;
+    return ESN_SUCCESS;
+}
+
+int esn_fft_plan_exec(esn_fft_plan p, void *data, int sign, void *stream) {
+    if (!p) return fail(ESN_SIZE_ERROR, "null plan");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != p->device) return fail(ESN_SIZE_ERROR, "FFT plan made on device %d, current device %d", p->device, dev);
+    std::lock_guard<std::mutex> lk(p->mu);
+    return exec_fft(p->h, p->dtype, data, sign, (cudaStream_t)stream);
+}
+
+int64_t esn_fft_plan_work_bytes(esn_fft_plan p) { return p ? (int64_t)p->work : 0; }
+
+int esn_fft_plan_destroy(esn_fft_plan p) {
+    if (!p) return ESN_SUCCESS;
+    {
+        std::lock_guard<std::mutex> lk(p->mu);
+        if (p->h) cufftDestroy(p->h);
+    }
+    delete p;
+    return ESN_SUCCESS;
+}
+
+// drops the plan-less esn_fft handles (fft.py:101-106 clear_plan_cache(None))
+int esn_fft_cache_clear(void) {
+    std::lock_guard<std::mutex> lk(g_fft_mu);
+    for (auto &kv : g_fft_cache) cufftDestroy(kv.second);
+    g_fft_cache.clear();
+    return ESN_SUCCESS;
+}
 
 int esn_fft(int dim, int dtype, int ntransf, const int64_t *nfine, void *data, int sign, void *stream) {
     if (dim < 1 || dim > 3) return fail(ESN_SIZE_ERROR, "dimension must be 1, 2, or 3");

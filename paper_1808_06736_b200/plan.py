@@ -160,6 +160,12 @@ class Plan:
         _lib.check(_lib.lib.esn_plan_hot_kernel_seconds(self.h, ctypes.byref(v)))
         return v.value
 
+    def tasks(self) -> int:
+        """Subproblems of the last sort (the kernels' scheduling units)."""
+        v = ctypes.c_int64()
+        _lib.check(_lib.lib.esn_plan_tasks(self.h, ctypes.byref(v)))
+        return int(v.value)
+
     def bins(self):
         nb = ctypes.c_int()
         bs = (ctypes.c_int * 3)()

@@ -60,6 +60,20 @@ def ensure_sorted(points: NuPointSet, threads: int = 1) -> NuPointSet:
     return points
 
 
+def _fill_stats(stats: dict, p: Plan, kw: dict) -> None:
+    """spreadinterp.py:165-184: ``busy_per_thread`` (seconds per worker) and
+    ``tasks`` (work items).  On the GPU the worker is the device stream the
+    plan runs on (key 0; its busy time is the spread / interp kernel's
+    CUDA-event time) and the tasks are the sort's subproblems, which the
+    persistent kernels claim dynamically.  Stage times (sort / spread / fft /
+    correct) are added as well."""
+    timed = kw.get("timing", True)
+    stats["busy_per_thread"] = {0: p.hot_kernel_seconds() if timed else 0.0}
+    stats["tasks"] = p.tasks()
+    if timed:
+        stats.update(p.stage_times())
+
+
 def _spreader(points: NuPointSet, params: KernelParams, use_exact: bool, ntransf: int, **kw):
     p = Plan(0, points.dim, nfine=points.sizes, ntransf=ntransf, params=params,
              use_exact_kernel=use_exact, check_bounds=points.check_bounds, sigma=params.sigma,
@@ -89,7 +103,7 @@ def spread(points: NuPointSet, strengths, params: KernelParams, threads: int = 1
     if st:
         raise_data_error(st, idx, d, points.coords, "strength")
     if stats is not None:
-        stats.update(p.stage_times() if kw.get("timing", True) else {})
+        _fill_stats(stats, p, kw)
     p.close()
     return D.to_output(grid, like_torch)
 
@@ -115,5 +129,7 @@ def interp(points: NuPointSet, grid, params: KernelParams, threads: int = 1,
     st, idx, d = p.check_info()
     if st:
         raise_data_error(st, idx, d, points.coords)
+    if stats is not None:
+        _fill_stats(stats, p, kw)
     p.close()
     return D.to_output(out, like_torch)

@@ -437,4 +437,7 @@ def nufft3d3(x, y, z, c, s, t, u, **kw):
 
 
 def clear_plan_cache() -> None:
+    """Drop the cached transform plans and the cuFFT plans (fft.py:101-106)."""
+    from . import fft
     PLANS.clear()
+    fft.clear_plan_cache()

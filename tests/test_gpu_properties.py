@@ -243,3 +243,50 @@ def test_fft_seam_sign_and_roundtrip(esn):
     np.testing.assert_allclose(got, ref, atol=1e-11)
     back = fft_exec(FftPlanKey((12, 10), BACKWARD), got)
     np.testing.assert_allclose(back, 120 * a, atol=1e-10)
+
+
+@pytest.mark.gpu
+def test_fft_plan_cache(esn):
+    """fft.py:87-111: get_plan builds once per key and caches; plan_cache_size
+    counts; clear_plan_cache(key) / () drop; a cached plan executes like the
+    plan-less path (reference test: esnufft tests/test_fft.py plan cache)."""
+    import torch
+    from paper_1808_06736_b200 import fft as F
+    F.clear_plan_cache()
+    assert F.plan_cache_size() == 0
+    k1, k2 = F.FftPlanKey((16, 12), F.FORWARD), F.FftPlanKey((9,), F.BACKWARD)
+    p1 = F.get_plan(k1)
+    assert F.get_plan(k1) is p1 and p1.strategy == "cufft" and p1.build_time >= 0
+    F.get_plan(k2)
+    assert F.plan_cache_size() == 2
+    rng = np.random.default_rng(5)
+    a = rng.standard_normal((16, 12)) + 1j * rng.standard_normal((16, 12))
+    t = torch.tensor(a, device="cuda")
+    p1.execute(t)
+    np.testing.assert_allclose(t.cpu().numpy(), np.fft.ifftn(a) * a.size, atol=1e-11)
+    np.testing.assert_allclose(F.fft_exec(k1, a), np.fft.ifftn(a) * a.size, atol=1e-11)
+    F.clear_plan_cache(k2)
+    assert F.plan_cache_size() == 1 and F.get_plan(k1) is p1
+    F.clear_plan_cache()
+    assert F.plan_cache_size() == 0
+    np.testing.assert_allclose(F.fft_exec(k1, a), np.fft.ifftn(a) * a.size, atol=1e-11)
+
+
+@pytest.mark.gpu
+def test_spread_interp_stats(esn):
+    """spreadinterp.py:165-184: stats gets busy_per_thread and tasks (plus the
+    GPU stage times)."""
+    from paper_1808_06736_b200 import spreadinterp as S
+    from paper_1808_06736_b200.kernel import select_params
+    rng = np.random.default_rng(6)
+    m = 20_000
+    xs = [rng.uniform(-np.pi, np.pi, m) for _ in range(2)]
+    c = rng.standard_normal(m) + 1j * rng.standard_normal(m)
+    kp = select_params(1e-6)
+    pts = S.build_point_set(xs, (64, 48))
+    st = {}
+    g = S.spread(pts, c, kp, stats=st)
+    assert st["tasks"] >= 1 and set(st["busy_per_thread"]) == {0} and st["busy_per_thread"][0] > 0
+    st2 = {}
+    S.interp(pts, g, kp, stats=st2)
+    assert st2["tasks"] >= 1 and st2["busy_per_thread"][0] > 0
