@@ -1836,7 +1836,7 @@ struct InterpUnit {
 // P_d <= n_d (each patch row wraps at most once).
 template <typename T, int DIM, int W>
 __global__ void __launch_bounds__(256, interp_minb<DIM, W>())
-    k_interp_bulk(SpreadArgs<T> a, T *cout, const T *gridp, int slice) {
+    k_interp_bulk(SpreadArgs<T> a, T *cout, const T *gridp, int slice, int dprod) {
     using C = typename Cx<T>::type;
     extern __shared__ __align__(16) unsigned char bulk_smem[];
     __shared__ uint64_t s_full[2], s_empty[2];
@@ -1928,13 +1928,23 @@ __global__ void __launch_bounds__(256, interp_minb<DIM, W>())
         p_pb = 1;
         mbar_init(&s_full[0], 1);
         mbar_init(&s_full[1], 1);
-        mbar_init(&s_empty[0], nwarps);
-        mbar_init(&s_empty[1], nwarps);
+        mbar_init(&s_empty[0], dprod ? nwarps - 1 : nwarps);
+        mbar_init(&s_empty[1], dprod ? nwarps - 1 : nwarps);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (tid == 0) p_next = atomicAdd(a.work, 1);
+    // dprod: the last warp only produces (queues unit k + 1 as soon as every
+    // consumer released unit k - 1); else warp 0 produces between its own
+    // units, so a late warp 0 shortened the prefetch distance
+    const int pw = dprod ? nwarps - 1 : 0;
+    if (warp == pw && lane == 0) p_next = atomicAdd(a.work, 1);  // (the producer's own claim)
     __syncthreads();
-    int producing = warp == 0 ? produce(0) : 0;
+    const int cthreads = dprod ? blockDim.x - 32 : blockDim.x;
+    if (dprod && warp == pw) {
+        for (int k = 0;; ++k)
+            if (!produce(k)) break;
+        return;
+    }
+    int producing = warp == pw ? produce(0) : 0;
     const uint64_t keep = policy_evict_last();
     for (int k = 0;; ++k) {
         const int rb = k & 1;
@@ -1944,7 +1954,7 @@ __global__ void __launch_bounds__(256, interp_minb<DIM, W>())
         if (!u.valid) break;
         const Rec *recs = rec0 + rb * slice;
         const C *patch = patch0 + u.pb * ncell;
-        for (int kk = tid; kk < u.n; kk += blockDim.x) {
+        for (int kk = tid; kk < u.n; kk += cthreads) {
             const Rec rc = recs[kk];
             T r1[W], r2[W], r3[W];
             const int i1 = kernel_row<T, W>(rc.g[0], a.k, r1);

@@ -197,7 +197,11 @@ struct InterpOp {
                 int occ = 0;
                 ESN_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_interp_bulk<T, D, W>, 256, bsmem));
                 if (occ < 1) occ = 1;
-                k_interp_bulk<T, D, W><<<device_sm_count() * occ, 256, bsmem, st>>>(a, cout, grid, slice);
+                static const int dprod = [] {
+                    const char *e = getenv("ESN_INTERP_PRODUCER");
+                    return e && e[0] == '0' ? 0 : 1;
+                }();
+                k_interp_bulk<T, D, W><<<device_sm_count() * occ, 256, bsmem, st>>>(a, cout, grid, slice, dprod);
                 ESN_CUDA_TRY(cudaGetLastError());
                 return ESN_SUCCESS;
             }
