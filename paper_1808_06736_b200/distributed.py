@@ -113,6 +113,20 @@ def exec_type1_grid_reduced(coords, strengths, num_modes, opts, *, group=None, d
     return finish(state, grid, num_modes, opts)
 
 
+def _empty_slice_spec(part, ref, opts, group):
+    """dtype / device of this rank's all-gather buffer.  A rank without a
+    transform (T < world) has no result to copy them from: it uses the plan
+    precision and the device the backend needs (NCCL: this rank's CUDA
+    device; gloo: host), so every rank joins with matching buffers."""
+    if part is not None:
+        return part.dtype, part.device
+    prec = getattr(opts, "dtype", "float64")
+    dtype = torch.complex64 if prec == "float32" else torch.complex128
+    if dist.get_backend(group) == "nccl":
+        return dtype, torch.device("cuda", torch.cuda.current_device())
+    return (ref.dtype if ref.is_complex() else dtype), torch.device("cpu")
+
+
 def _gather_transform_slices(part, T, rank, world, group, tail_shape, dtype, device):
     """All-gather per-rank (T_r, ...) slices into the full (T, ...) array.
     Every rank joins the collective, including ranks whose slice is empty
@@ -146,8 +160,7 @@ def exec_type1_transform_sharded(coords, strengths_all, num_modes, opts, *, grou
     tail = tuple(reversed(nm))
     ref = strengths_all if isinstance(strengths_all, torch.Tensor) else torch.as_tensor(strengths_all)
     part = None if part is None else (part if isinstance(part, torch.Tensor) else torch.as_tensor(part))
-    dtype = part.dtype if part is not None else ref.dtype
-    device = part.device if part is not None else ref.device
+    dtype, device = _empty_slice_spec(part, ref, opts, group)
     return _gather_transform_slices(part, T, rank, world, group, tail, dtype, device)
 
 
@@ -176,6 +189,5 @@ def exec_type2_transform_sharded(coords, modes_all, opts, *, group=None, compute
     part = None if part is None else (part if isinstance(part, torch.Tensor) else torch.as_tensor(part))
     if part is not None and part.ndim == 1:
         part = part[None]
-    dtype = part.dtype if part is not None else ref.dtype
-    device = part.device if part is not None else ref.device
+    dtype, device = _empty_slice_spec(part, ref, opts, group)
     return _gather_transform_slices(part, T, rank, world, group, (M,), dtype, device)

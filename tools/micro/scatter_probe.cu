@@ -160,6 +160,34 @@ __global__ void __launch_bounds__(1024) k_g2(const double *x, const double *y, i
         for (int u = 0; u < 4; ++u) { int i = base + u * blockDim.x; if (i < hi) st256(out + (pos[u] & mask), a[u], b[u], i, pf); }
     }
 }
+
+// C2: the current scatter's shape but a 4-byte index store (perm[pos] = j)
+__global__ void __launch_bounds__(256) k_c2(const double *x, const double *y, int M, int K, int *cur, int *perm, int mask) {
+    uint64_t pl;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pl));
+    const int S = gridDim.x * blockDim.x * 8;
+    for (int base = blockIdx.x * blockDim.x * 8 + threadIdx.x; base < M; base += S) {
+        double a[8], b[8]; int pos[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) { int i = base + u * blockDim.x; a[u] = i < M ? x[i] : 0; b[u] = i < M ? y[i] : 0; }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            int i = base + u * blockDim.x;
+            uint32_t k = hash32(i + (a[u] + b[u] > 1e300)) % K;
+            if (i < M) asm volatile("atom.global.add.L2::cache_hint.u32 %0, [%1], 1, %2;" : "=r"(pos[u]) : "l"(cur + k), "l"(pl) : "memory");
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            int i = base + u * blockDim.x;
+            if (i < M) asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" :: "l"(perm + (pos[u] & mask)), "r"(i), "l"(pl) : "memory");
+        }
+    }
+}
+// key positions with spatial locality like the real sort: key = (i*2654435761 >> 10) % K ... here:
+// cursors start at k * (M / K) so positions are a true permutation-ish
+__global__ void k_init_cur(int *cur, int K, int M) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < K; k += gridDim.x * blockDim.x) cur[k] = (int)((long)k * M / K);
+}
 // H: index gather of coordinates (interp-side): read perm sequentially,
 // gather x[j], y[j]; j restricted to a window of C points (target chunk)
 __global__ void k_gather(const int *perm, const double *x, const double *y, int M, double *sink) {
@@ -234,6 +262,13 @@ int main() {
             char nm[96]; snprintf(nm, 96, "G2 smem-cursor scatter K=%d ncta=%d", K, ncta);
             TIME(nm, (k_g2<<<ncta, 1024, K * 4>>>(x, y, M, K, mat, rec, mask)));
         }
+
+    {
+        int *permb; cudaMalloc(&permb, (size_t)(mask + 1) * 4);
+        TIME("C2 atom-ret + 4 B index (ILP 8, L2 hints), 4 Mi keys", (k_init_cur<<<1024, 256>>>(cnt, KF, M), k_c2<<<nsm * 8, 256>>>(x, y, M, KF, cnt, permb, mask)));
+        TIME("B2 (same cursor init), 4 Mi keys", (k_init_cur<<<1024, 256>>>(cnt, KF, M), k_b2<<<nsm * 8, 256>>>(x, y, M, KF, cnt, rec, mask)));
+        TIME("init only", (k_init_cur<<<1024, 256>>>(cnt, KF, M)));
+    }
     for (int C : {M, M / 2, M / 4, M / 8, M / 16}) {
         k_make_perm<<<nsm * 8, 256>>>(perm, M, C);
         char nm[64]; snprintf(nm, 64, "H  gather x[j],y[j], chunk %d", C);
