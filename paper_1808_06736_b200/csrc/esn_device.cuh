@@ -428,8 +428,9 @@ __global__ void __launch_bounds__(RowsCfg<T, DIM, W>::NT, RowsCfg<T, DIM, W>::MI
 //    per chunk; lists are built per warp by ballot compaction (no atomics).
 template <typename T, int W>
 struct Rows3Cfg {
-    using R = RowsCfg<T, 3, W>;
-    static constexpr int BX = R::BX, X = R::X, RY = R::RY, RZ = R::RZ, NT = R::NT, MINB = R::MINB;
+    using R = Rows3Geo<T, W>;
+    static constexpr int BX = R::BX, X = R::X, RY = R::RY, RZ = R::RZ, NT = R::NT, MINB = 2;
+    static constexpr int LY = R::LY, LZ = R::LZ, WY = R::WY, WZ = R::WZ;
     static constexpr int NW = NT / 32;
     static constexpr int VT = 16 / (int)sizeof(T);                // T per 16-byte vector
     static constexpr int OFN = VT;                                // (oy, oz, ox, pad) ints
@@ -446,7 +447,7 @@ struct Rows3Cfg {
     static constexpr size_t LIST_B = (size_t)NW * CH * sizeof(unsigned);
     static constexpr size_t SMEM = 2 * STAGE_B + RING_B + CRING_B + LIST_B;
     static_assert(2 * STAGE_B / 16 <= 0xffff && (RECS * sizeof(T)) % 16 == 0, "list entries address 16-byte units");
-    static_assert(BX <= 32 && RY - W + 1 <= 16 && RZ - W + 1 <= 16, "list entries pack ox (5), oy (4), oz (4) bits");
+    static_assert(BX <= 32 && RY - W + 1 <= 32 && RZ - W + 1 <= 16, "list entries pack ox (5), oy (5), oz (4) bits");
     static constexpr size_t TILE_B = (size_t)RY * RZ * X * 2 * sizeof(T);
     // flush passes over z slabs so one slab fits the two stages (the record
     // ring may still have copies in flight)
@@ -470,7 +471,7 @@ __device__ __forceinline__ Rows3Pre<T> rows3_load(const unsigned char *stage, un
     p.off = e & 0xffffu;
     const T *rec = reinterpret_cast<const T *>(stage + 16u * p.off);
     // (y, z) offsets ride in the list entry: no dependent shared load
-    const int dy = ry - (int)((e >> 21) & 15u), dz = rz - (int)((e >> 25) & 15u);
+    const int dy = ry - (int)((e >> 21) & 31u), dz = rz - (int)((e >> 26) & 15u);
     const bool cov = (unsigned)dy < (unsigned)W && (unsigned)dz < (unsigned)W;
     p.f = rec[Cfg::O_R2 + (cov ? dy : W)];  // r2[W] == 0
     p.cz = *reinterpret_cast<const C *>(rec + Cfg::O_CZ + 2 * (cov ? dz : 0));
@@ -510,7 +511,7 @@ __device__ __forceinline__ void rows3_apply(typename Cx<T>::type *acc, const uns
 }
 
 // one run of equal x offset OX from the warp list (entry = record offset in
-// 16-byte units | ox << 16 | oy << 21 | oz << 25); the next point's operands load before this one's FMAs
+// 16-byte units | ox << 16 | oy << 21 | oz << 26); the next point's operands load before this one's FMAs
 template <typename T, int W, int OX>
 __device__ __forceinline__ int rows3_run(typename Cx<T>::type *acc, const unsigned char *stage,
                                          const unsigned *list, int i, int nq, int ry, int rz) {
@@ -539,13 +540,19 @@ __global__ void __launch_bounds__(Rows3Cfg<T, W>::NT, Rows3Cfg<T, W>::MINB) k_sp
     __shared__ int s_sub;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wy = warp & 1, wz = warp >> 1;  // 2 x 4 row blocks of 8 (y) x 4 (z)
-    const int ry = wy * 8 + (lane & 7), rz = wz * 4 + (lane >> 3);
-    const int by0 = wy * 8, bz0 = wz * 4;
-    // point threads (phase A, one staged point each) are the warps of the two
-    // z-edge row blocks, whose lists are about half as long as the others'
-    static_assert(NT == 256 && RZ == 16, "point-thread map assumes 2 x 4 row blocks");
-    const int pt = wz == 0 ? warp * 32 + lane : (wz == 3 ? (warp - 4) * 32 + lane : CH);  // warps 0,1,6,7
+    constexpr int LY = Cfg::LY, LZ = Cfg::LZ, WY = Cfg::WY, WZ = Cfg::WZ;
+    const int wy = warp % WY, wz = warp / WY;  // WY x WZ row blocks of LY (y) x LZ (z)
+    const int ry = wy * LY + (lane % LY), rz = wz * LZ + (lane / LY);
+    const int by0 = wy * LY, bz0 = wz * LZ;
+    // point threads (phase A, one staged point each) are the four warps of
+    // the edge row blocks (z edges of the square tile, y edges of the thin
+    // one), whose lists are the shortest
+    static_assert(NT == 256 && CH <= 128, "four point-thread warps");
+    int edge = -1;
+    if constexpr (WZ > 1) edge = wz == 0 ? wy : (wz == WZ - 1 ? 2 + wy : -1);
+    else edge = wy < 2 ? wy : (wy >= WY - 2 ? wy - (WY - 2) + 2 : -1);
+    static_assert(WZ > 1 ? WY == 2 : WY >= 4, "edge warps 0..3");
+    const int pt = edge >= 0 ? edge * 32 + lane : CH;
     const int n1 = a.g.n[0], n2 = a.g.n[1], n3 = a.g.n[2];
     const int nsub = *a.nsub;
     unsigned *mylist = s_list + warp * CH;
@@ -635,7 +642,7 @@ __global__ void __launch_bounds__(Rows3Cfg<T, W>::NT, Rows3Cfg<T, W>::MINB) k_sp
                 int ox = 0, oy = 0, oz = 0;
                 if (q < nch) {
                     const int4 o = *reinterpret_cast<const int4 *>(stg + q * RECS);
-                    cov = o.x <= by0 + 7 && o.x + W - 1 >= by0 && o.y <= bz0 + 3 && o.y + W - 1 >= bz0;
+                    cov = o.x <= by0 + LY - 1 && o.x + W - 1 >= by0 && o.y <= bz0 + LZ - 1 && o.y + W - 1 >= bz0;
                     ox = o.z;
                     oy = o.x;
                     oz = o.y;
@@ -644,7 +651,7 @@ __global__ void __launch_bounds__(Rows3Cfg<T, W>::NT, Rows3Cfg<T, W>::MINB) k_sp
                 if (cov)
                     mylist[n + __popc(bal & ((1u << lane) - 1u))] =
                         (unsigned)(((st & 1) * Cfg::STAGE_B + q * RECS * sizeof(T)) / 16) | ((unsigned)ox << 16) |
-                        ((unsigned)oy << 21) | ((unsigned)oz << 25);
+                        ((unsigned)oy << 21) | ((unsigned)oz << 26);
                 n += __popc(bal);
             }
             __syncwarp();

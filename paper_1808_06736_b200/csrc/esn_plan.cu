@@ -227,10 +227,20 @@ static int ensure_key_space(esn_plan p) {
 template <int W>
 static void rows_bins(int dtype, int dim, int ntransf, int *bs) {
     if (dim == 3) {
-        if (dtype == ESN_F64) {
+        // bins of the spreader that will run: k_spread_rows3 (Rows3Geo) or,
+        // with ESN_SPREAD3=rows, the earlier k_spread_rows (RowsCfg)
+        static const bool old_rows = [] {
+            const char *e = getenv("ESN_SPREAD3");
+            return e && std::string(e) == "rows";
+        }();
+        if (old_rows && dtype == ESN_F64) {
             bs[0] = RowsCfg<double, 3, W>::BX; bs[1] = RowsCfg<double, 3, W>::BY; bs[2] = RowsCfg<double, 3, W>::BZ;
-        } else {
+        } else if (old_rows) {
             bs[0] = RowsCfg<float, 3, W>::BX; bs[1] = RowsCfg<float, 3, W>::BY; bs[2] = RowsCfg<float, 3, W>::BZ;
+        } else if (dtype == ESN_F64) {
+            bs[0] = Rows3Geo<double, W>::BX; bs[1] = Rows3Geo<double, W>::BY; bs[2] = Rows3Geo<double, W>::BZ;
+        } else {
+            bs[0] = Rows3Geo<float, W>::BX; bs[1] = Rows3Geo<float, W>::BY; bs[2] = Rows3Geo<float, W>::BZ;
         }
     } else if (esn::batched_spread(dtype, dim, W, ntransf, ESN_METHOD_TILE)) {
         bs[0] = Batch2Cfg<float, W>::BX; bs[1] = Batch2Cfg<float, W>::BY; bs[2] = 1;
