@@ -83,9 +83,9 @@ def hot_kernel_name(cfg):
 BINDING = {
     "c1": "launch / latency (1e5 points; CUDA-graph replay)",
     "c2": "shared-memory wavefronts (~75 % busy) + FP64 pipe (~37 %), not HBM",
-    "c3": "FP64 pipe (w^3 = 343 DFMA pairs per point), not HBM",
-    "c3f": "issue / FP32 pipe, not HBM",
-    "c4": "FP64 pipe (w^3 = 1000 DFMA pairs per point), not HBM",
+    "c3": "issue / shared-memory wavefronts (~44 instructions around 14 DFMA per point-warp pass; FP64 pipe ~25 %), not HBM",
+    "c3f": "issue / shared-memory wavefronts (per-pass overhead around 10 FFMA), not HBM",
+    "c4": "issue / FP64 pipe (~44 % active; 1000 cells per point at 45 % lane coverage), not HBM",
     "c5": "issue (~80 instructions per point-strip visit, 45 % issue efficiency), DRAM ~ algorithmic bytes",
 }
 
