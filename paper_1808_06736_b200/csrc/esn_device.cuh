@@ -435,8 +435,15 @@ struct Rows3Cfg {
     static constexpr int VT = 16 / (int)sizeof(T);                // T per 16-byte vector
     static constexpr int OFN = VT;                                // (oy, oz, ox, pad) ints
     static constexpr int R1N = (W + VT - 1) / VT * VT;           // r1, whole vectors
-    static constexpr int R2N = (W + 1 + VT - 1) / VT * VT;       // r2 + zero (uncovered rows)
-    static constexpr int CZN = 2 * W;                             // c * r3 (complex)
+    // thin tile: r2 and c * r3 zero-padded over every (dy, dz) a listed point
+    // can meet (dy in [-(LY-1), LY+W-2], dz in [-(BZ-1), LZ-1]), so the
+    // pass indexes them with no coverage test; square tile: r2 + one zero
+    static constexpr bool PAD = R::THIN;
+    static constexpr int PY = LY - 1, PZ = R::BZ - 1;             // index bias
+    static constexpr int R2E = PAD ? 2 * LY + W - 2 : W + 1;      // r2 entries
+    static constexpr int CZE = PAD ? PZ + LZ : W;                 // c * r3 entries (complex)
+    static constexpr int R2N = (R2E + VT - 1) / VT * VT;
+    static constexpr int CZN = 2 * CZE;
     static constexpr int O_R1 = OFN, O_R2 = OFN + R1N, O_CZ = OFN + R1N + R2N;
     static constexpr int RECN = (O_CZ + CZN + VT - 1) / VT * VT;
     static constexpr int RECS = RECN + VT;  // stride: +16 B keeps phase-A stores conflict-free
@@ -472,9 +479,14 @@ __device__ __forceinline__ Rows3Pre<T> rows3_load(const unsigned char *stage, un
     const T *rec = reinterpret_cast<const T *>(stage + 16u * p.off);
     // (y, z) offsets ride in the list entry: no dependent shared load
     const int dy = ry - (int)((e >> 21) & 31u), dz = rz - (int)((e >> 26) & 15u);
-    const bool cov = (unsigned)dy < (unsigned)W && (unsigned)dz < (unsigned)W;
-    p.f = rec[Cfg::O_R2 + (cov ? dy : W)];  // r2[W] == 0
-    p.cz = *reinterpret_cast<const C *>(rec + Cfg::O_CZ + 2 * (cov ? dz : 0));
+    if constexpr (Cfg::PAD) {
+        p.f = rec[Cfg::O_R2 + Cfg::PY + dy];
+        p.cz = *reinterpret_cast<const C *>(rec + Cfg::O_CZ + 2 * (Cfg::PZ + dz));
+    } else {
+        const bool cov = (unsigned)dy < (unsigned)W && (unsigned)dz < (unsigned)W;
+        p.f = rec[Cfg::O_R2 + (cov ? dy : W)];  // r2[W] == 0
+        p.cz = *reinterpret_cast<const C *>(rec + Cfg::O_CZ + 2 * (cov ? dz : 0));
+    }
     return p;
 }
 
@@ -619,13 +631,17 @@ __global__ void __launch_bounds__(Rows3Cfg<T, W>::NT, Rows3Cfg<T, W>::MINB) k_sp
                 for (int m = 0; m < Cfg::R1N; ++m) rec[Cfg::O_R1 + m] = m < W ? r[m] : (T)0;
                 i0 = kernel_row<T, W>(rc.g[1], a.k, r);
                 const int oy = (i0 < 0 ? i0 + n2 : i0) - lo2;
+                constexpr int B2 = Cfg::PAD ? Cfg::PY : 0, BZ3 = Cfg::PAD ? Cfg::PZ : 0;
 #pragma unroll
-                for (int m = 0; m < Cfg::R2N; ++m) rec[Cfg::O_R2 + m] = m < W ? r[m] : (T)0;
+                for (int m = 0; m < Cfg::R2N; ++m)
+                    rec[Cfg::O_R2 + m] = (m >= B2 && m < B2 + W) ? r[m - B2 < W ? m - B2 : 0] : (T)0;
                 i0 = kernel_row<T, W>(rc.g[2], a.k, r);
                 const int oz = (i0 < 0 ? i0 + n3 : i0) - lo3;
 #pragma unroll
-                for (int m = 0; m < W; ++m)
-                    *reinterpret_cast<C *>(rec + Cfg::O_CZ + 2 * m) = C{c.x * r[m], c.y * r[m]};
+                for (int m = 0; m < Cfg::CZN / 2; ++m) {
+                    const T rm = (m >= BZ3 && m < BZ3 + W) ? r[m - BZ3 < W ? m - BZ3 : 0] : (T)0;
+                    *reinterpret_cast<C *>(rec + Cfg::O_CZ + 2 * m) = C{c.x * rm, c.y * rm};
+                }
                 *reinterpret_cast<int4 *>(rec) = make_int4(oy, oz, ox, 0);
             }
         };
