@@ -528,12 +528,12 @@ __device__ __forceinline__ void rows3_apply(typename Cx<T>::type *acc, const uns
 template <typename T, int W, int OX>
 __device__ __forceinline__ int rows3_run(typename Cx<T>::type *acc, const unsigned char *stage,
                                          const unsigned *list, int i, int nq, int ry, int rz) {
-    unsigned e = list[i];
+    // bit 31 of an entry marks the last point of its x-offset run (and of the list)
+    (void)nq;
     for (;;) {
+        const unsigned e = list[i++];
         rows3_apply<T, W, OX>(acc, stage, rows3_load<T, W>(stage, e, ry, rz));
-        if (++i >= nq) break;
-        e = list[i];
-        if (((e >> 16) & 31u) != (unsigned)OX) break;
+        if (e >> 31) break;
     }
     return i;
 }
@@ -670,6 +670,13 @@ __global__ void __launch_bounds__(Rows3Cfg<T, W>::NT, Rows3Cfg<T, W>::MINB) k_sp
                         (unsigned)(((st & 1) * Cfg::STAGE_B + q * RECS * sizeof(T)) / 16) | ((unsigned)ox << 16) |
                         ((unsigned)oy << 21) | ((unsigned)oz << 26);
                 n += __popc(bal);
+            }
+            __syncwarp();
+            // run ends: bit 31 where the next entry's x offset differs (or at the end)
+            for (int i = lane; i < n; i += 32) {
+                const unsigned e = mylist[i];
+                const unsigned en = i + 1 < n ? mylist[i + 1] : 0xffffffffu;
+                if (((e ^ en) >> 16) & 31u || i + 1 == n) mylist[i] = e | 0x80000000u;
             }
             __syncwarp();
             nq = n;
