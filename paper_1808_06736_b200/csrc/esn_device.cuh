@@ -452,9 +452,10 @@ struct Rows3Cfg {
     static constexpr size_t STAGE_B = (size_t)CH * RECS * sizeof(T);
     static constexpr size_t RING_B = (size_t)2 * CH * sizeof(Rec);
     static constexpr size_t CRING_B = (size_t)CH * 2 * sizeof(T);
-    static constexpr size_t LIST_B = (size_t)NW * CH * sizeof(unsigned);
+    static constexpr size_t LIST_B = (size_t)NW * CH * sizeof(uint2);
     static constexpr size_t SMEM = 2 * STAGE_B + RING_B + CRING_B + LIST_B;
     static_assert(2 * STAGE_B / 16 <= 0xffff && (RECS * sizeof(T)) % 16 == 0, "list entries address 16-byte units");
+    static_assert(2 * STAGE_B / sizeof(T) + RECS + 64 <= 0xffff && O_CZ % 2 == 0, "operand indices fit 16 bits");
     static_assert(BX <= 32 && RY - W + 1 <= 32 && RZ - W + 1 <= 16, "list entries pack ox (5), oy (5), oz (4) bits");
     static constexpr size_t TILE_B = (size_t)RY * RZ * X * 2 * sizeof(T);
     // flush passes over z slabs so one slab fits the two stages (the record
@@ -471,23 +472,20 @@ struct Rows3Pre {
     unsigned off;  // record offset in 16-byte units
 };
 
+// One warp-list entry (two words):
+//   x = record offset in 16-byte units | ox << 16 | last-of-run << 31
+//   y = (T index of r2[PY - oy] + 32) | (complex index of cz[PZ - oz] + 32) << 16
+// so a lane's operands are base_f + sizeof(T) * (y & 0xffff) and
+// base_cz + sizeof(C) * (y >> 16) with lane-constant bases (ry, rz folded in).
 template <typename T, int W>
-__device__ __forceinline__ Rows3Pre<T> rows3_load(const unsigned char *stage, unsigned e, int ry, int rz) {
+__device__ __forceinline__ Rows3Pre<T> rows3_load(const unsigned char *stage, uint2 e, const unsigned char *base_f,
+                                                  const unsigned char *base_cz) {
     using C = typename Cx<T>::type;
-    using Cfg = Rows3Cfg<T, W>;
     Rows3Pre<T> p;
-    p.off = e & 0xffffu;
-    const T *rec = reinterpret_cast<const T *>(stage + 16u * p.off);
-    // (y, z) offsets ride in the list entry: no dependent shared load
-    const int dy = ry - (int)((e >> 21) & 31u), dz = rz - (int)((e >> 26) & 15u);
-    if constexpr (Cfg::PAD) {
-        p.f = rec[Cfg::O_R2 + Cfg::PY + dy];
-        p.cz = *reinterpret_cast<const C *>(rec + Cfg::O_CZ + 2 * (Cfg::PZ + dz));
-    } else {
-        const bool cov = (unsigned)dy < (unsigned)W && (unsigned)dz < (unsigned)W;
-        p.f = rec[Cfg::O_R2 + (cov ? dy : W)];  // r2[W] == 0
-        p.cz = *reinterpret_cast<const C *>(rec + Cfg::O_CZ + 2 * (cov ? dz : 0));
-    }
+    p.off = e.x & 0xffffu;
+    p.f = *reinterpret_cast<const T *>(base_f + (unsigned)sizeof(T) * (e.y & 0xffffu));
+    p.cz = *reinterpret_cast<const C *>(base_cz + (unsigned)sizeof(C) * (e.y >> 16));
+    (void)stage;
     return p;
 }
 
@@ -523,17 +521,15 @@ __device__ __forceinline__ void rows3_apply(typename Cx<T>::type *acc, const uns
     }
 }
 
-// one run of equal x offset OX from the warp list (entry = record offset in
-// 16-byte units | ox << 16 | oy << 21 | oz << 26); the next point's operands load before this one's FMAs
+// one run of equal x offset OX from the warp list; bit 31 of an entry's first
+// word marks the last point of its run (and of the list)
 template <typename T, int W, int OX>
-__device__ __forceinline__ int rows3_run(typename Cx<T>::type *acc, const unsigned char *stage,
-                                         const unsigned *list, int i, int nq, int ry, int rz) {
-    // bit 31 of an entry marks the last point of its x-offset run (and of the list)
-    (void)nq;
+__device__ __forceinline__ int rows3_run(typename Cx<T>::type *acc, const unsigned char *stage, const uint2 *list,
+                                         int i, const unsigned char *base_f, const unsigned char *base_cz) {
     for (;;) {
-        const unsigned e = list[i++];
-        rows3_apply<T, W, OX>(acc, stage, rows3_load<T, W>(stage, e, ry, rz));
-        if (e >> 31) break;
+        const uint2 e = list[i++];
+        rows3_apply<T, W, OX>(acc, stage, rows3_load<T, W>(stage, e, base_f, base_cz));
+        if (e.x >> 31) break;
     }
     return i;
 }
@@ -548,7 +544,7 @@ __global__ void __launch_bounds__(Rows3Cfg<T, W>::NT, Rows3Cfg<T, W>::MINB) k_sp
     T *s_stage = reinterpret_cast<T *>(smem_raw);                                        // 2 x CH x RECS
     Rec *s_ring = reinterpret_cast<Rec *>(smem_raw + 2 * Cfg::STAGE_B);                  // 2 x CH
     C *s_c = reinterpret_cast<C *>(smem_raw + 2 * Cfg::STAGE_B + Cfg::RING_B);           // CH
-    unsigned *s_list = reinterpret_cast<unsigned *>(smem_raw + 2 * Cfg::STAGE_B + Cfg::RING_B + Cfg::CRING_B);  // NW x CH
+    uint2 *s_list = reinterpret_cast<uint2 *>(smem_raw + 2 * Cfg::STAGE_B + Cfg::RING_B + Cfg::CRING_B);  // NW x CH
     C *s_tile = reinterpret_cast<C *>(smem_raw);  // flush slab (aliases the stages)
     __shared__ int s_sub;
 
@@ -568,7 +564,11 @@ __global__ void __launch_bounds__(Rows3Cfg<T, W>::NT, Rows3Cfg<T, W>::MINB) k_sp
     const int pt = edge >= 0 ? edge * 32 + lane : CH;
     const int n1 = a.g.n[0], n2 = a.g.n[1], n3 = a.g.n[2];
     const int nsub = *a.nsub;
-    unsigned *mylist = s_list + warp * CH;
+    uint2 *mylist = s_list + warp * CH;
+    // lane-constant operand bases (entries carry the per-point parts, biased by 32)
+    static_assert(Cfg::PAD, "two-word entries index the zero-padded r2 / c * r3");
+    const unsigned char *base_f = smem_raw + (int)sizeof(T) * (ry - 32);
+    const unsigned char *base_cz = smem_raw + (int)sizeof(C) * (rz - 32);
     uint64_t pol_first, pol_last;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
@@ -665,18 +665,20 @@ __global__ void __launch_bounds__(Rows3Cfg<T, W>::NT, Rows3Cfg<T, W>::MINB) k_sp
                     oz = o.y;
                 }
                 const unsigned bal = __ballot_sync(0xffffffffu, cov);
-                if (cov)
-                    mylist[n + __popc(bal & ((1u << lane) - 1u))] =
-                        (unsigned)(((st & 1) * Cfg::STAGE_B + q * RECS * sizeof(T)) / 16) | ((unsigned)ox << 16) |
-                        ((unsigned)oy << 21) | ((unsigned)oz << 26);
+                if (cov) {
+                    const unsigned rb = (unsigned)((st & 1) * Cfg::STAGE_B + q * RECS * sizeof(T));  // record byte offset
+                    const unsigned fi = rb / (unsigned)sizeof(T) + Cfg::O_R2 + Cfg::PY - oy + 32;
+                    const unsigned zi = rb / (unsigned)sizeof(C) + Cfg::O_CZ / 2 + Cfg::PZ - oz + 32;
+                    mylist[n + __popc(bal & ((1u << lane) - 1u))] = make_uint2((rb / 16) | ((unsigned)ox << 16), fi | (zi << 16));
+                }
                 n += __popc(bal);
             }
             __syncwarp();
             // run ends: bit 31 where the next entry's x offset differs (or at the end)
             for (int i = lane; i < n; i += 32) {
-                const unsigned e = mylist[i];
-                const unsigned en = i + 1 < n ? mylist[i + 1] : 0xffffffffu;
-                if (((e ^ en) >> 16) & 31u || i + 1 == n) mylist[i] = e | 0x80000000u;
+                const unsigned e = mylist[i].x;
+                const unsigned en = i + 1 < n ? mylist[i + 1].x : 0xffffffffu;
+                if (((e ^ en) >> 16) & 31u || i + 1 == n) mylist[i].x = e | 0x80000000u;
             }
             __syncwarp();
             nq = n;
@@ -733,11 +735,11 @@ __global__ void __launch_bounds__(Rows3Cfg<T, W>::NT, Rows3Cfg<T, W>::MINB) k_sp
                 const unsigned char *stg = smem_raw;
                 int i = 0;
                 while (i < nq) {
-                    const int ox = (mylist[i] >> 16) & 31;
+                    const int ox = (mylist[i].x >> 16) & 31;
                     switch (ox) {
 #define ESN_R3_CASE(OX)                                                                  \
     case OX:                                                                             \
-        if constexpr (OX < BX) i = rows3_run<T, W, OX>(acc, stg, mylist, i, nq, ry, rz); \
+        if constexpr (OX < BX) i = rows3_run<T, W, OX>(acc, stg, mylist, i, base_f, base_cz); \
         else i = nq;                                                                     \
         break;
                         ESN_R3_CASE(0) ESN_R3_CASE(1) ESN_R3_CASE(2) ESN_R3_CASE(3)
