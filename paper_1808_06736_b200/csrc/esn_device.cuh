@@ -442,7 +442,7 @@ struct Rows3Cfg {
     static constexpr int PY = LY - 1;                             // index biases
     static constexpr int PZ = (LZ - 1 < R::BZ - 1) ? LZ - 1 : R::BZ - 1;
     static constexpr int R2E = PAD ? 2 * LY + W - 2 : W + 1;      // r2 entries
-    static constexpr int CZE = !PAD ? W : (R::THIN ? PZ + LZ : PZ + LZ + W - 1);  // c * r3 entries (complex)
+    static constexpr int CZE = !PAD ? W : (R::WZ == 1 ? PZ + LZ : PZ + LZ + W - 1);  // c * r3 entries (complex)
     static constexpr int R2N = (R2E + VT - 1) / VT * VT;
     static constexpr int CZN = 2 * CZE;
     static constexpr int O_R1 = OFN, O_R2 = OFN + R1N, O_CZ = OFN + R1N + R2N;
