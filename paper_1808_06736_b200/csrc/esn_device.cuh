@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(RowsCfg<T, DIM, W>::NT, RowsCfg<T, DIM, W>::MI
 template <typename T, int W>
 struct Rows3Cfg {
     using R = Rows3Geo<T, W>;
-    static constexpr int BX = R::BX, X = R::X, RY = R::RY, RZ = R::RZ, NT = R::NT, MINB = 2;
+    static constexpr int BX = R::BX, X = R::X, RY = R::RY, RZ = R::RZ, NT = R::NT, MINB = NT == 512 ? 1 : 2;
     static constexpr int LY = R::LY, LZ = R::LZ, WY = R::WY, WZ = R::WZ;
     static constexpr int NW = NT / 32;
     static constexpr int VT = 16 / (int)sizeof(T);                // T per 16-byte vector
@@ -455,8 +455,10 @@ struct Rows3Cfg {
     static constexpr size_t LIST_B = (size_t)NW * CH * sizeof(uint2);
     static constexpr size_t SMEM = 2 * STAGE_B + RING_B + CRING_B + LIST_B;
     static_assert(2 * STAGE_B / 16 <= 0xffff && (RECS * sizeof(T)) % 16 == 0, "list entries address 16-byte units");
-    static_assert(2 * STAGE_B / sizeof(T) + RECS + 64 <= 0xffff && O_CZ % 2 == 0, "operand indices fit 16 bits");
-    static_assert(BX <= 32 && RY - W + 1 <= 32 && RZ - W + 1 <= 16, "list entries pack ox (5), oy (5), oz (4) bits");
+    static_assert(2 * STAGE_B / sizeof(T) + RECS + 128 <= 0xffff && O_CZ % 2 == 0, "operand indices fit 16 bits");
+    static_assert(BX <= 32, "list entries pack ox in 5 bits");
+    static constexpr int EBIAS = 64;  // operand-index bias of the list entries (> any oy, oz)
+    static_assert(RY - W + 1 < EBIAS && RZ - W + 1 < EBIAS, "biased indices stay positive");
     static constexpr size_t TILE_B = (size_t)RY * RZ * X * 2 * sizeof(T);
     // flush passes over z slabs so one slab fits the two stages (the record
     // ring may still have copies in flight)
@@ -474,7 +476,7 @@ struct Rows3Pre {
 
 // One warp-list entry (two words):
 //   x = record offset in 16-byte units | ox << 16 | last-of-run << 31
-//   y = (T index of r2[PY - oy] + 32) | (complex index of cz[PZ - oz] + 32) << 16
+//   y = (T index of r2[PY - oy] + EBIAS) | (complex index of cz[PZ - oz] + EBIAS) << 16
 // so a lane's operands are base_f + sizeof(T) * (y & 0xffff) and
 // base_cz + sizeof(C) * (y >> 16) with lane-constant bases (ry, rz folded in).
 template <typename T, int W>
@@ -556,7 +558,7 @@ __global__ void __launch_bounds__(Rows3Cfg<T, W>::NT, Rows3Cfg<T, W>::MINB) k_sp
     // point threads (phase A, one staged point each) are the four warps of
     // the edge row blocks (z edges of the square tile, y edges of the thin
     // one), whose lists are the shortest
-    static_assert(NT == 256 && CH <= 128, "four point-thread warps");
+    static_assert(NT % 32 == 0 && CH <= 128, "four point-thread warps");
     int edge = -1;
     if constexpr (WZ > 1) edge = wz == 0 ? wy : (wz == WZ - 1 ? 2 + wy : -1);
     else edge = wy < 2 ? wy : (wy >= WY - 2 ? wy - (WY - 2) + 2 : -1);
@@ -565,10 +567,10 @@ __global__ void __launch_bounds__(Rows3Cfg<T, W>::NT, Rows3Cfg<T, W>::MINB) k_sp
     const int n1 = a.g.n[0], n2 = a.g.n[1], n3 = a.g.n[2];
     const int nsub = *a.nsub;
     uint2 *mylist = s_list + warp * CH;
-    // lane-constant operand bases (entries carry the per-point parts, biased by 32)
+    // lane-constant operand bases (entries carry the per-point parts, biased by EBIAS)
     static_assert(Cfg::PAD, "two-word entries index the zero-padded r2 / c * r3");
-    const unsigned char *base_f = smem_raw + (int)sizeof(T) * (ry - 32);
-    const unsigned char *base_cz = smem_raw + (int)sizeof(C) * (rz - 32);
+    const unsigned char *base_f = smem_raw + (int)sizeof(T) * (ry - Cfg::EBIAS);
+    const unsigned char *base_cz = smem_raw + (int)sizeof(C) * (rz - Cfg::EBIAS);
     uint64_t pol_first, pol_last;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
@@ -667,8 +669,8 @@ __global__ void __launch_bounds__(Rows3Cfg<T, W>::NT, Rows3Cfg<T, W>::MINB) k_sp
                 const unsigned bal = __ballot_sync(0xffffffffu, cov);
                 if (cov) {
                     const unsigned rb = (unsigned)((st & 1) * Cfg::STAGE_B + q * RECS * sizeof(T));  // record byte offset
-                    const unsigned fi = rb / (unsigned)sizeof(T) + Cfg::O_R2 + Cfg::PY - oy + 32;
-                    const unsigned zi = rb / (unsigned)sizeof(C) + Cfg::O_CZ / 2 + Cfg::PZ - oz + 32;
+                    const unsigned fi = rb / (unsigned)sizeof(T) + Cfg::O_R2 + Cfg::PY - oy + Cfg::EBIAS;
+                    const unsigned zi = rb / (unsigned)sizeof(C) + Cfg::O_CZ / 2 + Cfg::PZ - oz + Cfg::EBIAS;
                     mylist[n + __popc(bal & ((1u << lane) - 1u))] = make_uint2((rb / 16) | ((unsigned)ox << 16), fi | (zi << 16));
                 }
                 n += __popc(bal);

@@ -127,6 +127,9 @@ struct RowsCfg {
 // every warp's block, so a warp visit covers w / 8 of its z rows and only
 // the y overlap varies (c3, w = 7: 61 % of the lanes covered, against 35 %
 // for 8 x 4 blocks of a 16 x 16 tile); wider kernels keep the square tile.
+#ifndef ESN_THIN_RY
+#define ESN_THIN_RY 32
+#endif
 #ifndef ESN_THIN16_MAXW
 #define ESN_THIN16_MAXW 10
 #endif
@@ -137,11 +140,11 @@ struct Rows3Geo {
     static constexpr int BX = RowsCfg<T, 3, W>::BX;
     static constexpr int X = BX + W - 1;
     static constexpr int LY = THIN ? 4 : (THIN16 ? 2 : 8), LZ = THIN ? 8 : (THIN16 ? 16 : 4);
-    static constexpr int RY = THIN ? 32 : 16, RZ = THIN ? 8 : 16;
+    static constexpr int RY = THIN ? ESN_THIN_RY : 16, RZ = THIN ? 8 : 16;
     static constexpr int WY = RY / LY, WZ = RZ / LZ;  // warp blocks
     static constexpr int BY = RY - W + 1, BZ = RZ - W + 1;
     static constexpr int NT = RY * RZ;
-    static_assert(NT == 256 && WY * WZ == 8, "8 warps of 32 rows");
+    static_assert((NT == 256 || NT == 512) && WY * WZ * 32 == NT, "8 or 16 warps of 32 rows");
 };
 
 template <typename T, int W>
