@@ -528,10 +528,29 @@ __device__ __forceinline__ void rows3_apply(typename Cx<T>::type *acc, const uns
 template <typename T, int W, int OX>
 __device__ __forceinline__ int rows3_run(typename Cx<T>::type *acc, const unsigned char *stage, const uint2 *list,
                                          int i, const unsigned char *base_f, const unsigned char *base_cz) {
+    // float32: two points of the run per step (both points' operand loads in
+    // flight before either's FMAs; c3f 1.65 -> 1.57 ms); float64 keeps one
+    // (same time, fewer spills)
+    if constexpr (sizeof(T) == 4) {
+    for (;;) {
+        const uint2 e0 = list[i++];
+        if (e0.x >> 31) {
+            rows3_apply<T, W, OX>(acc, stage, rows3_load<T, W>(stage, e0, base_f, base_cz));
+            break;
+        }
+        const uint2 e1 = list[i++];
+        const Rows3Pre<T> p0 = rows3_load<T, W>(stage, e0, base_f, base_cz);
+        const Rows3Pre<T> p1 = rows3_load<T, W>(stage, e1, base_f, base_cz);
+        rows3_apply<T, W, OX>(acc, stage, p0);
+        rows3_apply<T, W, OX>(acc, stage, p1);
+        if (e1.x >> 31) break;
+    }
+    } else {
     for (;;) {
         const uint2 e = list[i++];
         rows3_apply<T, W, OX>(acc, stage, rows3_load<T, W>(stage, e, base_f, base_cz));
         if (e.x >> 31) break;
+    }
     }
     return i;
 }
