@@ -37,10 +37,15 @@ COLS = [
 
 
 def so_sha():
+    """Identity of the build: sha256 over the library's SOURCES (csrc/ and
+    the Makefile; nvcc output is not byte-reproducible across rebuilds)."""
     h = hashlib.sha256()
-    with open(SO, "rb") as f:
-        for blk in iter(lambda: f.read(1 << 20), b""):
-            h.update(blk)
+    src = os.path.join(os.path.dirname(SO), "csrc")
+    for name in sorted(os.listdir(src)):
+        if name.endswith((".cu", ".cuh", ".h", ".cpp")) or name == "Makefile":
+            h.update(name.encode())
+            with open(os.path.join(src, name), "rb") as f:
+                h.update(f.read())
     return h.hexdigest()[:16]
 
 
@@ -129,7 +134,7 @@ if __name__ == "__main__":
         d = json.load(open(tp)) if os.path.exists(tp) else {}
         d["_doc"] = ("DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per launch of each config's "
                      "hot kernel from `ncu --metrics` (tools/gpu_evidence.sh -> tools/kernel_table.py); "
-                     "_so holds the sha256 prefix of the libesnufft_b200.so each entry was measured on")
+                     "_so holds the sha256 prefix of the library sources (csrc/) each entry was measured on")
         d[cfg] = int(traffic)
         d.setdefault("_so", {})[cfg] = so_sha()
         json.dump(d, open(tp, "w"), indent=2, sort_keys=True)
