@@ -7,9 +7,9 @@ Prints, per kernel name (mean over its launches): device time, DRAM bytes
 read + written, achieved DRAM GB/s, L2 RED / atomic sectors and requests,
 L2 throughput %, FP64 / FMA pipe % and instructions.  With
 --update-traffic, the config's hot-kernel DRAM bytes per launch go into
-profiles/traffic.json together with the sha256 of the libesnufft_b200.so
-that produced them, so bench.py can say whether roofline.traffic belongs
-to the build being benched.
+profiles/traffic.json together with a sha256 of the library sources that
+produced them, so bench.py can say whether roofline.traffic belongs to the
+build being benched.
 """
 import csv
 import hashlib
