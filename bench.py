@@ -199,24 +199,36 @@ def cpu_run(name, M_sample, T_sample, steps, warmup, dist="uniform"):
     M_sample = cfg["M_actual"]
     wcoords, wdata, _ = cases.make_inputs(name, M=min(M_sample, 2000), ntransf=T_sample, dist=dist)
 
+    stage = {}
+
     def one(cs, dd):
+        st = {}
         if cfg["ttype"] == 1:
             batch = dd if dd.ndim == 2 else dd[None]
             for c in batch:  # the reference has no batch API: a loop of transforms
-                O.exec_type1(cs, c, cfg["nm"], tol=cfg["tol"], isign=cfg["isign"], threads=cores)
+                tt = {}
+                O.exec_type1(cs, c, cfg["nm"], tol=cfg["tol"], isign=cfg["isign"], threads=cores, timings=tt)
+                for k, v in tt.items():
+                    st[k] = st.get(k, 0.0) + v
         else:
-            O.exec_type2(cs, dd, tol=cfg["tol"], isign=cfg["isign"], threads=cores)
+            O.exec_type2(cs, dd, tol=cfg["tol"], isign=cfg["isign"], threads=cores, timings=st)
+        return st
 
     one(wcoords, wdata)
     for _ in range(warmup):
         one(coords, data)
-    ts = []
+    ts, sts = [], []
     for _ in range(steps):
         t0 = time.perf_counter()
-        one(coords, data)
+        sts.append(one(coords, data))
         ts.append(time.perf_counter() - t0)
     per_step = statistics.median(ts)
     T = T_sample if cfg["ttype"] == 1 else 1
+    # M / t_total and M / t_spread (the spread / interp stage alone)
+    spread_s = statistics.median([x.get("spread", float("nan")) for x in sts])
+    stage.update({k: statistics.median([x.get(k, 0.0) for x in sts]) for k in ("sort", "spread", "fft", "correct")})
+    cpu_run.last = {"value_spread_stage": M_sample * T / spread_s if spread_s > 0 else None,
+                    "stages_s": stage}
     return M_sample * T / per_step, per_step, cores
 
 
@@ -642,7 +654,7 @@ def main():
                     cpu_baseline=dict({"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                                        "sample": f"{args.config} with M={Ms:.0e}, ntransf={Ts} per step "
                                                  "(oracle/ C+OpenMP restatement of the reference path, "
-                                                 "scipy pocketfft)"}, **cpu_info()),
+                                                 "scipy pocketfft)"}, **cpu_info(), **getattr(cpu_run, "last", {})),
                     e2e={"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
         line["n_gpus"] = args.gpus
         print(json.dumps(line), flush=True)
@@ -700,7 +712,7 @@ def main():
                 line["cpu_baseline"] = dict({"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                                              "sample": f"{args.config} with M={Ms:.0e}, ntransf={Ts}, one "
                                                        "full transform (oracle/ C+OpenMP port, scipy FFT)"},
-                                            **cpu_info())
+                                            **cpu_info(), **getattr(cpu_run, "last", {}))
             except Exception as exc:  # the baseline must never sink the GPU line
                 line["cpu_baseline"] = {"value": None, "error": str(exc)[:200]}
         print(json.dumps(line), flush=True)
