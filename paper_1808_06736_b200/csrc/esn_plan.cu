@@ -274,6 +274,14 @@ static void choose_bins(esn_plan p) {
         if (dim == 2) {
             bs[0] = 32;
             bs[1] = 32;
+            static const char *be = getenv("ESN_T2_BIN");  // "WxH": 2D interpolation bin (cells)
+            if (be) {
+                int bw = 0, bh = 0;
+                if (sscanf(be, "%dx%d", &bw, &bh) == 2 && bw > 0 && bh > 0) {
+                    bs[0] = bw;
+                    bs[1] = bh;
+                }
+            }
         } else {
             bs[0] = 16;
             bs[1] = 8;
