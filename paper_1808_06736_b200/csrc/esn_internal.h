@@ -67,6 +67,7 @@ struct SetptsArgs {
     int64_t chunk_len;      // > 0: points per target chunk (key major part)
     double inv_chunk;       // 1 / chunk_len
     double inv_bs[3];       // 1 / bs (fast division, corrected exactly)
+    int bs_log2[3];         // log2 bs when bs is a power of two, else -1
     int64_t M;
     int coord_f32;          // input coordinates are float (else double)
     int grid_units;         // coordinates already in grid units [0, n) (no fold)

@@ -798,6 +798,8 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
     for (int d = 0; d < 3; ++d) {
         a.sbl[d] = p->sbl[d];
         a.inv_bs[d] = 1.0 / (double)p->geom.bs[d];
+        const int b = p->geom.bs[d];
+        a.bs_log2[d] = (b > 0 && (b & (b - 1)) == 0) ? __builtin_ctz((unsigned)b) : -1;
     }
     a.spb = p->spb;
     a.nkeys = p->nkeys;

@@ -128,7 +128,8 @@ __device__ __forceinline__ int point_key(const SetptsArgs &a, int64_t i, const d
         int i0 = __double2int_rd(g - 0.5 * a.g.w + 1.0);  // floor (spreadinterp.py:117-120)
         if (i0 < 0) i0 += a.g.n[d];
         const int bs = a.g.bs[d];
-        const int q = fast_div(i0, bs, a.inv_bs[d]);
+        // power-of-two bins (the interpolation bins): shifts, else a float64 reciprocal
+        const int q = a.bs_log2[d] >= 0 ? i0 >> a.bs_log2[d] : fast_div(i0, bs, a.inv_bs[d]);
         bin += q * bmul;
         bmul *= a.g.nb[d];
         loc += ((i0 - q * bs) >> a.sbl[d]) * lmul;
