@@ -1541,6 +1541,7 @@ static int pipelined(HostSlot *slot, int type, int dim, int64_t M, const double 
         if (type == 1) {
             if (c64in && (rc = launch_upcast_c64(stage64(lo), blk, cnt * T, hs))) return rc;
             if ((rc = do_spread(q, blk, p->grid, false))) return rc;
+            if (trace) cudaEventRecord(tev[2][k], hs);
         } else {
             if ((rc = do_interp(q, p->grid, blk))) return rc;
             ESN_CUDA_TRY(cudaEventRecord(slot->ev_comp[k], hs));
@@ -1569,12 +1570,19 @@ static int pipelined(HostSlot *slot, int type, int dim, int64_t M, const double 
                 std::chrono::duration<double, std::milli>(t_enq - t_start).count(),
                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_enq).count());
         cudaDeviceSynchronize();
-        for (int k = 0; k < K && type == 2; ++k) {
+        for (int k = 0; k < K; ++k) {
             float a = 0, b = 0, d = 0;
             cudaEventElapsedTime(&a, tev[0][0], tev[1][k]);
             cudaEventElapsedTime(&b, tev[0][0], tev[2][k]);
-            cudaEventElapsedTime(&d, tev[0][0], tev[3][k]);
+            if (type == 2) cudaEventElapsedTime(&d, tev[0][0], tev[3][k]);
             fprintf(stderr, "[esn]   chunk %2d: up %.3f  comp %.3f  down %.3f ms\n", k, a, b, d);
+        }
+        if (type == 1) {  // FFT + deconvolution + download of the modes on the plan stream
+            cudaEventRecord(tev[3][K], st);
+            cudaEventSynchronize(tev[3][K]);
+            float e = 0;
+            cudaEventElapsedTime(&e, tev[0][0], tev[3][K]);
+            fprintf(stderr, "[esn]   done (FFT, deconvolution, D2H): %.3f ms\n", e);
         }
         cudaGetLastError();  // (events a transfer-only probe never recorded)
     }
