@@ -555,7 +555,7 @@ __device__ __forceinline__ int rows3_run(typename Cx<T>::type *acc, const unsign
     return i;
 }
 
-template <typename T, int W>
+template <typename T, int W, bool ROLL = false>
 __global__ void __launch_bounds__(Rows3Cfg<T, W>::NT, Rows3Cfg<T, W>::MINB) k_spread_rows3(SpreadArgs<T> a) {
     using C = typename Cx<T>::type;
     using Cfg = Rows3Cfg<T, W>;
@@ -589,17 +589,56 @@ __global__ void __launch_bounds__(Rows3Cfg<T, W>::NT, Rows3Cfg<T, W>::MINB) k_sp
     // lane-constant operand bases (entries carry the per-point parts, biased by EBIAS)
     static_assert(Cfg::PAD, "two-word entries index the zero-padded r2 / c * r3");
     const unsigned char *base_f = smem_raw + (int)sizeof(T) * (ry - Cfg::EBIAS);
+    // rz_eff: the lane's z row relative to the current bin's first plane
+    // (= rz, except in the z-rolling mode below where the lane's plane stays
+    // fixed while the bins advance)
+    int rz_eff = rz;
     const unsigned char *base_cz = smem_raw + (int)sizeof(C) * (rz - Cfg::EBIAS);
     uint64_t pol_first, pol_last;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
-    for (;;) {
-        if (tid == 0) s_sub = atomicAdd(a.work, 1);
-        __syncthreads();
-        const int s = s_sub;
-        __syncthreads();
-        if (s >= nsub) break;
+    C acc[X];
+#pragma unroll
+    for (int x = 0; x < X; ++x) acc[x] = C{(T)0, (T)0};
+    // flush of the tile rows whose rz_eff < zcount (all rows: zcount = RZ)
+    // through the shared-memory slab (aliases the stages): coalesced REDs
+    auto flush_planes = [&](int t, int lo1, int lo2, int lo3, int zcount) {
+        C *grid = reinterpret_cast<C *>(a.grid) + (int64_t)t * a.gstride;
+        constexpr int ZS = RZ / Cfg::FP;  // z rows per pass
+#pragma unroll 1
+        for (int zlo = 0; zlo < zcount; zlo += ZS) {
+            const int zn = min(ZS, zcount - zlo);
+            if (rz_eff >= zlo && rz_eff < zlo + zn) {
+                C *dst = s_tile + ((rz_eff - zlo) * RY + ry) * X;
+#pragma unroll
+                for (int x = 0; x < X; ++x) dst[x] = acc[x];
+            }
+            __syncthreads();
+            for (int i = tid; i < zn * RY * X; i += NT) {
+                const C v = s_tile[i];
+                if (v.x == (T)0 && v.y == (T)0) continue;
+                const int row = i / X, x = i - row * X;
+                const int yy = row % RY, zz = zlo + row / RY;
+                int g1 = lo1 + x;
+                while (g1 >= n1) g1 -= n1;
+                int g2 = lo2 + yy;
+                while (g2 >= n2) g2 -= n2;
+                int g3 = lo3 + zz;
+                while (g3 >= n3) g3 -= n3;
+                red_add(grid + ((int64_t)g3 * n2 + g2) * n1 + g1, v);
+            }
+            __syncthreads();
+        }
+        if (rz_eff < zcount) {
+#pragma unroll
+            for (int x = 0; x < X; ++x) acc[x] = C{(T)0, (T)0};
+        }
+    };
+    // one subproblem's points into acc; unless rolling, each transform's
+    // tile is flushed whole when its last chunk is done
+    auto run_sub = [&](int s, bool rolling) __attribute__((always_inline)) {
         const int4 sp = a.subprob[s];
+
         const int bin = sp.x, start = sp.y, cnt = sp.z;
         const int b1 = bin % a.g.nb[0];
         const int b2 = (bin / a.g.nb[0]) % a.g.nb[1];
@@ -704,39 +743,6 @@ __global__ void __launch_bounds__(Rows3Cfg<T, W>::NT, Rows3Cfg<T, W>::MINB) k_sp
             __syncwarp();
             nq = n;
         };
-        C acc[X];
-#pragma unroll
-        for (int x = 0; x < X; ++x) acc[x] = C{(T)0, (T)0};
-        auto flush = [&](int t) {
-            C *grid = reinterpret_cast<C *>(a.grid) + (int64_t)t * a.gstride;
-            constexpr int ZS = RZ / Cfg::FP;  // z rows per pass
-#pragma unroll 1
-            for (int p = 0; p < Cfg::FP; ++p) {
-                const int zlo = p * ZS;
-                if (rz >= zlo && rz < zlo + ZS) {
-                    C *dst = s_tile + ((rz - zlo) * RY + ry) * X;
-#pragma unroll
-                    for (int x = 0; x < X; ++x) dst[x] = acc[x];
-                }
-                __syncthreads();
-                for (int i = tid; i < ZS * RY * X; i += NT) {
-                    const C v = s_tile[i];
-                    if (v.x == (T)0 && v.y == (T)0) continue;
-                    const int row = i / X, x = i - row * X;
-                    const int yy = row % RY, zz = zlo + row / RY;
-                    int g1 = lo1 + x;
-                    while (g1 >= n1) g1 -= n1;
-                    int g2 = lo2 + yy;
-                    while (g2 >= n2) g2 -= n2;
-                    int g3 = lo3 + zz;
-                    while (g3 >= n3) g3 -= n3;
-                    red_add(grid + ((int64_t)g3 * n2 + g2) * n1 + g1, v);
-                }
-                __syncthreads();
-            }
-#pragma unroll
-            for (int x = 0; x < X; ++x) acc[x] = C{(T)0, (T)0};
-        };
         // prologue: step 0 staged and listed
         issue_rec(0);
         cp_async_wait<0>();
@@ -779,15 +785,116 @@ __global__ void __launch_bounds__(Rows3Cfg<T, W>::NT, Rows3Cfg<T, W>::MINB) k_sp
                 }
             }
             cp_async_wait<1>();  // own strength of step st + 1
-            if ((st + 1) % nck == 0) {  // transform st / nck complete
+            if (!rolling && (st + 1) % nck == 0) {  // transform st / nck complete
                 __syncthreads();
-                flush(st / nck);
+                flush_planes(st / nck, lo1, lo2, lo3, RZ);
             }
             phase_a(st + 1);
             __syncthreads();
             if (st + 1 < nsteps) build_list(st + 1);
         }
         cp_async_wait<0>();
+    };
+    const int nb0 = a.g.nb[0], nb1 = a.g.nb[1], nb2 = a.g.nb[2];
+    const int nbins = nb0 * nb1 * nb2;
+    auto nsub_of = [&](int bin) { return (bin + 1 < nbins ? a.subofs[bin + 1] : nsub) - a.subofs[bin]; };
+    // a bin is rolled when it is one subproblem of at most ROLLMAX points:
+    // larger bins (clustered data, large pipeline chunks) stay independent
+    // subproblems so no segment carries many times a CTA's share of the work
+    constexpr int ROLLMAX = 1024;
+    auto rolled = [&](int bin) {
+        return nsub_of(bin) == 1 && a.bin_start[bin + 1] - a.bin_start[bin] <= ROLLMAX;
+    };
+    auto claim = [&](int q) {  // next item of work queue q (CTA-uniform)
+        if (tid == 0) s_sub = atomicAdd(a.work + q, 1);
+        __syncthreads();
+        const int v = s_sub;
+        __syncthreads();
+        return v;
+    };
+    // Work: plain mode -- every subproblem of queue 0 with a whole-tile
+    // flush.  z-rolling mode (thin tiles, one transform): queue 0 holds
+    // columns (b1, b2) x segments of ZB bins along z.  A bin's tile is planes
+    // [lo3, lo3 + RZ); after the bin only its first BZ planes are complete,
+    // so only those rows are flushed and the lanes holding them take over the
+    // next bin's top planes (a lane's plane stays fixed, rz_eff = (plane -
+    // lo3) mod RZ): BZ / RZ of the tile per bin instead of all of it.  Bins
+    // split into several subproblems (clustered points) go to queue 1, whose
+    // subproblems run one by one with whole-tile flushes.  One call site of
+    // run_sub (code size).
+    // segment length: up to 8 bins, fewer when that would leave under ~8
+    // segments per CTA (tail balance)
+    constexpr int ZBMAX = 8;
+    __shared__ int s_nsb[ZBMAX], s_sof[ZBMAX];
+    const int ZB = max(1, min(ZBMAX, nbins / (8 * (int)gridDim.x)));
+    // (ROLL is a template flag: the plain instantiation keeps rz_eff == rz
+    // a constant and the rolling driver out of its code)
+    const bool roll = ROLL && WZ == 1 && a.ntransf == 1 && a.subofs != nullptr;
+    const int BZ = a.g.bs[2];
+    const int nitems = nb0 * nb1 * ((nb2 + ZB - 1) / ZB);
+    const int reach = (RZ - 1) / BZ;  // bins before b3 whose tiles reach b3's first plane
+    int phase = roll ? 0 : 2;
+    int b3 = 0, b3s = 0, b3b = 0, lo1r = 0, lo2r = 0, lo3r = 0, last_pts = -1000000;
+    for (;;) {
+        int s = -1;
+        if (phase == 0) {
+            if (b3 >= b3b) {  // next segment
+                const int item = claim(0);
+                if (item >= nitems) {
+                    phase = 1;
+                    if constexpr (ROLL) {
+                        rz_eff = rz;
+                        base_cz = smem_raw + (int)sizeof(C) * (rz - Cfg::EBIAS);
+                    }
+                    continue;
+                }
+                const int b1 = item % nb0, b2 = (item / nb0) % nb1, seg = item / (nb0 * nb1);
+                lo1r = b1 * a.g.bs[0];
+                lo2r = b2 * a.g.bs[1];
+                b3 = b3s = seg * ZB;
+                b3b = min(nb2, b3 + ZB);
+                lo3r = b3 * BZ;
+                last_pts = -1000000;
+                if constexpr (ROLL) {
+                    rz_eff = ((rz - lo3r) % RZ + RZ) % RZ;
+                    base_cz = smem_raw + (int)sizeof(C) * (rz_eff - Cfg::EBIAS);
+                }
+                // the segment's subproblem counts, loaded at once (empty
+                // columns then cost one memory latency, not one per bin)
+                if (tid < b3b - b3) {
+                    const int bin = b1 + nb0 * (b2 + nb1 * (b3 + tid));
+                    s_sof[tid] = a.subofs[bin];
+                    s_nsb[tid] = rolled(bin) ? 1 : 0;
+                }
+                __syncthreads();
+            }
+            if (s_nsb[b3 - b3s] == 1) s = s_sof[b3 - b3s];
+        } else if (phase == 1) {
+            s = claim(1);
+            if (s >= nsub) break;
+            const int bin = a.subprob[s].x;
+            if (rolled(bin) || nsub_of(bin) == 0) continue;  // (done by a segment)
+        } else {
+            s = claim(0);
+            if (s >= nsub) break;
+        }
+        if (s >= 0) run_sub(s, phase == 0);
+        if (phase == 0) {
+            if (s >= 0) last_pts = b3;
+            // the bin's first BZ planes are complete (all of them at the
+            // segment end); nothing to flush unless a bin with points reached them
+            const bool last = b3 + 1 >= b3b;
+            if (last_pts >= b3 - reach) {
+                __syncthreads();
+                flush_planes(0, lo1r, lo2r, lo3r, last ? RZ : BZ);
+            }
+            ++b3;
+            lo3r += BZ;
+            if constexpr (ROLL) {
+                rz_eff = ((rz - lo3r) % RZ + RZ) % RZ;
+                base_cz = smem_raw + (int)sizeof(C) * (rz_eff - Cfg::EBIAS);
+            }
+        }
     }
 }
 

@@ -65,13 +65,23 @@ struct SpreadRowsOp {
             }();
             if (!old_rows) {
                 using Cfg3 = Rows3Cfg<T, W>;
-                static PerDev<int> grid3_;
-                int &grid3 = grid3_();
-                if (grid3 == 0) {
-                    int rc = persistent_launch(k_spread_rows3<T, W>, Cfg3::NT, Cfg3::SMEM, st, nullptr, &grid3);
-                    if (rc) return rc;
+                if (Cfg3::R::THIN && a.roll && a.ntransf == 1) {  // z-rolling segments (small bins, w <= 7)
+                    static PerDev<int> gridr_;
+                    int &gridr = gridr_();
+                    if (gridr == 0) {
+                        int rc = persistent_launch(k_spread_rows3<T, W, true>, Cfg3::NT, Cfg3::SMEM, st, nullptr, &gridr);
+                        if (rc) return rc;
+                    }
+                    k_spread_rows3<T, W, true><<<gridr, Cfg3::NT, Cfg3::SMEM, st>>>(a);
+                } else {
+                    static PerDev<int> grid3_;
+                    int &grid3 = grid3_();
+                    if (grid3 == 0) {
+                        int rc = persistent_launch(k_spread_rows3<T, W, false>, Cfg3::NT, Cfg3::SMEM, st, nullptr, &grid3);
+                        if (rc) return rc;
+                    }
+                    k_spread_rows3<T, W, false><<<grid3, Cfg3::NT, Cfg3::SMEM, st>>>(a);
                 }
-                k_spread_rows3<T, W><<<grid3, Cfg3::NT, Cfg3::SMEM, st>>>(a);
                 ESN_CUDA_TRY(cudaGetLastError());
                 return ESN_SUCCESS;
             }

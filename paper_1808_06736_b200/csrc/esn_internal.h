@@ -99,6 +99,8 @@ struct SpreadArgs {
     int spb;                 // sub-cells per bin
     int sbl[3];              // log2 sub-cell size per dim
     const int *nsub;         // device count of subproblems
+    const int *subofs;       // first subproblem of every bin (type 1; nullptr: unused)
+    int roll;                // 3D row spreader: z-rolling segments (small bins on average)
     int *work;               // work-queue counter (zeroed before launch)
     const T *c;              // (ntransf, M) interleaved complex
     T *grid;                 // (ntransf, n3, n2, n1) interleaved complex

@@ -873,6 +873,14 @@ static SpreadArgs<T> make_spread_args(esn_plan p, const void *c, void *grid) {
     a.spb = p->spb;
     for (int d = 0; d < 3; ++d) a.sbl[d] = p->sbl[d];
     a.nsub = p->nsub;
+    a.subofs = p->type == 2 ? nullptr : p->subofs;
+    // z-rolling pays where bins hold a few hundred points (c3: ~490; its
+    // host-pipeline chunks ~100); c3f's ~2000-point bins gain nothing from it
+    static const int roll_env = [] {
+        const char *e = getenv("ESN_ROLL3");
+        return e ? atoi(e) : -1;
+    }();
+    a.roll = roll_env >= 0 ? roll_env : (p->nbins > 0 && p->M <= (int64_t)512 * p->nbins);
     a.work = p->work;
     a.c = (const T *)c;
     a.grid = (T *)grid;
@@ -934,7 +942,7 @@ static int do_spread(esn_plan p, const void *c, void *grid, bool zero = true) {
     const bool owner = esn::batched_owner(p->dtype, p->dim, p->kp.w, p->ntransf, method, p->sbl, p->geom.bs);
     if (zero && !owner)
         ESN_CUDA_TRY(cudaMemsetAsync(grid, 0, real_size(p->dtype) * 2 * (size_t)p->G * p->ntransf, p->st));
-    ESN_CUDA_TRY(cudaMemsetAsync(p->work, 0, sizeof(int), p->st));
+    ESN_CUDA_TRY(cudaMemsetAsync(p->work, 0, sizeof(int) * 2, p->st));  // (two work queues)
     if (p->have_events) ESN_CUDA_TRY(rec_ev(p, p->ev[6], p->st));
     int rc;
     if (p->dtype == ESN_F64) {
