@@ -101,6 +101,20 @@ def algorithmic_bytes(cfg, M, T):
     return M * cfg["dim"] * sr + T * M * sc + T * G * sc, G
 
 
+# measured FMA peaks of the box (tools/micro/fma_peak.cu; profiles/r01/fma_peak.txt)
+FMA_PEAK = {"float64": 1.7e13, "float32": 3.57e13}
+
+
+def algorithmic_fma(cfg, M, T):
+    """FMAs the spread / interp kernel must issue: the ES rows by Horner
+    (d w (w + 3) per point, shared by the transforms) plus the separable
+    complex accumulation 2 (w + w^2 + ... + w^d) per point and transform."""
+    w, d = select_w(cfg), cfg["dim"]
+    rows = d * w * (w + 3)
+    acc = 2 * sum(w ** k for k in range(1, d + 1))
+    return M * rows + M * T * acc
+
+
 def select_w(cfg):
     return min(max(math.ceil(math.log10(1.0 / cfg["tol"])) + 1, 2), 16)
 
@@ -372,6 +386,7 @@ def gpu_run(args, name, rank, world, local_rank, *, steps, warmup, reduce, e2e, 
     peak, peak_kind = peaks()
     res = dict(value=value, elapsed=elapsed, steps=steps, hot_s=hot_s, achieved=B / hot_s / 1e9, peak=peak,
                mode=mode, M=M, peak_kind=peak_kind, B=B, G=G, clocks=clk.summary(), reduce=reduce,
+               fma=algorithmic_fma(cfg, Mr, Tr),
                stages={k: v / steps for k, v in st.items()} if not args.stage_sync
                else {k: v / steps for k, v in stages.items()})
     plan.close()
@@ -576,6 +591,13 @@ def line_for(args, name, res, world, base):
                           "binding": BINDING.get(name)},
                 stages_ms={k: v * 1e3 for k, v in res["stages"].items()},
                 clocks=res["clocks"], gpu_launches=n_launches(cfg) * res["steps"])
+    if "fma" in res:  # the compute roof beside the HBM one (which binds for fp64 interp / 3D spread)
+        fpk = FMA_PEAK["float32" if cfg["dtype"] == "float32" else "float64"]
+        ach = res["fma"] / res["hot_s"]
+        line["roofline"]["compute"] = {"unit": "FMA/s", "algorithmic_fma": res["fma"], "achieved": ach,
+                                       "peak": fpk, "frac": ach / fpk,
+                                       "peak_source": "measured on a B200 (tools/micro/fma_peak.cu, "
+                                                      "profiles/r01/fma_peak.txt)"}
     if traffic is not None:
         line["roofline"]["traffic_source"] = "profiles/traffic.json (ncu dram__bytes_read+write of this kernel)"
         try:  # was it measured on the library being benched? (tools/kernel_table.py)
