@@ -112,7 +112,7 @@ def clear_plan_cache(key: FftPlanKey | None = None) -> None:
             gone = [p for ck, p in _cache.items() if ck[0] == key]
             for ck in [ck for ck in _cache if ck[0] == key]:
                 del _cache[ck]
-    if gone or key is None:
+    if (gone or key is None) and torch.cuda.is_available() and torch.cuda.is_initialized():
         torch.cuda.synchronize()  # no FFT of a dropped plan may still be running
     for p in gone:
         p._destroy()
