@@ -108,3 +108,17 @@ def test_plan_without_gpu_fails_loudly():
         pytest.skip("GPU present")
     with pytest.raises(E.InternalError):
         E.nufft1d1(np.zeros(3), np.ones(3, complex), 8)
+
+
+def test_fft_plan_cache_api_without_gpu():
+    """fft.py:99-111 surface: the cache starts empty, clear_plan_cache (all
+    or one key) and plan_cache_size work on a host without a GPU; plans
+    themselves are built on first use on the device (test_gpu_properties)."""
+    from paper_1808_06736_b200 import fft
+    from paper_1808_06736_b200.errors import SizeError
+    fft.clear_plan_cache()
+    assert fft.plan_cache_size() == 0
+    fft.clear_plan_cache(fft.FftPlanKey((8, 8), fft.FORWARD))
+    assert fft.plan_cache_size() == 0
+    with pytest.raises(SizeError):
+        fft.FftPlanKey((8,), "sideways")
