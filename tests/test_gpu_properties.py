@@ -290,3 +290,37 @@ def test_spread_interp_stats(esn):
     st2 = {}
     S.interp(pts, g, kp, stats=st2)
     assert st2["tasks"] >= 1 and st2["busy_per_thread"][0] > 0
+
+
+@pytest.mark.gpu
+def test_error_tracks_tolerance(esn, oracle):
+    """Reference tests/test_transforms.py error_tracks_tolerance_slope: the
+    achieved error against the exact sum falls with the requested tolerance,
+    log-log slope close to 1, and stays within 10 tol."""
+    rng = np.random.default_rng(6)
+    m, nm = 400, (60,)
+    x = [rng.uniform(-np.pi, np.pi, m)]
+    c = rng.standard_normal(m) + 1j * rng.standard_normal(m)
+    exact = oracle.direct_type1(x, c, nm)
+    tols = [1e-3, 1e-5, 1e-7, 1e-9, 1e-11]
+    errs = []
+    for tol in tols:
+        got, _ = esn.exec_type1(x, c, nm, esn.TransformOptions(tolerance=tol))
+        errs.append(max(float(np.linalg.norm(got - exact) / np.linalg.norm(exact)), 1e-16))
+    slope = np.polyfit(np.log10(tols), np.log10(errs), 1)[0]
+    assert 0.7 <= slope <= 1.2, (slope, errs)
+    assert all(e <= 10 * t for e, t in zip(errs, tols)), errs
+
+
+@pytest.mark.gpu
+def test_timings_reported(esn):
+    """exec_type1/2 return the reference's stage keys with device seconds."""
+    rng = np.random.default_rng(9)
+    x = [rng.uniform(-np.pi, np.pi, 2000) for _ in range(2)]
+    c = rng.standard_normal(2000) + 1j * rng.standard_normal(2000)
+    _, t1 = esn.exec_type1(x, c, (32, 24), esn.TransformOptions(tolerance=1e-6))
+    f = rng.standard_normal((24, 32)) + 1j * rng.standard_normal((24, 32))
+    _, t2 = esn.exec_type2(x, f, esn.TransformOptions(tolerance=1e-6))
+    for t in (t1, t2):
+        assert set(t) == {"sort", "spread", "fft", "correct"}
+        assert all(v >= 0.0 for v in t.values()) and t["spread"] > 0.0
