@@ -324,3 +324,26 @@ def test_timings_reported(esn):
     for t in (t1, t2):
         assert set(t) == {"sort", "spread", "fft", "correct"}
         assert all(v >= 0.0 for v in t.values()) and t["spread"] > 0.0
+
+
+@pytest.mark.gpu
+def test_type2_worst_case_bounded_by_l1_norm(esn, oracle):
+    """Reference test_transforms.py type2_worst_case_bounded_by_l1_norm: the
+    aliasing probe (type 1 of every unit strength against the exact sum,
+    oracle.py aliasing_probe -- here one batched call with the identity as
+    strengths) bounds the type-2 error for any modes: max |c~ - c| <=
+    2 max|E| ||f||_1 (linearity; the type-2 map is the transpose)."""
+    from paper_1808_06736_b200.kernel import params_for_width
+    rng = np.random.default_rng(7)
+    m, n = 32, 32
+    x = rng.uniform(-np.pi, np.pi, m)
+    p = params_for_width(7, 2.0)
+    o = esn.TransformOptions(params=p)
+    unit = np.eye(m, dtype=np.complex128)
+    fast1, _ = esn.exec_type1((x,), unit, (n,), o)
+    exact1 = np.stack([oracle.direct_type1([x], unit[j], (n,)) for j in range(m)])
+    eps = float(np.abs(fast1 - exact1).max())
+    f = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    fast2, _ = esn.exec_type2((x,), f, o)
+    exact2 = oracle.direct_type2([x], f)
+    assert np.abs(fast2 - exact2).max() <= 2.0 * eps * np.abs(f).sum()
