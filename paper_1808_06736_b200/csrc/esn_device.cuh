@@ -124,6 +124,32 @@ __device__ __forceinline__ void red_add(float2 *p, float2 v) {
     atomicAdd(p, v);  // sm_90+: one vector RED.F32x2 per complex cell
 }
 
+// acc + v * w and v * w on an interleaved complex value.  float32: one packed
+// FFMA2 / FMUL2 (fma.rn.f32x2, sm_100+: the scalar w is a broadcast operand in
+// SASS) -- the same FMA-pipe time as two FFMAs in half the issue slots; each
+// lane of the pair rounds like fmaf, so results are unchanged.
+__device__ __forceinline__ float2 cfma(float2 v, float w, float2 acc) {
+    const float2 ww = make_float2(w, w);
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(d)
+        : "l"(*reinterpret_cast<const unsigned long long *>(&v)), "l"(*reinterpret_cast<const unsigned long long *>(&ww)),
+          "l"(*reinterpret_cast<const unsigned long long *>(&acc)));
+    return *reinterpret_cast<float2 *>(&d);
+}
+__device__ __forceinline__ float2 cmul(float2 v, float w) {
+    const float2 ww = make_float2(w, w);
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;"
+        : "=l"(d)
+        : "l"(*reinterpret_cast<const unsigned long long *>(&v)), "l"(*reinterpret_cast<const unsigned long long *>(&ww)));
+    return *reinterpret_cast<float2 *>(&d);
+}
+__device__ __forceinline__ double2 cfma(double2 v, double w, double2 acc) {
+    return double2{fma(v.x, w, acc.x), fma(v.y, w, acc.y)};
+}
+__device__ __forceinline__ double2 cmul(double2 v, double w) { return double2{v.x * w, v.y * w}; }
+
 template <typename T>
 __device__ __forceinline__ bool finite2(typename Cx<T>::type v) {
     return isfinite(v.x) && isfinite(v.y);
@@ -497,7 +523,7 @@ __device__ __forceinline__ void rows3_apply(typename Cx<T>::type *acc, const uns
     using C = typename Cx<T>::type;
     using Cfg = Rows3Cfg<T, W>;
     const T *rec = reinterpret_cast<const T *>(stage + 16u * p.off);
-    const C v{p.cz.x * p.f, p.cz.y * p.f};
+    const C v = cmul(p.cz, p.f);
     T r1[Cfg::R1N];
     if constexpr (sizeof(T) == 8) {
 #pragma unroll
@@ -517,10 +543,7 @@ __device__ __forceinline__ void rows3_apply(typename Cx<T>::type *acc, const uns
         }
     }
 #pragma unroll
-    for (int m = 0; m < W; ++m) {
-        acc[OX + m].x = fma(v.x, r1[m], acc[OX + m].x);
-        acc[OX + m].y = fma(v.y, r1[m], acc[OX + m].y);
-    }
+    for (int m = 0; m < W; ++m) acc[OX + m] = cfma(v, r1[m], acc[OX + m]);
 }
 
 // one run of equal x offset OX from the warp list; bit 31 of an entry's first
@@ -1938,7 +1961,7 @@ __global__ void __launch_bounds__(128, 3) k_spread_b2roll(SpreadArgs<T> a, const
                 const float2 cc = lds_f2(cb + k * CB);
                 C v[W];
 #pragma unroll
-                for (int dy = 0; dy < W; ++dy) v[dy] = C{cc.x * r2[dy], cc.y * r2[dy]};
+                for (int dy = 0; dy < W; ++dy) v[dy] = cmul(cc, r2[dy]);
                 int cs = i1 - xb;
                 if (cs < 0) cs += n1;
 #define ESN_ROLL_CASE(CS)                                                                 \
@@ -1948,8 +1971,7 @@ __global__ void __launch_bounds__(128, 3) k_spread_b2roll(SpreadArgs<T> a, const
                 constexpr int XL = CS - H;                                                \
                 if (XL + m >= 0 && XL + m < BXS) {                                        \
                     _Pragma("unroll") for (int dy = 0; dy < W; ++dy) {                    \
-                        acc[dy][XL + m].x = fma(v[dy].x, r1[m], acc[dy][XL + m].x);       \
-                        acc[dy][XL + m].y = fma(v[dy].y, r1[m], acc[dy][XL + m].y);       \
+                        acc[dy][XL + m] = cfma(v[dy], r1[m], acc[dy][XL + m]);            \
                     }                                                                     \
                 }                                                                         \
             }                                                                             \
