@@ -2019,7 +2019,7 @@ struct InterpUnit {
 // P_d <= n_d (each patch row wraps at most once).
 template <typename T, int DIM, int W>
 __global__ void __launch_bounds__(256, interp_minb<DIM, W>())
-    k_interp_bulk(SpreadArgs<T> a, T *cout, const T *gridp, int slice, int dprod) {
+    k_interp_bulk(SpreadArgs<T> a, T *cout, const T *gridp, int slice, int dprod, int pitch1) {
     using C = typename Cx<T>::type;
     extern __shared__ __align__(16) unsigned char bulk_smem[];
     __shared__ uint64_t s_full[2], s_empty[2];
@@ -2033,7 +2033,10 @@ __global__ void __launch_bounds__(256, interp_minb<DIM, W>())
     const int P1 = a.g.bs[0] + W - 1;
     const int P2 = DIM > 1 ? a.g.bs[1] + W - 1 : 1;
     const int P3 = DIM > 2 ? a.g.bs[2] + W - 1 : 1;
-    const int ncell = P1 * P2 * P3;
+    // pitch1 >= P1: patch row pitch in cells (a multiple of 8 cells = 128
+    // bytes keeps a quarter-warp that runs off a bin row's end onto the next
+    // row on distinct banks)
+    const int ncell = pitch1 * P2 * P3;
     Rec *const rec0 = reinterpret_cast<Rec *>(bulk_smem);              // 2 x slice records
     C *const patch0 = reinterpret_cast<C *>(rec0 + 2 * slice);         // 2 x ncell cells
     const int nsub = *a.nsub;
@@ -2077,8 +2080,9 @@ __global__ void __launch_bounds__(256, interp_minb<DIM, W>())
             s_unit[rb] = u;
             // arrival (release) publishes s_unit[rb]; the phase completes when
             // the copies' bytes have landed
-            mbar_expect_tx(&s_full[rb], valid ? (uint32_t)u.n * sizeof(Rec) + (fresh ? (uint32_t)ncell * sizeof(C) : 0u)
-                                              : 0u);
+            mbar_expect_tx(&s_full[rb],
+                           valid ? (uint32_t)u.n * sizeof(Rec) + (fresh ? (uint32_t)(P1 * P2 * P3) * sizeof(C) : 0u)
+                                 : 0u);
         }
         fresh = __shfl_sync(0xffffffffu, fresh, 0);
         valid = __shfl_sync(0xffffffffu, valid, 0);
@@ -2098,7 +2102,7 @@ __global__ void __launch_bounds__(256, interp_minb<DIM, W>())
                 if (g2 >= n2) g2 -= n2;
                 if (g3 >= n3) g3 -= n3;
                 const C *row = grid + ((int64_t)g3 * n2 + g2) * n1;
-                C *dst = patch0 + pb * ncell + r * P1;
+                C *dst = patch0 + pb * ncell + r * pitch1;
                 bulk_g2s(dst, row + lo1, (uint32_t)head * sizeof(C), &s_full[rb]);
                 if (head < P1) bulk_g2s(dst + head, row, (uint32_t)(P1 - head) * sizeof(C), &s_full[rb]);
             }
@@ -2137,8 +2141,24 @@ __global__ void __launch_bounds__(256, interp_minb<DIM, W>())
         if (!u.valid) break;
         const Rec *recs = rec0 + rb * slice;
         const C *patch = patch0 + u.pb * ncell;
+        // a quarter-warp's eight 32-byte records: lanes 0-3 fetch the first
+        // half then the second, lanes 4-7 the second then the first, so each
+        // 128-bit load covers eight distinct 16-byte bank groups (all-first
+        // halves sit on four of them: 2-way conflicts, 8-way for a 32-bit
+        // load of j)
+        const int hsel = (lane >> 2) & 1;
         for (int kk = tid; kk < u.n; kk += cthreads) {
-            const Rec rc = recs[kk];
+            Rec rc;
+            {
+                const uint32_t ra = smem_u32(recs + kk) + 16u * hsel;
+                long long ax, ay, bx, by;
+                asm volatile("ld.shared.v2.s64 {%0, %1}, [%2];" : "=l"(ax), "=l"(ay) : "r"(ra));
+                asm volatile("ld.shared.v2.s64 {%0, %1}, [%2];" : "=l"(bx), "=l"(by) : "r"(ra ^ 16u));
+                rc.g[0] = __longlong_as_double(hsel ? bx : ax);
+                rc.g[1] = __longlong_as_double(hsel ? by : ay);
+                rc.g[2] = __longlong_as_double(hsel ? ax : bx);
+                rc.j = (int)(unsigned)((hsel ? ay : by) & 0xffffffffll);
+            }
             T r1[W], r2[W], r3[W];
             const int i1 = kernel_row<T, W>(rc.g[0], a.k, r1);
             const int o1 = (i1 < 0 ? i1 + n1 : i1) - u.lo1;
@@ -2152,7 +2172,7 @@ __global__ void __launch_bounds__(256, interp_minb<DIM, W>())
                 o3 = (i3 < 0 ? i3 + n3 : i3) - u.lo3;
             }
             T are = 0, aim = 0;
-            const C *base = patch + (o3 * P2 + o2) * P1 + o1;
+            const C *base = patch + (o3 * P2 + o2) * pitch1 + o1;
             // 2D: rows unrolled (static r2 index; a select chain per row cost
             // 2 (w - 1) instructions); 3D keeps rolled loops (registers)
             constexpr int U2 = DIM == 2 ? W : 1;
@@ -2164,7 +2184,7 @@ __global__ void __launch_bounds__(256, interp_minb<DIM, W>())
                     T pre = 0, pim = 0;
 #pragma unroll
                     for (int m1 = 0; m1 < W; ++m1) {
-                        const C v = base[(m3 * P2 + m2) * P1 + m1];
+                        const C v = base[(m3 * P2 + m2) * pitch1 + m1];
                         pre = fma(r1[m1], v.x, pre);
                         pim = fma(r1[m1], v.y, pim);
                     }

@@ -194,7 +194,19 @@ struct InterpOp {
         }
         if constexpr (sizeof(C) == 16) if (fits && !(mode && std::string(mode) == "tile")) {
             static const char *sl = getenv("ESN_INTERP_SLICE");
-            const int slice = sl ? atoi(sl) : 512;
+            int slice = sl ? atoi(sl) : 512;
+            // patch row pitch: ESN_INTERP_PITCH=<cells> (>= bs + w - 1), 0 = rows packed;
+            // default a multiple of 8 cells (128 bytes) for D >= 2
+            static const char *pe = getenv("ESN_INTERP_PITCH");
+            const int P1 = a.g.bs[0] + W - 1;
+            int pitch1 = D >= 2 ? (P1 + 7) / 8 * 8 : P1;
+            if (pe) pitch1 = atoi(pe) > P1 ? atoi(pe) : P1;
+            cells = cells / (size_t)P1 * (size_t)pitch1;
+            // three CTAs per SM when the patches allow it: 228 KB less 1 KB
+            // reserved and the static words per CTA
+            constexpr size_t kThree = 233472 / 3 - 1024 - 256;
+            if (!sl)
+                while (slice > 256 && 2 * cells * sizeof(C) + 2 * (size_t)slice * sizeof(Rec) > kThree) slice -= 32;
             const size_t bsmem = 2 * cells * sizeof(C) + 2 * (size_t)slice * sizeof(Rec);
             if (bsmem <= 112 * 1024) {
                 static PerDev<size_t> bconf_;
@@ -211,7 +223,7 @@ struct InterpOp {
                     const char *e = getenv("ESN_INTERP_PRODUCER");
                     return e && e[0] == '0' ? 0 : 1;
                 }();
-                k_interp_bulk<T, D, W><<<device_sm_count() * occ, 256, bsmem, st>>>(a, cout, grid, slice, dprod);
+                k_interp_bulk<T, D, W><<<device_sm_count() * occ, 256, bsmem, st>>>(a, cout, grid, slice, dprod, pitch1);
                 ESN_CUDA_TRY(cudaGetLastError());
                 return ESN_SUCCESS;
             }
