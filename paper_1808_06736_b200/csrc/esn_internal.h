@@ -161,8 +161,15 @@ struct Batch2Cfg {
 };
 
 // ---- launchers (esn_kernels.cu)
+// aux (optional): a second stream and two events of the caller; the
+// subproblem tables (they need only the scanned bin starts) are then built
+// beside the record scatter instead of after it
+struct SetptsAux {
+    cudaStream_t st = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
 int launch_setpts(const SetptsArgs &a, int nbins, int max_subprob, int4 *subprob, int *nsub, int *subofs,
-                  cudaStream_t st);
+                  cudaStream_t st, const SetptsAux *aux = nullptr);
 constexpr int kScanTile = 4096;  // keys per scan block
 // records in original order, no sort (small 1D type-1 plans, global-atomic spreader)
 int launch_setpts_unsorted(const SetptsArgs &a, cudaStream_t st);

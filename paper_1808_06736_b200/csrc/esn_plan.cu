@@ -137,6 +137,8 @@ struct esn_plan_s {
     // of the sorted points join e_sorted on st first (join_sort)
     cudaStream_t st2 = nullptr;
     cudaEvent_t e_in = nullptr, e_sorted = nullptr;
+    // aux stream of setpts (subproblem tables beside the record scatter)
+    SetptsAux aux;
     bool sort_pending = false;
     // CUDA-graph replay of launch-bound calls (small M): the stream work of
     // setpts / execute is captured once per signature on a private stream
@@ -482,6 +484,12 @@ int esn_plan_destroy(esn_plan p) {
         cudaEventDestroy(p->e_sorted);
         cudaStreamDestroy(p->st2);
     }
+    if (p->aux.st) {
+        cudaStreamSynchronize(p->aux.st);
+        cudaEventDestroy(p->aux.fork);
+        cudaEventDestroy(p->aux.join);
+        cudaStreamDestroy(p->aux.st);
+    }
     if (p->gs) {
         cudaStreamSynchronize(p->gs);
         for (auto &g : p->gexec)
@@ -581,14 +589,42 @@ int esn_plan_create(int type, int dim, const int64_t *nmodes, int isign, int ntr
         return !(e && std::string(e) == "0");
     }();
     if (type == 2 && overlap) {
+        // the sort is the critical path of a type-2 step (the amplify + FFT
+        // beside it have slack): highest priority, so its small scan kernels
+        // do not queue behind the FFT's CTAs (ESN_SORT_PRIO=0: the plan
+        // stream's priority)
         int prio = 0;
         cudaStreamGetPriority(p->st, &prio);
+        static const bool high = [] {
+            const char *e = getenv("ESN_SORT_PRIO");
+            return !(e && e[0] == '0');
+        }();
+        if (high) {
+            int least = 0, greatest = 0;
+            if (cudaDeviceGetStreamPriorityRange(&least, &greatest) == cudaSuccess) prio = greatest;
+            else cudaGetLastError();
+        }
         if (cudaStreamCreateWithPriority(&p->st2, cudaStreamNonBlocking, prio) != cudaSuccess ||
             cudaEventCreateWithFlags(&p->e_in, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&p->e_sorted, cudaEventDisableTiming) != cudaSuccess) {
             cudaGetLastError();
             esn_plan_destroy(p);
             return fail(ESN_INTERNAL_ERROR, "side stream creation failed");
+        }
+    }
+    static const bool auxtab = [] {
+        const char *e = getenv("ESN_SORT_AUX");
+        return !(e && e[0] == '0');
+    }();
+    if (auxtab) {
+        int least = 0, greatest = 0;
+        if (cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) cudaGetLastError();
+        if (cudaStreamCreateWithPriority(&p->aux.st, cudaStreamNonBlocking, greatest) != cudaSuccess ||
+            cudaEventCreateWithFlags(&p->aux.fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&p->aux.join, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            esn_plan_destroy(p);
+            return fail(ESN_INTERNAL_ERROR, "aux stream creation failed");
         }
     }
     *out = p;
@@ -775,12 +811,16 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
     // (the previous execute may still read the records this sort rewrites)
     cudaStream_t ss = p->st;
     if (side) {
+        // the fill cursors are touched by the sort only (side stream): clear
+        // them before joining the plan stream, i.e. beside the previous
+        // execute instead of after it (c2: 16 MB, ~9 us off the step)
+        ESN_CUDA_TRY(cudaMemsetAsync(p->key_count, 0, sizeof(int) * p->nkeys, p->st2));
         ESN_CUDA_TRY(cudaEventRecord(p->e_in, p->st));
         ESN_CUDA_TRY(cudaStreamWaitEvent(p->st2, p->e_in, 0));
         ss = p->st2;
     }
     if (p->have_events) ESN_CUDA_TRY(rec_ev(p, p->ev[0], ss));
-    ESN_CUDA_TRY(cudaMemsetAsync(p->key_count, 0, sizeof(int) * p->nkeys, ss));
+    if (!side) ESN_CUDA_TRY(cudaMemsetAsync(p->key_count, 0, sizeof(int) * p->nkeys, ss));
     // point flags [0..5] only when overlapped: flag 6 (data) belongs to the
     // concurrent execute on the plan stream
     if (!p->keep_flags)
@@ -830,7 +870,8 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
                           p->method == ESN_METHOD_GLOBAL;
     if (unsorted) {
         if ((rc = launch_setpts_unsorted(a, ss))) return rc;
-    } else if ((rc = launch_setpts(a, p->nbk, p->maxsub, p->subprob, p->nsub, p->subofs, ss))) {
+    } else if ((rc = launch_setpts(a, p->nbk, p->maxsub, p->subprob, p->nsub, p->subofs, ss,
+                                   (p->aux.st && !graphed) ? &p->aux : nullptr))) {
         return rc;
     }
     if (p->have_events) ESN_CUDA_TRY(rec_ev(p, p->ev[1], ss));

@@ -403,7 +403,7 @@ __global__ void k_fill_subprob(const int *bin_start, const int *subofs, int nbin
 
 template <typename XT, int DIM>
 static int setpts_impl(const SetptsArgs &a, int nbins, int maxsub, int4 *subprob, int *nsub, int *subofs,
-                       cudaStream_t st) {
+                       cudaStream_t st, const SetptsAux *aux) {
     const int threads = 256;
     // persistent grids: exactly one wave of resident CTAs (a partial second
     // wave left SMs idle at the tail)
@@ -431,17 +431,35 @@ static int setpts_impl(const SetptsArgs &a, int nbins, int maxsub, int4 *subprob
     k_scan_top<<<1, 1024, 0, st>>>(a.block_sums, nsb);
     k_scan_down<<<nsb, 1024, 0, st>>>(a.key_count, a.nkeys, a.block_sums, a.cursor, a.bin_start, a.spb, nbins);
     ESN_CUDA_TRY(cudaGetLastError());
+    // the subproblem tables depend on the bin starts only: with an aux stream
+    // they are built beside the scatter (launched first, so their few CTAs
+    // are placed before the scatter's wave takes the SMs)
+    const bool fork = aux && aux->st && a.M > 0;
+    cudaStream_t ts = fork ? aux->st : st;
+    auto tables = [&]() -> int {
+        k_scan_subprob<<<1, 1024, 0, ts>>>(a.bin_start, nbins, maxsub, subofs, nsub);
+        int fb = (nbins + 255) / 256;
+        k_fill_subprob<<<fb < 1 ? 1 : fb, 256, 0, ts>>>(a.bin_start, subofs, nbins, maxsub, subprob);
+        ESN_CUDA_TRY(cudaGetLastError());
+        return ESN_SUCCESS;
+    };
+    if (fork) {
+        ESN_CUDA_TRY(cudaEventRecord(aux->fork, st));
+        ESN_CUDA_TRY(cudaStreamWaitEvent(aux->st, aux->fork, 0));
+        if (int rc = tables()) return rc;
+        ESN_CUDA_TRY(cudaEventRecord(aux->join, aux->st));
+    }
     if (a.M > 0) {
         int64_t sb = (a.M + threads * kSILP - 1) / (threads * kSILP);
         if (sb > cap_scatter) sb = cap_scatter;
         k_setpts_scatter<XT, DIM><<<(int)sb, threads, 0, st>>>(a);
         ESN_CUDA_TRY(cudaGetLastError());
     }
-    k_scan_subprob<<<1, 1024, 0, st>>>(a.bin_start, nbins, maxsub, subofs, nsub);
-    int fb = (nbins + 255) / 256;
-    k_fill_subprob<<<fb < 1 ? 1 : fb, 256, 0, st>>>(a.bin_start, subofs, nbins, maxsub, subprob);
-    ESN_CUDA_TRY(cudaGetLastError());
-    return ESN_SUCCESS;
+    if (fork) {
+        ESN_CUDA_TRY(cudaStreamWaitEvent(st, aux->join, 0));
+        return ESN_SUCCESS;
+    }
+    return tables();
 }
 
 __global__ void k_sort_view(const Rec *rec, const int *bin_start, int nbins, int *perm, int *keys) {
@@ -494,13 +512,13 @@ int launch_setpts_unsorted(const SetptsArgs &a, cudaStream_t st) {
 }
 
 int launch_setpts(const SetptsArgs &a, int nbins, int max_subprob, int4 *subprob, int *nsub, int *subofs,
-                  cudaStream_t st) {
+                  cudaStream_t st, const SetptsAux *aux) {
     auto run = [&](auto xt) {
         using XT = decltype(xt);
         switch (a.g.dim) {
-            case 1: return setpts_impl<XT, 1>(a, nbins, max_subprob, subprob, nsub, subofs, st);
-            case 2: return setpts_impl<XT, 2>(a, nbins, max_subprob, subprob, nsub, subofs, st);
-            default: return setpts_impl<XT, 3>(a, nbins, max_subprob, subprob, nsub, subofs, st);
+            case 1: return setpts_impl<XT, 1>(a, nbins, max_subprob, subprob, nsub, subofs, st, aux);
+            case 2: return setpts_impl<XT, 2>(a, nbins, max_subprob, subprob, nsub, subofs, st, aux);
+            default: return setpts_impl<XT, 3>(a, nbins, max_subprob, subprob, nsub, subofs, st, aux);
         }
     };
     return a.coord_f32 ? run(0.0f) : run(0.0);
