@@ -2019,11 +2019,13 @@ struct InterpUnit {
 // P_d <= n_d (each patch row wraps at most once).
 template <typename T, int DIM, int W>
 __global__ void __launch_bounds__(256, interp_minb<DIM, W>())
-    k_interp_bulk(SpreadArgs<T> a, T *cout, const T *gridp, int slice, int dprod, int pitch1) {
+    k_interp_bulk(SpreadArgs<T> a, T *cout, const T *gridp, int slice, int dprod, int pitch1, int R) {
     using C = typename Cx<T>::type;
     extern __shared__ __align__(16) unsigned char bulk_smem[];
-    __shared__ uint64_t s_full[2], s_empty[2];
-    __shared__ InterpUnit s_unit[2];
+    constexpr int RMAX = 4;  // record slots (R <= RMAX); the patches keep two
+    __shared__ uint64_t s_full[RMAX], s_empty[RMAX];
+    __shared__ InterpUnit s_unit[RMAX];
+    __shared__ int s_plast[2];  // (producer) last unit that reads each patch slot
     // producer state, touched by lane 0 of warp 0 only (kept in shared
     // memory so it costs the compute threads no registers)
     __shared__ int s_prod[8];
@@ -2037,8 +2039,8 @@ __global__ void __launch_bounds__(256, interp_minb<DIM, W>())
     // bytes keeps a quarter-warp that runs off a bin row's end onto the next
     // row on distinct banks)
     const int ncell = pitch1 * P2 * P3;
-    Rec *const rec0 = reinterpret_cast<Rec *>(bulk_smem);              // 2 x slice records
-    C *const patch0 = reinterpret_cast<C *>(rec0 + 2 * slice);         // 2 x ncell cells
+    Rec *const rec0 = reinterpret_cast<Rec *>(bulk_smem);              // R x slice records
+    C *const patch0 = reinterpret_cast<C *>(rec0 + R * slice);         // 2 x ncell cells
     const int nsub = *a.nsub;
     const int nwork = nsub * a.ntransf;
     const int nbins_geo = a.g.nb[0] * a.g.nb[1] * a.g.nb[2];
@@ -2047,11 +2049,11 @@ __global__ void __launch_bounds__(256, interp_minb<DIM, W>())
     int &p_t = s_prod[4], &p_lo1 = s_prod[5], &p_lo2 = s_prod[6], &p_lo3 = s_prod[7];
     int p_next = 0;  // (lane 0 of warp 0) work index claimed one subproblem ahead
 
-    // warp 0: choose unit k and queue its copies into slot k & 1
+    // producer warp: choose unit k and queue its copies into slot k mod R
     auto produce = [&](int k) -> int {
-        const int rb = k & 1;
-        if (k >= 2) mbar_wait(&s_empty[rb], ((k >> 1) - 1) & 1);  // every warp released unit k - 2
-        int fresh = 0, valid = 0;
+        const int rb = k % R;
+        if (k >= R) mbar_wait(&s_empty[rb], ((k / R) - 1) & 1);  // every warp released unit k - R
+        int fresh = 0, valid = 0, guard = -1;
         InterpUnit u;
         if (lane == 0) {
             while (p_off >= p_cnt) {
@@ -2071,7 +2073,13 @@ __global__ void __launch_bounds__(256, interp_minb<DIM, W>())
                 u.valid = 0;
                 p_cnt = 0; p_off = 0; fresh = 0;
             } else {
-                if (fresh) p_pb ^= 1;  // the patch slot the previous subproblem did not use
+                if (fresh) {
+                    p_pb ^= 1;  // the patch slot the previous subproblem did not use
+                    // ... whose last reader (the subproblem before that) may
+                    // still be in flight when the ring is deeper than two
+                    if (s_plast[p_pb] > k - R) guard = s_plast[p_pb];
+                }
+                s_plast[p_pb] = k;
                 u.valid = 1; u.t = p_t; u.start = p_start + p_off; u.n = min(slice, p_cnt - p_off);
                 u.lo1 = p_lo1; u.lo2 = p_lo2; u.lo3 = p_lo3; u.pb = p_pb;
                 p_off += slice;
@@ -2086,7 +2094,11 @@ __global__ void __launch_bounds__(256, interp_minb<DIM, W>())
         }
         fresh = __shfl_sync(0xffffffffu, fresh, 0);
         valid = __shfl_sync(0xffffffffu, valid, 0);
+        guard = __shfl_sync(0xffffffffu, guard, 0);
         if (!valid) return 0;
+        // unit `guard` is released when its slot's empty barrier completes
+        // phase guard / R (unit guard + R is not produced yet: unambiguous)
+        if (guard >= 0) mbar_wait(&s_empty[guard % R], (guard / R) & 1);
         if (lane == 0)
             bulk_g2s_hint(rec0 + rb * slice, a.rec + u.start, (uint32_t)u.n * sizeof(Rec), &s_full[rb],
                           policy_evict_first());  // records stream through once
@@ -2113,10 +2125,11 @@ __global__ void __launch_bounds__(256, interp_minb<DIM, W>())
     if (tid == 0) {
         p_start = p_cnt = p_off = p_t = p_lo1 = p_lo2 = p_lo3 = 0;
         p_pb = 1;
-        mbar_init(&s_full[0], 1);
-        mbar_init(&s_full[1], 1);
-        mbar_init(&s_empty[0], dprod ? nwarps - 1 : nwarps);
-        mbar_init(&s_empty[1], dprod ? nwarps - 1 : nwarps);
+        s_plast[0] = s_plast[1] = -(1 << 30);
+        for (int r = 0; r < R; ++r) {
+            mbar_init(&s_full[r], 1);
+            mbar_init(&s_empty[r], dprod ? nwarps - 1 : nwarps);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // dprod: the last warp only produces (queues unit k + 1 as soon as every
@@ -2134,9 +2147,9 @@ __global__ void __launch_bounds__(256, interp_minb<DIM, W>())
     int producing = warp == pw ? produce(0) : 0;
     const uint64_t keep = policy_evict_last();
     for (int k = 0;; ++k) {
-        const int rb = k & 1;
+        const int rb = k % R;
         if (producing) producing = produce(k + 1);
-        mbar_wait(&s_full[rb], (k >> 1) & 1);
+        mbar_wait(&s_full[rb], (k / R) & 1);
         const InterpUnit u = s_unit[rb];
         if (!u.valid) break;
         const Rec *recs = rec0 + rb * slice;
@@ -2150,10 +2163,12 @@ __global__ void __launch_bounds__(256, interp_minb<DIM, W>())
         for (int kk = tid; kk < u.n; kk += cthreads) {
             Rec rc;
             {
-                const uint32_t ra = smem_u32(recs + kk) + 16u * hsel;
+                // (no alignment assumed beyond 16 bytes: the dynamic segment
+                // follows the static words)
+                const uint32_t r0 = smem_u32(recs + kk);
                 long long ax, ay, bx, by;
-                asm volatile("ld.shared.v2.s64 {%0, %1}, [%2];" : "=l"(ax), "=l"(ay) : "r"(ra));
-                asm volatile("ld.shared.v2.s64 {%0, %1}, [%2];" : "=l"(bx), "=l"(by) : "r"(ra ^ 16u));
+                asm volatile("ld.shared.v2.s64 {%0, %1}, [%2];" : "=l"(ax), "=l"(ay) : "r"(r0 + 16u * hsel));
+                asm volatile("ld.shared.v2.s64 {%0, %1}, [%2];" : "=l"(bx), "=l"(by) : "r"(r0 + 16u - 16u * hsel));
                 rc.g[0] = __longlong_as_double(hsel ? bx : ax);
                 rc.g[1] = __longlong_as_double(hsel ? by : ay);
                 rc.g[2] = __longlong_as_double(hsel ? ax : bx);

@@ -194,6 +194,9 @@ struct InterpOp {
         }
         if constexpr (sizeof(C) == 16) if (fits && !(mode && std::string(mode) == "tile")) {
             static const char *sl = getenv("ESN_INTERP_SLICE");
+            // record ring: ESN_INTERP_RING=<2..4> slots of ESN_INTERP_SLICE records
+            static const char *re = getenv("ESN_INTERP_RING");
+            const int R = re ? std::min(4, std::max(2, atoi(re))) : 2;
             int slice = sl ? atoi(sl) : 512;
             // patch row pitch: ESN_INTERP_PITCH=<cells> (>= bs + w - 1), 0 = rows packed;
             // default a multiple of 8 cells (128 bytes) for D >= 2
@@ -204,10 +207,10 @@ struct InterpOp {
             cells = cells / (size_t)P1 * (size_t)pitch1;
             // three CTAs per SM when the patches allow it: 228 KB less 1 KB
             // reserved and the static words per CTA
-            constexpr size_t kThree = 233472 / 3 - 1024 - 256;
+            constexpr size_t kThree = 233472 / 3 - 1024 - 512;
             if (!sl)
-                while (slice > 256 && 2 * cells * sizeof(C) + 2 * (size_t)slice * sizeof(Rec) > kThree) slice -= 32;
-            const size_t bsmem = 2 * cells * sizeof(C) + 2 * (size_t)slice * sizeof(Rec);
+                while (slice > 128 && 2 * cells * sizeof(C) + (size_t)R * slice * sizeof(Rec) > kThree) slice -= 32;
+            const size_t bsmem = 2 * cells * sizeof(C) + (size_t)R * slice * sizeof(Rec);
             if (bsmem <= 112 * 1024) {
                 static PerDev<size_t> bconf_;
                 size_t &bconfigured = bconf_();
@@ -223,7 +226,7 @@ struct InterpOp {
                     const char *e = getenv("ESN_INTERP_PRODUCER");
                     return e && e[0] == '0' ? 0 : 1;
                 }();
-                k_interp_bulk<T, D, W><<<device_sm_count() * occ, 256, bsmem, st>>>(a, cout, grid, slice, dprod, pitch1);
+                k_interp_bulk<T, D, W><<<device_sm_count() * occ, 256, bsmem, st>>>(a, cout, grid, slice, dprod, pitch1, R);
                 ESN_CUDA_TRY(cudaGetLastError());
                 return ESN_SUCCESS;
             }
