@@ -262,7 +262,9 @@ def cpu_sample_size(name):
 
 def run_mode(cfg, world, reduce):
     """Multi-GPU mode of a config."""
-    if world > 1 and cfg["ttype"] == 1 and cfg["ntransf"] == 1 and cfg["dim"] == 3:
+    # (--reduce peer also runs the point-split path on one GPU: the fused
+    # spread-into-the-root's-grid code with a world of one)
+    if (world > 1 or reduce == "peer") and cfg["ttype"] == 1 and cfg["ntransf"] == 1 and cfg["dim"] == 3:
         return "points"
     if world > 1 and cfg["ntransf"] > 1:
         return "transforms"
@@ -326,9 +328,37 @@ def gpu_run(args, name, rank, world, local_rank, *, steps, warmup, reduce, e2e, 
     fine = None
     if mode == "points" and reduce == "grid":
         fine = torch.empty(tuple(reversed(plan.nfine)), dtype=cplx, device=dev)
+    peer_grid = peer_target = None
+    if mode == "points" and reduce == "peer":
+        # reduction fused into the spreader: rank 0 owns the fine grid in
+        # peer-mappable memory, every rank's tile flushes RED into it over
+        # NVLink (distributed.exec_type1_peer_reduced); no reduce collective
+        from paper_1808_06736_b200 import peer
+        shape = tuple(reversed(plan.nfine))
+        box = [None]
+        if rank == 0:
+            pbuf = peer.PeerBuffer(int(np.prod(shape)) * (16 if cplx == torch.complex128 else 8), dev)
+            peer_grid = pbuf.tensor(cplx, shape)
+            box[0] = pbuf.handle
+        if world > 1:
+            dist.broadcast_object_list(box, src=0)
+        peer_target = peer_grid if rank == 0 else peer.open_peer(box[0], dev)
 
     def step():
         plan.setpts(xs)
+        if peer_target is not None:
+            if rank == 0:
+                peer_grid.zero_()
+                stream.synchronize()
+            if world > 1:
+                dist.barrier()  # the grid is zeroed before any rank adds
+            plan.spread_add(cin, peer_target)
+            if world > 1:
+                stream.synchronize()
+                dist.barrier()  # every rank's REDs have landed
+            if rank == 0:
+                plan.finish_type1(peer_grid, fout)
+            return
         if fine is not None:
             # fine-grid reduce (north_star): spread, NCCL-reduce the fine
             # grids, root alone runs FFT + deconvolution
@@ -390,6 +420,12 @@ def gpu_run(args, name, rank, world, local_rank, *, steps, warmup, reduce, e2e, 
                stages={k: v / steps for k, v in st.items()} if not args.stage_sync
                else {k: v / steps for k, v in stages.items()})
     plan.close()
+    if peer_target is not None:
+        if world > 1:
+            dist.barrier()  # nobody still adds into the root's grid
+        peer_grid = None
+        if rank == 0:
+            pbuf.free()
     del xs, d, out, fine, gathered
     torch.cuda.empty_cache()
     if e2e:
@@ -476,6 +512,8 @@ def e2e_sharded(cfg, coords, data, M, Mr, T, Tr, mode, reduce, rank, world, dev,
         def call():
             if reduce == "grid":
                 r = DD.exec_type1_grid_reduced(hx, hd, cfg["nm"], opts, dst=0)
+            elif reduce == "peer":
+                r = DD.exec_type1_peer_reduced(hx, hd, cfg["nm"], opts, dst=0)
             else:
                 r = DD.exec_type1_point_sharded(hx, hd, cfg["nm"], opts, dst=0)
             return r.cpu() if rank == 0 else None
@@ -497,7 +535,8 @@ def e2e_sharded(cfg, coords, data, M, Mr, T, Tr, mode, reduce, rank, world, dev,
     for _ in range(max(1, warmup)):
         call()
     torch.cuda.synchronize(dev)
-    dist.barrier()
+    if world > 1:
+        dist.barrier()
     k = 5
     t0 = time.perf_counter()
     for _ in range(k):
@@ -506,7 +545,8 @@ def e2e_sharded(cfg, coords, data, M, Mr, T, Tr, mode, reduce, rank, world, dev,
     el = time.perf_counter() - t0
     return {"elapsed": el, "calls": k, "calls_timed": k, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h),
-            "api": ("distributed.exec_type1_grid_reduced" if mode == "points" and reduce == "grid" else
+            "api": ("distributed.exec_type1_peer_reduced" if mode == "points" and reduce == "peer" else
+                    "distributed.exec_type1_grid_reduced" if mode == "points" and reduce == "grid" else
                     "distributed.exec_type1_point_sharded" if mode == "points" else
                     "distributed.exec_type1_transform_sharded")
                    + " (pinned host shards; H2D, spread/FFT, NCCL, D2H on rank 0)"}
@@ -521,8 +561,11 @@ def config_block(name, world, dist="uniform", M=None, mode="replica", reduce="gr
     par = "1 GPU"
     if world > 1:
         par = {"replica": f"replica shards x{world} (independent points per GPU)",
-               "points": f"points split x{world}, NCCL reduce of the partial "
-                         + ("fine grids, root FFT + deconv" if reduce == "grid" else "mode arrays"),
+               "points": f"points split x{world}, "
+                         + ("spreaders RED into the root's peer-mapped fine grid (no reduce collective), "
+                            "root FFT + deconv" if reduce == "peer" else
+                            "NCCL reduce of the partial "
+                            + ("fine grids, root FFT + deconv" if reduce == "grid" else "mode arrays")),
                "transforms": f"transforms split x{world}, all-gather of the results"}[mode]
     return {
         "workload": f"{name}: {cfg['dim']}D type-{cfg['ttype']}, modes {nm}, M={M:.0e}{per}, "
@@ -639,7 +682,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=list(cases.CONFIGS))
     ap.add_argument("--method", default="auto")
-    ap.add_argument("--reduce", default="grid", choices=["modes", "grid"],
+    ap.add_argument("--reduce", default="grid", choices=["modes", "grid", "peer"],
                     help="multi-GPU single 3D type 1: NCCL-reduce the fine grids (north_star; root alone "
                          "runs FFT + deconv) or the per-rank mode arrays (each rank FFTs + deconvolves)")
     ap.add_argument("--points", default="uniform", choices=list(cases.DISTRIBUTIONS),

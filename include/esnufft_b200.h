@@ -164,6 +164,26 @@ int esn_plan_interp(esn_plan p, const void *grid, void *c);
  * deconvolution into f (N_d..N_1).  esn_plan_spread(p, c, grid) followed by
  * esn_plan_finish_type1(p, grid, f) equals esn_plan_execute(p, c, f). */
 int esn_plan_finish_type1(esn_plan p, void *grid, void *f);
+/* Spread c ADDING into grid (device array (ntransf, n_d..n_1), not zeroed
+ * here): the spreader's tile flushes are REDs (atomic adds), so several
+ * plans -- on this GPU or on peer GPUs that map the same grid through
+ * esn_peer_open -- may add into one grid concurrently.  This is the
+ * point-split multi-GPU type 1 with the reduction fused into the spreader:
+ * every rank flushes straight into the root's fine grid over NVLink
+ * instead of spreading into a private grid that NCCL then reduces
+ * (the reference has no counterpart: its spread() writes a
+ * private array, spreadinterp.py:187-256).  SIZE_ERROR for the batched 2D
+ * owner-computes spreader (plain stores, not concurrent-safe). */
+int esn_plan_spread_add(esn_plan p, const void *c, void *grid);
+/* Peer-mappable device memory (cudaMalloc + CUDA IPC): esn_peer_alloc
+ * returns the pointer and a 64-byte handle that another PROCESS (one per
+ * GPU) turns into a pointer valid on its own device with esn_peer_open
+ * (peer access over NVLink enabled lazily).  esn_peer_close unmaps an
+ * opened pointer, esn_peer_free releases an allocated one. */
+int esn_peer_alloc(int64_t bytes, void **ptr, unsigned char handle[64]);
+int esn_peer_open(const unsigned char handle[64], void **ptr);
+int esn_peer_close(void *ptr);
+int esn_peer_free(void *ptr);
 /* Synchronise the plan stream and report data errors found on device:
  * returns ESN_DATA_ERROR / ESN_BOUNDS_VIOLATION with the offending point
  * index in info[0] and the (1-based) dimension in info[1] (0 = strength).*/

@@ -67,6 +67,11 @@ SIGNATURES = {
     "esn_plan_destroy": (i32, [vp]),
     "esn_plan_sort_view": (i32, [vp, vp, vp, vp]),
     "esn_plan_finish_type1": (i32, [vp, vp, vp]),
+    "esn_plan_spread_add": (i32, [vp, vp, vp]),
+    "esn_peer_alloc": (i32, [i64, ctypes.POINTER(vp), ctypes.c_char_p]),
+    "esn_peer_open": (i32, [ctypes.c_char_p, ctypes.POINTER(vp)]),
+    "esn_peer_close": (i32, [vp]),
+    "esn_peer_free": (i32, [vp]),
     "esn_plan_target_chunks": (i32, [vp, vp]),
     "esn_plan_bins": (i32, [vp, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)]),
     "esn_plan_tasks": (i32, [vp, P_i64]),

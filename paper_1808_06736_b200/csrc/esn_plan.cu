@@ -1054,6 +1054,65 @@ int esn_plan_finish_type1(esn_plan p, void *grid, void *f) {
     return fft_deconv_type1(p, grid, f, p->st, nullptr);
 }
 
+int esn_plan_spread_add(esn_plan p, const void *c, void *grid) {
+    if (!p || !p->points_set) return fail(ESN_SIZE_ERROR, "plan has no points (call esn_plan_setpts first)");
+    if (!grid) return fail(ESN_SIZE_ERROR, "null grid");
+    const int method = p->type == 2 ? ESN_METHOD_GLOBAL : p->method;
+    if (esn::batched_owner(p->dtype, p->dim, p->kp.w, p->ntransf, method, p->sbl, p->geom.bs))
+        return fail(ESN_SIZE_ERROR, "spread_add: the batched owner-computes spreader stores without atomics");
+    ESN_CUDA_TRY(cudaMemsetAsync(p->flags + 6, 0xff, sizeof(unsigned long long), p->st));
+    return do_spread(p, c, grid, false);
+}
+
+static_assert(sizeof(cudaIpcMemHandle_t) == 64, "the ABI carries 64-byte handles");
+
+int esn_peer_alloc(int64_t bytes, void **ptr, unsigned char handle[64]) {
+    if (!ptr || !handle || bytes <= 0) return fail(ESN_SIZE_ERROR, "peer_alloc: bad arguments");
+    void *d = nullptr;
+    cudaError_t e = cudaMalloc(&d, (size_t)bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(ESN_RESOURCE_ERROR, "peer allocation of %lld bytes failed (%s)", (long long)bytes,
+                    cudaGetErrorString(e));
+    }
+    cudaIpcMemHandle_t h;
+    e = cudaIpcGetMemHandle(&h, d);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(d);
+        return fail(ESN_RESOURCE_ERROR, "cudaIpcGetMemHandle failed (%s)", cudaGetErrorString(e));
+    }
+    std::memcpy(handle, &h, 64);
+    *ptr = d;
+    return ESN_SUCCESS;
+}
+
+int esn_peer_open(const unsigned char handle[64], void **ptr) {
+    if (!ptr || !handle) return fail(ESN_SIZE_ERROR, "peer_open: bad arguments");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    void *d = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&d, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(ESN_RESOURCE_ERROR, "cudaIpcOpenMemHandle failed (%s)", cudaGetErrorString(e));
+    }
+    *ptr = d;
+    return ESN_SUCCESS;
+}
+
+int esn_peer_close(void *ptr) {
+    if (!ptr) return ESN_SUCCESS;
+    ESN_CUDA_TRY(cudaIpcCloseMemHandle(ptr));
+    return ESN_SUCCESS;
+}
+
+int esn_peer_free(void *ptr) {
+    if (!ptr) return ESN_SUCCESS;
+    ESN_CUDA_TRY(cudaFree(ptr));
+    return ESN_SUCCESS;
+}
+
 int esn_plan_interp(esn_plan p, const void *grid, void *c) {
     if (!p || !p->points_set) return fail(ESN_SIZE_ERROR, "plan has no points (call esn_plan_setpts first)");
     return do_interp(p, grid, c);

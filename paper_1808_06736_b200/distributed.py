@@ -14,6 +14,10 @@ SURVEY.md section 8(e):
   runs its slice of strength / mode vectors -- no data-path collective; the
   slices are gathered at the end (exec_type1_transform_sharded,
   exec_type2_transform_sharded);
+* exec_type1_peer_reduced fuses that reduction into the spreader: the root's
+  fine grid is peer-mapped (CUDA IPC over NVLink) on every rank and each
+  rank's tile flushes RED straight into it -- no per-rank grids, no reduce
+  collective;
 * type 2 and single-GPU configs run as independent replicas (each rank owns
   its own targets; type-2 outputs are independent per point).
 
@@ -111,6 +115,58 @@ def exec_type1_grid_reduced(coords, strengths, num_modes, opts, *, group=None, d
             if rank != dst:
                 return None
     return finish(state, grid, num_modes, opts)
+
+
+_PEER_GRIDS: dict = {}
+
+
+def exec_type1_peer_reduced(coords, strengths, num_modes, opts, *, group=None, dst: int = 0):
+    """Type 1 over points distributed across ranks with the reduction FUSED
+    into the spreader (B200: NVLink 5 / NVSwitch peer
+    memory).  ``dst`` owns the fine grid in peer-mappable memory
+    (peer.PeerBuffer, CUDA IPC); every rank sorts its shard and its spread
+    kernel flushes its tiles with REDs straight into that grid -- the
+    partial sums never exist as per-rank grids and no reduce collective
+    runs; ``dst`` then runs the FFT + deconvolution.  Exact up to the
+    floating-point order of the atomic adds (as between two runs of a
+    single-GPU spread).  The process group carries only the 64-byte handle
+    and two barriers, so any backend works.  Returns the modes on ``dst``,
+    None elsewhere."""
+    from . import peer
+    from .transforms import finish_type1_grid, prepare_type1_spread
+    rank, world = _world(group)
+    plan, c, xs, shape = prepare_type1_spread(coords, strengths, num_modes, opts)
+    dev = c.device
+    nbytes = c.element_size()
+    for v in shape:
+        nbytes *= int(v)
+    grid = None
+    if rank == dst:
+        key = (str(dev), nbytes)
+        buf = _PEER_GRIDS.get(key)
+        if buf is None:
+            buf = _PEER_GRIDS[key] = peer.PeerBuffer(nbytes, dev)
+        grid = buf.tensor(c.dtype, shape)
+        with torch.cuda.device(dev):
+            grid.zero_()
+            torch.cuda.current_stream(dev).synchronize()  # zeroed before any peer adds
+        target = grid
+    if world > 1:
+        box = [buf.handle if rank == dst else None]
+        dist.broadcast_object_list(box, src=dst, group=group)  # (also: the grid is zeroed)
+        if rank != dst:
+            target = peer.open_peer(box[0], dev)
+    with plan.lock:
+        plan.spread_add(c, target)
+        st, idx, d = plan.check_info()  # waits for this rank's flushes
+    if world > 1:
+        dist.barrier(group=group)  # every rank's REDs have landed
+    if st:  # (after the barrier: a rank with bad data must not strand the others)
+        from .transforms import raise_data_error
+        raise_data_error(st, idx, d, xs, "strength")
+    if rank != dst:
+        return None
+    return finish_type1_grid(plan, grid)
 
 
 def _empty_slice_spec(part, ref, opts, group):

@@ -130,6 +130,12 @@ class Plan:
     def spread(self, c: torch.Tensor, grid: torch.Tensor):
         _lib.check(_lib.lib.esn_plan_spread(self.h, _ptr(c), _ptr(grid)))
 
+    def spread_add(self, c: torch.Tensor, grid):
+        """Spread ADDING into ``grid`` (a tensor, or the integer device
+        pointer of a peer-mapped grid: esn_plan_spread_add)."""
+        g = _ptr(grid) if isinstance(grid, torch.Tensor) else ctypes.c_void_p(int(grid))
+        _lib.check(_lib.lib.esn_plan_spread_add(self.h, _ptr(c), g))
+
     def finish_type1(self, grid: torch.Tensor, f: torch.Tensor):
         """cuFFT (in place on ``grid``) + deconvolution into ``f``."""
         _lib.check(_lib.lib.esn_plan_finish_type1(self.h, _ptr(grid), _ptr(f)))

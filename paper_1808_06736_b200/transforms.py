@@ -198,6 +198,30 @@ def spread_type1_grid(coords, strengths, num_modes, opts: TransformOptions):
     return grid, plan
 
 
+def prepare_type1_spread(coords, strengths, num_modes, opts: TransformOptions):
+    """Plan + sorted points of a type-1 spread whose grid lives elsewhere
+    (``Plan.spread_add`` into a shared / peer-mapped fine grid): returns
+    (plan, strengths on the device, fine-grid shape (T,) n_d..n_1)."""
+    params = opts.kernel_params()
+    dim = len(coords)
+    nm = _as_mode_tuple(num_modes, dim)
+    ModeIndexSet(nm)
+    sizes = fine_grid_sizes(nm, opts.sigma, params.w)
+    _grid_cap_check(int(np.prod(sizes)), opts.max_grid_values)
+    dev = D.device_of(opts.device)
+    with torch.cuda.device(dev):
+        xs, m = _coords_to_device(coords, dev)
+        c = D.as_complex(strengths, dev, D.CPLX[opts.dtype])
+        ntransf = 1 if c.dim() == 1 else c.shape[0]
+        if c.shape[-1:] != (m,) or c.dim() > 2 or ntransf < 1:
+            raise SizeError(f"strengths shape {tuple(c.shape)} does not match M={m}")
+        plan = _plan_for(1, dim, nm, opts.isign, ntransf, params, opts, dev)
+        with plan.lock:
+            plan.setpts(xs)
+    shape = ((ntransf,) if c.dim() == 2 else ()) + tuple(reversed(sizes))
+    return plan, c, xs, shape
+
+
 def finish_type1_grid(plan: Plan, grid: torch.Tensor):
     """Second half: cuFFT (in place on ``grid``) and deconvolution
     (esn_plan_finish_type1); returns the modes (T, N_d..N_1) / (N_d..N_1)."""
