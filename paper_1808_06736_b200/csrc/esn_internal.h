@@ -167,6 +167,10 @@ struct Batch2Cfg {
 struct SetptsAux {
     cudaStream_t st = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
+    // optional: the count pass on its own stream (already ordered after its
+    // inputs by the caller); `counted` joins it into the sort stream
+    cudaStream_t count_st = nullptr;
+    cudaEvent_t counted = nullptr;
 };
 int launch_setpts(const SetptsArgs &a, int nbins, int max_subprob, int4 *subprob, int *nsub, int *subofs,
                   cudaStream_t st, const SetptsAux *aux = nullptr);

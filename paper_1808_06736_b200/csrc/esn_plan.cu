@@ -137,7 +137,9 @@ struct esn_plan_s {
     // of the sorted points join e_sorted on st first (join_sort)
     cudaStream_t st2 = nullptr;
     cudaEvent_t e_in = nullptr, e_sorted = nullptr;
-    // aux stream of setpts (subproblem tables beside the record scatter)
+    // aux stream of setpts (subproblem tables beside the record scatter);
+    // type-2 side sorts also run their count pass on aux.count_st at the plan
+    // stream's priority (see esn_plan_setpts)
     SetptsAux aux;
     bool sort_pending = false;
     // CUDA-graph replay of launch-bound calls (small M): the stream work of
@@ -484,6 +486,11 @@ int esn_plan_destroy(esn_plan p) {
         cudaEventDestroy(p->e_sorted);
         cudaStreamDestroy(p->st2);
     }
+    if (p->aux.count_st) {
+        cudaStreamSynchronize(p->aux.count_st);
+        cudaEventDestroy(p->aux.counted);
+        cudaStreamDestroy(p->aux.count_st);
+    }
     if (p->aux.st) {
         cudaStreamSynchronize(p->aux.st);
         cudaEventDestroy(p->aux.fork);
@@ -610,6 +617,24 @@ int esn_plan_create(int type, int dim, const int64_t *nmodes, int isign, int ntr
             cudaGetLastError();
             esn_plan_destroy(p);
             return fail(ESN_INTERNAL_ERROR, "side stream creation failed");
+        }
+    }
+    // the count pass of a side-stream sort at the PLAN stream's priority: it
+    // is bound by L2 atomics, not by SM time, and at the sort's high priority
+    // its resident CTAs starved the amplify + FFT beside it, whose tail then
+    // ran after the scatter (ESN_SORT_COUNT_LO=0: count on the sort stream)
+    static const bool countlo = [] {
+        const char *e = getenv("ESN_SORT_COUNT_LO");
+        return !(e && e[0] == '0');
+    }();
+    if (p->st2 && countlo) {
+        int prio = 0;
+        cudaStreamGetPriority(p->st, &prio);
+        if (cudaStreamCreateWithPriority(&p->aux.count_st, cudaStreamNonBlocking, prio) != cudaSuccess ||
+            cudaEventCreateWithFlags(&p->aux.counted, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            esn_plan_destroy(p);
+            return fail(ESN_INTERNAL_ERROR, "count stream creation failed");
         }
     }
     static const bool auxtab = [] {
@@ -810,21 +835,31 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
     // side stream: ordered after everything queued on the plan stream so far
     // (the previous execute may still read the records this sort rewrites)
     cudaStream_t ss = p->st;
+    // hs: the stream of the sort's head (clears, count pass) -- the sort
+    // stream itself, or the count stream, which the rest of the sort joins
+    // through aux.counted (launch_setpts)
+    cudaStream_t hs = ss;
+    SetptsAux aux = p->aux;
+    if (!(side && aux.st)) aux.count_st = nullptr;  // (the count stream rides on the aux block)
     if (side) {
-        // the fill cursors are touched by the sort only (side stream): clear
-        // them before joining the plan stream, i.e. beside the previous
-        // execute instead of after it (c2: 16 MB, ~9 us off the step)
-        ESN_CUDA_TRY(cudaMemsetAsync(p->key_count, 0, sizeof(int) * p->nkeys, p->st2));
-        ESN_CUDA_TRY(cudaEventRecord(p->e_in, p->st));
-        ESN_CUDA_TRY(cudaStreamWaitEvent(p->st2, p->e_in, 0));
         ss = p->st2;
+        hs = aux.count_st ? aux.count_st : ss;
+        // the count stream follows the previous sort (same plan, st2)
+        if (aux.count_st) ESN_CUDA_TRY(cudaStreamWaitEvent(hs, p->e_sorted, 0));
+        // the fill cursors are touched by the sort only: clear them before
+        // joining the plan stream, i.e. beside the previous execute instead
+        // of after it (c2: 16 MB, ~9 us off the step)
+        ESN_CUDA_TRY(cudaMemsetAsync(p->key_count, 0, sizeof(int) * p->nkeys, hs));
+        ESN_CUDA_TRY(cudaEventRecord(p->e_in, p->st));
+        ESN_CUDA_TRY(cudaStreamWaitEvent(hs, p->e_in, 0));
+        if (hs != ss) ESN_CUDA_TRY(cudaStreamWaitEvent(ss, p->e_in, 0));
     }
-    if (p->have_events) ESN_CUDA_TRY(rec_ev(p, p->ev[0], ss));
+    if (p->have_events) ESN_CUDA_TRY(rec_ev(p, p->ev[0], hs));
     if (!side) ESN_CUDA_TRY(cudaMemsetAsync(p->key_count, 0, sizeof(int) * p->nkeys, ss));
     // point flags [0..5] only when overlapped: flag 6 (data) belongs to the
     // concurrent execute on the plan stream
     if (!p->keep_flags)
-        ESN_CUDA_TRY(cudaMemsetAsync(p->flags, 0xff, sizeof(unsigned long long) * (side ? 6 : 8), ss));
+        ESN_CUDA_TRY(cudaMemsetAsync(p->flags, 0xff, sizeof(unsigned long long) * (side ? 6 : 8), hs));
     SetptsArgs a{};
     a.ibase = p->ibase;
     a.g = p->geom;
@@ -871,7 +906,7 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
     if (unsorted) {
         if ((rc = launch_setpts_unsorted(a, ss))) return rc;
     } else if ((rc = launch_setpts(a, p->nbk, p->maxsub, p->subprob, p->nsub, p->subofs, ss,
-                                   (p->aux.st && !graphed) ? &p->aux : nullptr))) {
+                                   (p->aux.st && !graphed) ? &aux : nullptr))) {
         return rc;
     }
     if (p->have_events) ESN_CUDA_TRY(rec_ev(p, p->ev[1], ss));

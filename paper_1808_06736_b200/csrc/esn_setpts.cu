@@ -418,11 +418,23 @@ static int setpts_impl(const SetptsArgs &a, int nbins, int maxsub, int4 *subprob
     const int64_t cap_count = (int64_t)device_sm_count() * 8;  // (atomics: oversubscribed is faster)
     static PerDev<int64_t> cap_scatter_;
     int64_t &cap_scatter = cap_scatter_();
-    if (cap_scatter == 0) cap_scatter = resident(k_setpts_scatter<XT, DIM>);
+    if (cap_scatter == 0) {
+        cap_scatter = resident(k_setpts_scatter<XT, DIM>);
+        // ESN_SCATTER_CTAS=<k>: at most k CTAs per SM (the scatter is bound by
+        // its random stores, not by occupancy; fewer resident CTAs leave SM
+        // slots to a concurrent FFT / the subproblem tables)
+        static const char *e = getenv("ESN_SCATTER_CTAS");
+        if (e && atoi(e) > 0) cap_scatter = std::min<int64_t>(cap_scatter, (int64_t)device_sm_count() * atoi(e));
+    }
     int64_t blocks = (a.M + threads * kILP - 1) / (threads * kILP);
     if (blocks > cap_count) blocks = cap_count;
     if (blocks < 1) blocks = 1;
-    if (a.M > 0) {
+    if (aux && aux->count_st) {
+        if (a.M > 0) k_setpts_count<XT, DIM><<<(int)blocks, threads, 0, aux->count_st>>>(a);
+        ESN_CUDA_TRY(cudaGetLastError());
+        ESN_CUDA_TRY(cudaEventRecord(aux->counted, aux->count_st));
+        ESN_CUDA_TRY(cudaStreamWaitEvent(st, aux->counted, 0));
+    } else if (a.M > 0) {
         k_setpts_count<XT, DIM><<<(int)blocks, threads, 0, st>>>(a);
         ESN_CUDA_TRY(cudaGetLastError());
     }
