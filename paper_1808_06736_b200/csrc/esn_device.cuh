@@ -452,6 +452,21 @@ __global__ void __launch_bounds__(RowsCfg<T, DIM, W>::NT, RowsCfg<T, DIM, W>::MI
 //  * phase A of chunk k + 1 (records + strength gather by cp.async two / one
 //    chunk ahead, Horner rows) runs after phase B of chunk k behind ONE barrier
 //    per chunk; lists are built per warp by ballot compaction (no atomics).
+// Warp-list entry of the 3D row spreader.  Wide (default): four words --
+// the packed word (record offset / 16 | ox << 16 | last-of-run << 31), then
+// the BYTE offsets of the lane-relative r2 operand, the c * r3 operand and the
+// record, ready to add to the lane's bases: a pass spends 2 integer adds on
+// addresses instead of ~8 shifts / masks on a two-word packed entry
+// (ESN_R3_WIDE=0 keeps the packed entry).
+#ifndef ESN_R3_WIDE
+#define ESN_R3_WIDE 1
+#endif
+#if ESN_R3_WIDE
+using Rows3Entry = uint4;
+#else
+using Rows3Entry = uint2;
+#endif
+
 template <typename T, int W>
 struct Rows3Cfg {
     using R = Rows3Geo<T, W>;
@@ -474,11 +489,26 @@ struct Rows3Cfg {
     static constexpr int O_R1 = OFN, O_R2 = OFN + R1N, O_CZ = OFN + R1N + R2N;
     static constexpr int RECN = (O_CZ + CZN + VT - 1) / VT * VT;
     static constexpr int RECS = RECN + VT;  // stride: +16 B keeps phase-A stores conflict-free
-    static constexpr int CH = (2 * 128 * RECS * (int)sizeof(T) <= 100 * 1024) ? 128 : 64;  // points per chunk
+    // points per chunk: 128 (64 for the widest records), trimmed in steps of
+    // 4 when that keeps two CTAs per SM with the four-word list entries
+    // (fp64 w = 7: 124)
+    static constexpr size_t smem_for(int ch) {
+        return (size_t)2 * ch * RECS * sizeof(T) + (size_t)2 * ch * sizeof(Rec) + (size_t)ch * 2 * sizeof(T) +
+               (size_t)NW * ch * sizeof(Rows3Entry);
+    }
+    static constexpr int pick_ch() {
+        const int ch0 = (2 * 128 * RECS * (int)sizeof(T) <= 100 * 1024) ? 128 : 64;
+        const size_t budget = 233472 / 2 - 1024 - 128;  // two CTAs: 228 KB less the reserved KB and the static words
+        if (MINB != 2 || smem_for(ch0) <= budget) return ch0;
+        for (int ch = ch0 - 4; ch >= ch0 - 16; ch -= 4)
+            if (smem_for(ch) <= budget) return ch;
+        return ch0;
+    }
+    static constexpr int CH = pick_ch();
     static constexpr size_t STAGE_B = (size_t)CH * RECS * sizeof(T);
     static constexpr size_t RING_B = (size_t)2 * CH * sizeof(Rec);
     static constexpr size_t CRING_B = (size_t)CH * 2 * sizeof(T);
-    static constexpr size_t LIST_B = (size_t)NW * CH * sizeof(uint2);
+    static constexpr size_t LIST_B = (size_t)NW * CH * sizeof(Rows3Entry);
     static constexpr size_t SMEM = 2 * STAGE_B + RING_B + CRING_B + LIST_B;
     static_assert(2 * STAGE_B / 16 <= 0xffff && (RECS * sizeof(T)) % 16 == 0, "list entries address 16-byte units");
     static_assert(2 * STAGE_B / sizeof(T) + RECS + 128 <= 0xffff && O_CZ % 2 == 0, "operand indices fit 16 bits");
@@ -497,7 +527,7 @@ template <typename T>
 struct Rows3Pre {
     typename Cx<T>::type cz;
     T f;
-    unsigned off;  // record offset in 16-byte units
+    unsigned off;  // record offset in bytes
 };
 
 // One warp-list entry (two words):
@@ -506,13 +536,19 @@ struct Rows3Pre {
 // so a lane's operands are base_f + sizeof(T) * (y & 0xffff) and
 // base_cz + sizeof(C) * (y >> 16) with lane-constant bases (ry, rz folded in).
 template <typename T, int W>
-__device__ __forceinline__ Rows3Pre<T> rows3_load(const unsigned char *stage, uint2 e, const unsigned char *base_f,
-                                                  const unsigned char *base_cz) {
+__device__ __forceinline__ Rows3Pre<T> rows3_load(const unsigned char *stage, Rows3Entry e,
+                                                  const unsigned char *base_f, const unsigned char *base_cz) {
     using C = typename Cx<T>::type;
     Rows3Pre<T> p;
-    p.off = e.x & 0xffffu;
+#if ESN_R3_WIDE
+    p.off = e.w;  // record offset in bytes
+    p.f = *reinterpret_cast<const T *>(base_f + e.y);
+    p.cz = *reinterpret_cast<const C *>(base_cz + e.z);
+#else
+    p.off = 16u * (e.x & 0xffffu);
     p.f = *reinterpret_cast<const T *>(base_f + (unsigned)sizeof(T) * (e.y & 0xffffu));
     p.cz = *reinterpret_cast<const C *>(base_cz + (unsigned)sizeof(C) * (e.y >> 16));
+#endif
     (void)stage;
     return p;
 }
@@ -522,7 +558,7 @@ __device__ __forceinline__ void rows3_apply(typename Cx<T>::type *acc, const uns
                                             const Rows3Pre<T> &p) {
     using C = typename Cx<T>::type;
     using Cfg = Rows3Cfg<T, W>;
-    const T *rec = reinterpret_cast<const T *>(stage + 16u * p.off);
+    const T *rec = reinterpret_cast<const T *>(stage + p.off);
     const C v = cmul(p.cz, p.f);
     T r1[Cfg::R1N];
     if constexpr (sizeof(T) == 8) {
@@ -549,19 +585,19 @@ __device__ __forceinline__ void rows3_apply(typename Cx<T>::type *acc, const uns
 // one run of equal x offset OX from the warp list; bit 31 of an entry's first
 // word marks the last point of its run (and of the list)
 template <typename T, int W, int OX>
-__device__ __forceinline__ int rows3_run(typename Cx<T>::type *acc, const unsigned char *stage, const uint2 *list,
+__device__ __forceinline__ int rows3_run(typename Cx<T>::type *acc, const unsigned char *stage, const Rows3Entry *list,
                                          int i, const unsigned char *base_f, const unsigned char *base_cz) {
     // float32: two points of the run per step (both points' operand loads in
     // flight before either's FMAs; c3f 1.65 -> 1.57 ms); float64 keeps one
     // (same time, fewer spills)
     if constexpr (sizeof(T) == 4) {
     for (;;) {
-        const uint2 e0 = list[i++];
+        const Rows3Entry e0 = list[i++];
         if (e0.x >> 31) {
             rows3_apply<T, W, OX>(acc, stage, rows3_load<T, W>(stage, e0, base_f, base_cz));
             break;
         }
-        const uint2 e1 = list[i++];
+        const Rows3Entry e1 = list[i++];
         const Rows3Pre<T> p0 = rows3_load<T, W>(stage, e0, base_f, base_cz);
         const Rows3Pre<T> p1 = rows3_load<T, W>(stage, e1, base_f, base_cz);
         rows3_apply<T, W, OX>(acc, stage, p0);
@@ -570,7 +606,7 @@ __device__ __forceinline__ int rows3_run(typename Cx<T>::type *acc, const unsign
     }
     } else {
     for (;;) {
-        const uint2 e = list[i++];
+        const Rows3Entry e = list[i++];
         rows3_apply<T, W, OX>(acc, stage, rows3_load<T, W>(stage, e, base_f, base_cz));
         if (e.x >> 31) break;
     }
@@ -588,7 +624,7 @@ __global__ void __launch_bounds__(Rows3Cfg<T, W>::NT, Rows3Cfg<T, W>::MINB) k_sp
     T *s_stage = reinterpret_cast<T *>(smem_raw);                                        // 2 x CH x RECS
     Rec *s_ring = reinterpret_cast<Rec *>(smem_raw + 2 * Cfg::STAGE_B);                  // 2 x CH
     C *s_c = reinterpret_cast<C *>(smem_raw + 2 * Cfg::STAGE_B + Cfg::RING_B);           // CH
-    uint2 *s_list = reinterpret_cast<uint2 *>(smem_raw + 2 * Cfg::STAGE_B + Cfg::RING_B + Cfg::CRING_B);  // NW x CH
+    Rows3Entry *s_list = reinterpret_cast<Rows3Entry *>(smem_raw + 2 * Cfg::STAGE_B + Cfg::RING_B + Cfg::CRING_B);  // NW x CH
     C *s_tile = reinterpret_cast<C *>(smem_raw);  // flush slab (aliases the stages)
     __shared__ int s_sub;
 
@@ -608,7 +644,7 @@ __global__ void __launch_bounds__(Rows3Cfg<T, W>::NT, Rows3Cfg<T, W>::MINB) k_sp
     const int pt = edge >= 0 ? edge * 32 + lane : CH;
     const int n1 = a.g.n[0], n2 = a.g.n[1], n3 = a.g.n[2];
     const int nsub = *a.nsub;
-    uint2 *mylist = s_list + warp * CH;
+    Rows3Entry *mylist = s_list + warp * CH;
     // lane-constant operand bases (entries carry the per-point parts, biased by EBIAS)
     static_assert(Cfg::PAD, "two-word entries index the zero-padded r2 / c * r3");
     const unsigned char *base_f = smem_raw + (int)sizeof(T) * (ry - Cfg::EBIAS);
@@ -752,7 +788,12 @@ __global__ void __launch_bounds__(Rows3Cfg<T, W>::NT, Rows3Cfg<T, W>::MINB) k_sp
                     const unsigned rb = (unsigned)((st & 1) * Cfg::STAGE_B + q * RECS * sizeof(T));  // record byte offset
                     const unsigned fi = rb / (unsigned)sizeof(T) + Cfg::O_R2 + Cfg::PY - oy + Cfg::EBIAS;
                     const unsigned zi = rb / (unsigned)sizeof(C) + Cfg::O_CZ / 2 + Cfg::PZ - oz + Cfg::EBIAS;
+#if ESN_R3_WIDE
+                    mylist[n + __popc(bal & ((1u << lane) - 1u))] =
+                        make_uint4((rb / 16) | ((unsigned)ox << 16), fi * (unsigned)sizeof(T), zi * (unsigned)sizeof(C), rb);
+#else
                     mylist[n + __popc(bal & ((1u << lane) - 1u))] = make_uint2((rb / 16) | ((unsigned)ox << 16), fi | (zi << 16));
+#endif
                 }
                 n += __popc(bal);
             }
