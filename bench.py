@@ -603,11 +603,12 @@ def cpu_info():
 
 
 def n_launches(cfg):
-    """Our kernels per step: setpts = count, scan x3, scatter, subproblem
-    scan + fill (7); type 2: amplify + interp; type 1: spread (batched:
-    permute + row table + spread) + deconv.  cuFFT's own kernels excluded."""
+    """Our kernels per step: setpts = count, scan x2 (reduce, down sweep),
+    scatter, subproblem scan + fill (6); type 2: amplify + interp; type 1:
+    spread (batched: permute + row table + spread) + deconv.  cuFFT's own
+    kernels excluded."""
     hk = hot_kernel_name(cfg)
-    return 7 + (2 if cfg["ttype"] == 2 else (3 if hk in ("k_spread_batch2d", "k_spread_b2own") else 1) + 1)
+    return 6 + (2 if cfg["ttype"] == 2 else (3 if hk in ("k_spread_batch2d", "k_spread_b2own", "k_spread_b2roll") else 1) + 1)
 
 
 def line_for(args, name, res, world, base):

@@ -240,7 +240,8 @@ __global__ void __launch_bounds__(256) k_setpts_scatter(SetptsArgs a) {
     }
 }
 
-// ---- exclusive scan of the key histogram: block reduce -> top scan -> down
+// ---- exclusive scan of the key histogram: block reduce -> down sweep (each
+// tile sums the totals before it)
 __device__ __forceinline__ int block_scan_excl(int v, int *total, int *wsum) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     int x = v;
@@ -283,24 +284,6 @@ __global__ void __launch_bounds__(1024) k_scan_reduce(const int *cnt, int n, int
     if (threadIdx.x == 0) block_sums[blockIdx.x] = total;
 }
 
-__global__ void __launch_bounds__(1024) k_scan_top(int *block_sums, int nblocks) {
-    __shared__ int wsum[32];
-    __shared__ int carry;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (int b0 = 0; b0 < nblocks; b0 += 1024) {
-        const int i = b0 + threadIdx.x;
-        const int v = i < nblocks ? block_sums[i] : 0;
-        int total;
-        const int e = block_scan_excl(v, &total, wsum);
-        if (i < nblocks) block_sums[i] = carry + e;
-        __syncthreads();
-        if (threadIdx.x == 0) carry += total;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) block_sums[nblocks] = carry;
-}
-
 // writes cursor[k] = exclusive prefix (kept: the spreaders read key starts)
 // and the same into cnt[k] (the scatter's fill cursors), and bin_start at
 // every bin head
@@ -313,6 +296,13 @@ __global__ void __launch_bounds__(1024) k_scan_down(int *cnt, int n, const int *
     // full vectors as int4 (the tile base is 16-byte aligned): one 128-bit
     // load / store per thread instead of four strided 32-bit ones
     const bool full = base + U <= n;
+    // this tile's offset = the sum of the tile totals before it, reduced
+    // here (<= a few thousand tiles) instead of by a one-CTA scan kernel
+    // between the two sweeps (one launch and its gap off the sort: ~7 us)
+    int pv = 0;
+    for (int i = threadIdx.x; i < (int)blockIdx.x; i += 1024) pv += block_sums[i];
+    int prefix;
+    block_scan_excl(pv, &prefix, wsum);
     int v[U], s = 0;
     if (full) {
         const int4 q = *reinterpret_cast<const int4 *>(cnt + base);
@@ -324,7 +314,7 @@ __global__ void __launch_bounds__(1024) k_scan_down(int *cnt, int n, const int *
 #pragma unroll
     for (int u = 0; u < U; ++u) s += v[u];
     int total;
-    int e = block_scan_excl(s, &total, wsum) + block_sums[blockIdx.x];
+    int e = block_scan_excl(s, &total, wsum) + prefix;
     int o[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -346,8 +336,8 @@ __global__ void __launch_bounds__(1024) k_scan_down(int *cnt, int n, const int *
             }
     }
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
-        bin_start[nbins] = block_sums[gridDim.x];
-        cursor[n] = block_sums[gridDim.x];  // end of the last key (cell-range readers use key + 1)
+        bin_start[nbins] = prefix + total;
+        cursor[n] = prefix + total;  // end of the last key (cell-range readers use key + 1)
     }
 }
 
@@ -440,7 +430,6 @@ static int setpts_impl(const SetptsArgs &a, int nbins, int maxsub, int4 *subprob
     }
     const int nsb = (a.nkeys + kScanTile - 1) / kScanTile;
     k_scan_reduce<<<nsb, 1024, 0, st>>>(a.key_count, a.nkeys, a.block_sums);
-    k_scan_top<<<1, 1024, 0, st>>>(a.block_sums, nsb);
     k_scan_down<<<nsb, 1024, 0, st>>>(a.key_count, a.nkeys, a.block_sums, a.cursor, a.bin_start, a.spb, nbins);
     ESN_CUDA_TRY(cudaGetLastError());
     // the subproblem tables depend on the bin starts only: with an aux stream
