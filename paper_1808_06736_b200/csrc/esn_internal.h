@@ -69,6 +69,7 @@ struct SetptsArgs {
     double inv_bs[3];       // 1 / bs (fast division, corrected exactly)
     int bs_log2[3];         // log2 bs when bs is a power of two, else -1
     int64_t M;
+    int rev;                // record scatter walks the input back to front
     int coord_f32;          // input coordinates are float (else double)
     int grid_units;         // coordinates already in grid units [0, n) (no fold)
     const void *x[3];

@@ -895,6 +895,11 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
         return e && e[0] == '0' ? 0 : 1;
     }();
     a.hints = hints;
+    static const int rev = [] {
+        const char *e = getenv("ESN_SCATTER_REV");
+        return e && e[0] == '0' ? 0 : 1;
+    }();
+    a.rev = rev;
     // small 1D type-1 plans spread point-parallel with global atomics: the
     // records need no order (ESN_SORT1D=1 forces the sort)
     static const bool sort1d = [] {

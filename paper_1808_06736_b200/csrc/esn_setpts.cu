@@ -193,7 +193,13 @@ __global__ void __launch_bounds__(256) k_setpts_scatter(SetptsArgs a) {
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
         asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
     }
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x * kSILP + threadIdx.x; base < a.M; base += stride) {
+    // input blocks in DESCENDING order: the count pass read the arrays front
+    // to back, so L2 still holds their tail (ESN_SCATTER_REV=0: ascending)
+    const int64_t per = (int64_t)blockDim.x * kSILP;
+    const int64_t nblk = (a.M + per - 1) / per;
+    (void)stride;
+    for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        const int64_t base = (a.rev ? nblk - 1 - blk : blk) * per + threadIdx.x;
         int pos[kSILP];
         double x[kSILP][3];
         load_coords<XT, DIM, kSILP>(a, base, x);
