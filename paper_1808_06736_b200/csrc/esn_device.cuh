@@ -1821,6 +1821,33 @@ __device__ __forceinline__ void lds_rows(uint32_t a, float *r1, float *r2) {
 template <int W>
 __host__ __device__ inline bool b2roll_fits(int n1, int n2) { return n1 >= kRollBX + W - 1 && n2 >= kRollSeg + W - 1; }
 
+// x-offset dispatch of the y-rolling batched spreader as a compare tree: the
+// offset CS selects which of the point's w columns land on the strip's owned
+// columns (static register indices).  (A switch compiled to a two-level
+// jump table here -- an indexed constant load and an indirect branch on the
+// critical path of every point.)
+#ifndef ESN_ROLL_TREE
+#define ESN_ROLL_TREE 1
+#endif
+template <typename T, int W, int BXS, int LO, int HI>
+__device__ __forceinline__ void roll_apply(int cs, typename Cx<T>::type (&acc)[W][BXS],
+                                           const typename Cx<T>::type (&v)[W], const T (&r1)[W]) {
+    if constexpr (LO == HI) {
+        constexpr int XL = LO - (W - 1);
+#pragma unroll
+        for (int m = 0; m < W; ++m) {
+            if (XL + m >= 0 && XL + m < BXS) {
+#pragma unroll
+                for (int dy = 0; dy < W; ++dy) acc[dy][XL + m] = cfma(v[dy], r1[m], acc[dy][XL + m]);
+            }
+        }
+    } else {
+        constexpr int MID = (LO + HI) / 2;
+        if (cs <= MID) roll_apply<T, W, BXS, LO, MID>(cs, acc, v, r1);
+        else roll_apply<T, W, BXS, MID + 1, HI>(cs, acc, v, r1);
+    }
+}
+
 template <typename T, int W>
 __global__ void __launch_bounds__(128, 3) k_spread_b2roll(SpreadArgs<T> a, const T *cperm, const PtRows2<W> *tab) {
     static_assert(sizeof(T) == 4, "float32 plans");
@@ -2018,6 +2045,9 @@ __global__ void __launch_bounds__(128, 3) k_spread_b2roll(SpreadArgs<T> a, const
             }                                                                             \
         }                                                                                 \
         break;
+#if ESN_ROLL_TREE
+                if ((unsigned)cs < (unsigned)NC) roll_apply<T, W, BXS, 0, NC - 1>(cs, acc, v, r1);
+#else
                 switch (cs) {
                     ESN_ROLL_CASE(0) ESN_ROLL_CASE(1) ESN_ROLL_CASE(2) ESN_ROLL_CASE(3)
                     ESN_ROLL_CASE(4) ESN_ROLL_CASE(5) ESN_ROLL_CASE(6) ESN_ROLL_CASE(7)
@@ -2027,6 +2057,7 @@ __global__ void __launch_bounds__(128, 3) k_spread_b2roll(SpreadArgs<T> a, const
                     default:
                         break;
                 }
+#endif
 #undef ESN_ROLL_CASE
             }
                 k0 = k1;
