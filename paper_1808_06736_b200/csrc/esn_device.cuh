@@ -49,6 +49,9 @@ __device__ __noinline__ void exact_row(double g, int i0, int W, T beta, T *row) 
     }
 }
 
+#ifndef ESN_HORNER_SYM
+#define ESN_HORNER_SYM 1
+#endif
 template <typename T, int W>
 __device__ __forceinline__ int kernel_row(double g, const KernelTab<T> &k, T *row) {
     // footprint origin and local coordinate in float64 exactly as the
@@ -64,6 +67,29 @@ __device__ __forceinline__ int kernel_row(double g, const KernelTab<T> &k, T *ro
         for (int m = 0; m < W; ++m) row[m] = tmp[m];
     } else {
         const T t = (T)(2.0 * ((double)i0 - g) + (double)(W - 1));
+#if ESN_HORNER_SYM
+        // The ES kernel is even, so piece W-1-m is piece m mirrored:
+        // p_{W-1-m}(t) = p_m(-t) (the fitted table is symmetric to ~3e-16).
+        // With p_m(t) = E(t^2) + t O(t^2) the pair costs two half-length
+        // Horner chains in t^2 plus two FMAs: (W+4) + 2 operations instead
+        // of 2 (W+3) -- 62 instead of 108 FP64 operations per 2D point at w = 6.
+        constexpr int NC = W + 4;        // coefficients per piece, highest degree first
+        const T s2 = t * t;
+#pragma unroll
+        for (int m = 0; m < (W + 1) / 2; ++m) {
+            // coefficient q multiplies t^(NC-1-q); split by the parity of the power
+            constexpr int QE = (NC - 1) % 2 == 0 ? 0 : 1;  // first even-power coefficient
+            constexpr int QO = 1 - QE;                      // first odd-power coefficient
+            T e = k.coef[m * NC + QE];
+#pragma unroll
+            for (int q = QE + 2; q < NC; q += 2) e = fma(e, s2, k.coef[m * NC + q]);
+            T o = k.coef[m * NC + QO];
+#pragma unroll
+            for (int q = QO + 2; q < NC; q += 2) o = fma(o, s2, k.coef[m * NC + q]);
+            row[m] = fma(t, o, e);
+            if (W - 1 - m != m) row[W - 1 - m] = fma(-t, o, e);
+        }
+#else
 #pragma unroll
         for (int m = 0; m < W; ++m) {
             T v = k.coef[m * (W + 4)];
@@ -71,6 +97,7 @@ __device__ __forceinline__ int kernel_row(double g, const KernelTab<T> &k, T *ro
             for (int q = 1; q < W + 4; ++q) v = fma(v, t, k.coef[m * (W + 4) + q]);
             row[m] = v;
         }
+#endif
     }
     return i0;
 }
