@@ -117,7 +117,17 @@ def exec_type1_grid_reduced(coords, strengths, num_modes, opts, *, group=None, d
     return finish(state, grid, num_modes, opts)
 
 
-_PEER_GRIDS: dict = {}
+_PEER_GRIDS: dict = {}  # (device, bytes) -> peer.PeerBuffer of the root's fine grid, reused across calls
+
+
+def release_peer_grids():
+    """Free the cached peer-mappable fine grids of this process and unmap
+    the peers' grids it opened (call on every rank, after a barrier: nobody
+    may still be adding into a grid that is freed)."""
+    from . import peer
+    for key in list(_PEER_GRIDS):
+        _PEER_GRIDS.pop(key).free()
+    peer.close_all_peers()
 
 
 def exec_type1_peer_reduced(coords, strengths, num_modes, opts, *, group=None, dst: int = 0):

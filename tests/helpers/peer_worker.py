@@ -15,7 +15,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 
 import paper_1808_06736_b200 as E  # noqa: E402
-from paper_1808_06736_b200.distributed import exec_type1_peer_reduced, shard_range  # noqa: E402
+from paper_1808_06736_b200.distributed import (exec_type1_peer_reduced, release_peer_grids,  # noqa: E402
+                                               shard_range)
 
 
 def main(out_path):
@@ -43,6 +44,7 @@ def main(out_path):
     if rank == 0:
         np.savez(out_path, world=world, **res)
     dist.barrier()
+    release_peer_grids()
     dist.destroy_process_group()
 
 
