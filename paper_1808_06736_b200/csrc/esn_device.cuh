@@ -515,7 +515,11 @@ struct Rows3Cfg {
     static constexpr int CZN = 2 * CZE;
     static constexpr int O_R1 = OFN, O_R2 = OFN + R1N, O_CZ = OFN + R1N + R2N;
     static constexpr int RECN = (O_CZ + CZN + VT - 1) / VT * VT;
-    static constexpr int RECS = RECN + VT;  // stride: +16 B keeps phase-A stores conflict-free
+    // stride: an ODD number of 16-byte units keeps the phase-A vector stores
+    // of a quarter-warp's eight records on distinct bank groups (an even
+    // count made them 2-way conflicts: 7.5 wavefronts per STS.128 in the
+    // source-level ncu view of fp64 w = 7, whose 42 doubles got a pad to 44)
+    static constexpr int RECS = ((RECN / VT) % 2 == 1) ? RECN : RECN + VT;
     // points per chunk: 128 (64 for the widest records), trimmed in steps of
     // 4 when that keeps two CTAs per SM with the four-word list entries
     // (fp64 w = 7: 124)
