@@ -1068,8 +1068,21 @@ __device__ __forceinline__ void batch2d_flush(const typename Cx<T>::type *acc, u
     __syncwarp();
 }
 
+// zero `n16` 16-byte units of the grid when *flag is set (the RED-flush
+// batched spreader taking over from an owner-computes one needs a zeroed grid)
+template <typename T>  // (a template only so that every instantiation unit may define it)
+__global__ void __launch_bounds__(256) k_zero_if(int4 *p, size_t n16, const int *flag) {
+    if (!*flag) return;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x)
+        p[i] = make_int4(0, 0, 0, 0);
+}
+
 template <typename T, int W, bool CELLKEYS>
 __global__ void __launch_bounds__(128) k_spread_batch2d(SpreadArgs<T> a, const T *cperm, const PtRows2<W> *tab) {
+    // (plans that may switch: this kernel runs only when the sort found the
+    // bins badly imbalanced; the owner-computes kernel launched before it
+    // then exited at once)
+    if (a.imb && !*a.imb) return;
     // Warp-independent: a persistent warp takes work items (subproblem,
     // transform group, tile row) from an atomic queue.  Lane = transform.
     // The item's points are one contiguous run of the finely sorted bin
@@ -1277,6 +1290,7 @@ constexpr size_t b2own_smem_bytes() { return 4 * (2 * batch2d_stage_bytes<T, W>(
 
 template <typename T, int W>
 __global__ void __launch_bounds__(128) k_spread_b2own(SpreadArgs<T> a, const T *cperm, const PtRows2<W> *tab) {
+    if (a.imb && *a.imb) return;  // imbalanced bins: the RED-flush kernel launched next takes over
     constexpr int R = kB2Rows;
     using C = typename Cx<T>::type;
     constexpr int BX = Batch2Cfg<T, W>::BX, BY = Batch2Cfg<T, W>::BY;
@@ -1857,6 +1871,12 @@ __host__ __device__ inline bool b2roll_fits(int n1, int n2) { return n1 >= kRoll
 // columns (static register indices).  (A switch compiled to a two-level
 // jump table here -- an indexed constant load and an indirect branch on the
 // critical path of every point.)
+#ifndef ESN_B2_TAIL
+#define ESN_B2_TAIL 1
+#endif
+#ifndef ESN_B2_TAIL_DIV
+#define ESN_B2_TAIL_DIV 4
+#endif
 #ifndef ESN_ROLL_TREE
 #define ESN_ROLL_TREE 1
 #endif
@@ -1881,6 +1901,7 @@ __device__ __forceinline__ void roll_apply(int cs, typename Cx<T>::type (&acc)[W
 
 template <typename T, int W>
 __global__ void __launch_bounds__(128, 3) k_spread_b2roll(SpreadArgs<T> a, const T *cperm, const PtRows2<W> *tab) {
+    if (a.imb && *a.imb) return;  // imbalanced bins: the RED-flush kernel launched next takes over
     static_assert(sizeof(T) == 4, "float32 plans");
     using C = typename Cx<T>::type;
     using Cfg = RollCfg<W>;
@@ -1908,7 +1929,22 @@ __global__ void __launch_bounds__(128, 3) k_spread_b2roll(SpreadArgs<T> a, const
     // bins are 16 x 16 cells on this path (batched_owner checks bs)
     constexpr int bx = Batch2Cfg<float, W>::BX, by = Batch2Cfg<float, W>::BY;
     const int ngroups = (a.ntransf + 31) / 32;
-    const int nstrips = (n1 + BXS - 1) / BXS, nsegs = (n2 + kRollSeg - 1) / kRollSeg;
+    // Segments: full ones (kRollSeg rows) first, then HALF segments over the
+    // last 1 / ESN_B2_TAIL_DIV of the rows.  Items come off one queue in this
+    // order, so every warp ends on a short item and the tail in which warps
+    // idle is shorter (c5: 8192 items of ~190 us on 1776 resident warps left
+    // a tail of ~half an item; the half segments pay (16 + w - 1) / 16
+    // instead of (32 + w - 1) / 32 origin rows per owned row).  The gain
+    // depends on how the full items divide into waves of resident warps (c5
+    // spread + permute, ms: none 1.085; last 1/2 1.048, 1/3 1.062, 1/4 1.0415,
+    // 1/5 1.058, 1/6 1.097, 1/8 1.13).  ESN_B2_TAIL=0 in the build keeps
+    // equal segments.
+    const int nstrips = (n1 + BXS - 1) / BXS;
+    const int nfull = n2 / kRollSeg;
+    const int nbig = (ESN_B2_TAIL && nfull >= 10) ? nfull - nfull / ESN_B2_TAIL_DIV : nfull;
+    const int rows_big = nbig * kRollSeg;
+    constexpr int HSEG = (ESN_B2_TAIL) ? kRollSeg / 2 : kRollSeg;
+    const int nsegs = nbig + (n2 - rows_big + HSEG - 1) / HSEG;
     const int nitems = nstrips * nsegs * ngroups;
     uint32_t par0 = 0, par1 = 0;  // mbarrier phase parity per buffer
     int next = 0;
@@ -1920,8 +1956,9 @@ __global__ void __launch_bounds__(128, 3) k_spread_b2roll(SpreadArgs<T> a, const
         const int tg = item % ngroups;
         const int sid = item / ngroups;
         const int strip = sid % nstrips, seg = sid / nstrips;
-        const int x0 = strip * BXS, y0 = seg * kRollSeg;
-        const int yend = min(y0 + kRollSeg, n2);  // owned rows y0 .. yend - 1
+        const int x0 = strip * BXS;
+        const int y0 = seg < nbig ? seg * kRollSeg : rows_big + (seg - nbig) * HSEG;
+        const int yend = min(y0 + (seg < nbig ? kRollSeg : HSEG), n2);  // owned rows y0 .. yend - 1
         const int nrows = yend - (y0 - H);         // origin rows of this item (<= R)
         int xb = x0 - H;
         while (xb < 0) xb += n1;  // window column k: (xb + k) mod n1

@@ -140,8 +140,9 @@ struct SpreadBatchOp {
                     rolled = true;
                 }
             }
+            const bool owner = batched_owner(ESN_F32, 2, W, a.ntransf, ESN_METHOD_TILE, a.sbl, a.g.bs);
             if (rolled) {
-            } else if (batched_owner(ESN_F32, 2, W, a.ntransf, ESN_METHOD_TILE, a.sbl, a.g.bs)) {
+            } else if (owner) {
                 constexpr size_t osmem = b2own_smem_bytes<T, W>();
                 static PerDev<int> grid_;
                 int &grid = grid_();
@@ -150,6 +151,26 @@ struct SpreadBatchOp {
                     if (rc) return rc;
                 }
                 k_spread_b2own<T, W><<<grid, 128, osmem, st>>>(a, cperm, tab);
+            }
+            // clustered points: one warp walks every point of an owner item, so a
+            // few dense items would carry the kernel (c5 on the disc-quadrature
+            // cloud: 9.5 ms against 2.7 ms for the subproblem-balanced RED-flush
+            // kernel).  setpts left a device flag; when it is set the kernels
+            // above returned at once and these two run instead.
+            if (owner && a.imb) {
+                if (!a.accumulate) {
+                    const size_t n16 = (size_t)a.gstride * a.ntransf * 2 * sizeof(T) / 16;
+                    k_zero_if<T><<<device_sm_count() * 8, 256, 0, st>>>(reinterpret_cast<int4 *>(a.grid), n16, a.imb);
+                }
+                static PerDev<int> grid_;
+                int &grid = grid_();
+                if (grid == 0) {
+                    int rc = persistent_launch(k_spread_batch2d<T, W, true>, 128, smem, st, nullptr, &grid);
+                    if (rc) return rc;
+                }
+                k_spread_batch2d<T, W, true><<<grid, 128, smem, st>>>(a, cperm, tab);
+            }
+            if (owner) {
             } else if (a.sbl[0] == 0 && a.sbl[1] == 0 && a.g.bs[0] == Cfg::BX) {
                 static PerDev<int> grid_;
                 int &grid = grid_();

@@ -102,6 +102,8 @@ struct SpreadArgs {
     const int *nsub;         // device count of subproblems
     const int *subofs;       // first subproblem of every bin (type 1; nullptr: unused)
     int roll;                // 3D row spreader: z-rolling segments (small bins on average)
+    const int *imb;          // batched 2D owner-computes plans: device flag set by setpts when the bin
+                             // counts are badly imbalanced (clustered points) -> RED-flush spreader; or null
     int *work;               // work-queue counter (zeroed before launch)
     const T *c;              // (ntransf, M) interleaved complex
     T *grid;                 // (ntransf, n3, n2, n1) interleaved complex
@@ -178,6 +180,8 @@ int launch_setpts(const SetptsArgs &a, int nbins, int max_subprob, int4 *subprob
 constexpr int kScanTile = 4096;  // keys per scan block
 // records in original order, no sort (small 1D type-1 plans, global-atomic spreader)
 int launch_setpts_unsorted(const SetptsArgs &a, cudaStream_t st);
+// device flag: 1 when the fullest bin holds > 2048 points and > 8x the mean (clustered points)
+int launch_bin_imbalance(const int *bin_start, int nbins, int64_t M, int *flag, cudaStream_t st);
 int launch_sort_view(int dtype, const void *rec, const int *bin_start, int nbins, int64_t M, int *perm,
                      int *keys, cudaStream_t st);
 // Bin geometry the chosen spreader needs: (bx, by, bz); returns 0 if the

@@ -123,6 +123,7 @@ struct esn_plan_s {
     int64_t keycap_req = (int64_t)8 << 20;  // key-space limit the current sbl was chosen for
     int4 *subprob = nullptr;
     unsigned long long *flags = nullptr;
+    int *imb = nullptr;  // batched owner-computes plans: bins badly imbalanced (set by setpts on the device)
     void *grid = nullptr;
     int64_t M = -1, Mcap = 0, subcap = 0;
     int64_t device_bytes = 0;
@@ -400,6 +401,15 @@ static int plan_common_init(esn_plan p, const esn_opts *o) {
     if ((rc = dmalloc(p, &p->flags, sizeof(unsigned long long) * 8))) return rc;
     if ((rc = dmalloc(p, &p->grid, real_size(p->dtype) * 2 * (size_t)p->G * p->ntransf))) return rc;
     ESN_CUDA_TRY(cudaMemsetAsync(p->flags, 0xff, sizeof(unsigned long long) * 8, p->st));
+    // (ESN_B2_SWITCH=0: batched owner-computes plans never hand over to the RED-flush spreader)
+    static const bool b2switch = [] {
+        const char *e = getenv("ESN_B2_SWITCH");
+        return !(e && e[0] == '0');
+    }();
+    if (b2switch && esn::batched_spread(p->dtype, p->dim, p->kp.w, p->ntransf, p->method)) {
+        if ((rc = dmalloc(p, &p->imb, sizeof(int)))) return rc;
+        ESN_CUDA_TRY(cudaMemsetAsync(p->imb, 0, sizeof(int), p->st));
+    }
     if (p->opts.timing) {
         for (int i = 0; i < 8; ++i) ESN_CUDA_TRY(cudaEventCreate(&p->ev[i]));
         p->have_events = true;
@@ -522,6 +532,7 @@ int esn_plan_destroy(esn_plan p) {
     dfree(p->work);
     dfree(p->subprob);
     dfree(p->flags);
+    dfree(p->imb);
     if (p->have_events)
         for (int i = 0; i < 8; ++i) cudaEventDestroy(p->ev[i]);
     if (p->fft_made) cufftDestroy(p->fft_h);
@@ -914,6 +925,12 @@ int esn_plan_setpts(esn_plan p, int64_t M, int coord_dtype, const void *x, const
                                    (p->aux.st && !graphed) ? &aux : nullptr))) {
         return rc;
     }
+    // batched owner-computes plans: let the device decide whether the
+    // points are too clustered for one warp per item (see esn_inst.cuh)
+    if (p->imb && !unsorted && M > 0 &&
+        esn::batched_owner(p->dtype, p->dim, p->kp.w, p->ntransf, p->method, p->sbl, p->geom.bs)) {
+        if ((rc = esn::launch_bin_imbalance(p->bin_start, p->nbins, M, p->imb, ss))) return rc;
+    }
     if (p->have_events) ESN_CUDA_TRY(rec_ev(p, p->ev[1], ss));
     if (side) ESN_CUDA_TRY(cudaEventRecord(p->e_sorted, p->st2));
     return ESN_SUCCESS;
@@ -968,6 +985,11 @@ static SpreadArgs<T> make_spread_args(esn_plan p, const void *c, void *grid) {
     a.gstride = p->G;
     a.ibase = p->ibase;
     a.flags = p->flags;
+    // (only plans on the owner-computes path switch; elsewhere the RED-flush kernel always runs)
+    a.imb = (p->imb && p->type == 1 &&
+             esn::batched_owner(p->dtype, p->dim, p->kp.w, p->ntransf, p->method, p->sbl, p->geom.bs))
+                ? p->imb
+                : nullptr;
     return a;
 }
 

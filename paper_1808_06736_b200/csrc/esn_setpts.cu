@@ -469,6 +469,35 @@ static int setpts_impl(const SetptsArgs &a, int nbins, int maxsub, int4 *subprob
     return tables();
 }
 
+// flag = 1 when one bin holds far more than its share of the points
+// (clustered clouds): the batched owner-computes spreaders walk a bin's points
+// with a single warp, so they hand such plans to the subproblem-balanced
+// RED-flush kernel (esn_inst.cuh).  One CTA over the bin starts.
+__global__ void __launch_bounds__(1024) k_bin_imbalance(const int *bin_start, int nbins, int64_t M, int *flag) {
+    __shared__ int smax[32];
+    int m = 0;
+    for (int b = threadIdx.x; b < nbins; b += 1024) m = max(m, bin_start[b + 1] - bin_start[b]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) smax[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        m = smax[threadIdx.x];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (threadIdx.x == 0) {
+            const int64_t mean = M / (nbins > 0 ? nbins : 1) + 1;
+            *flag = (m > 2048 && (int64_t)m > 8 * mean) ? 1 : 0;
+        }
+    }
+}
+
+int launch_bin_imbalance(const int *bin_start, int nbins, int64_t M, int *flag, cudaStream_t st) {
+    k_bin_imbalance<<<1, 1024, 0, st>>>(bin_start, nbins, M, flag);
+    ESN_CUDA_TRY(cudaGetLastError());
+    return ESN_SUCCESS;
+}
+
 __global__ void k_sort_view(const Rec *rec, const int *bin_start, int nbins, int *perm, int *keys) {
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < nbins; b += gridDim.x * blockDim.x) {
         for (int k = bin_start[b]; k < bin_start[b + 1]; ++k) {

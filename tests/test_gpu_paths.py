@@ -139,6 +139,8 @@ def test_spread_then_finish_equals_type1(esn, dim, nm, T):
     ((13, 9), 3, 4000, False),      # fine grid narrower than one 16 x 16 block: wrapped halo cells
     ((37, 21), 33, 20_000, False),  # partial last blocks in x and y, a partial second transform group
     ((64, 48), 4, 60_000, True),    # clustered: hundreds of points per cell, many pieces per source row
+    ((96, 80), 40, 600_000, True),  # clustered, above the graph threshold: the device-side imbalance flag
+                                    # hands the spread to the RED-flush kernel (k_zero_if + k_spread_batch2d)
     ((200, 150), 64, 80_000, False),  # two full transform groups, many strips / segments
 ])
 def test_batched_owner_spreader(esn, oracle, nm, T, m, clustered):
