@@ -173,9 +173,30 @@ __global__ void __launch_bounds__(256, 4) k_setpts_count(SetptsArgs a) {
             double g[3];
             key[u] = i < a.M ? point_key<DIM>(a, i, x[u], g, true) : -1;
         }
+        // Clustered clouds put runs of consecutive points on one key, and
+        // same-address REDs serialise in L2 (c2 on the disc quadrature: 1.05
+        // ms/step).  A warp that sees equal keys on neighbouring lanes adds
+        // once per key group (match.any); the others -- every warp of a
+        // uniform cloud -- keep the plain fire-and-forget REDs (the test costs
+        // one shuffle per point; an unconditional match.any cost c2 6 %).
+        const int lane = threadIdx.x & 31;
+        bool dup = false;
 #pragma unroll
-        for (int u = 0; u < kILP; ++u)
-            if (key[u] >= 0) atomicAdd(&a.key_count[key[u]], 1);
+        for (int u = 0; u < kILP; ++u) {
+            const int nb = __shfl_up_sync(0xffffffffu, key[u], 1);
+            dup |= lane > 0 && nb == key[u] && nb >= 0;
+        }
+        if (__any_sync(0xffffffffu, dup)) {
+#pragma unroll
+            for (int u = 0; u < kILP; ++u) {
+                const unsigned grp = __match_any_sync(0xffffffffu, key[u]);
+                if (key[u] >= 0 && lane == __ffs(grp) - 1) atomicAdd(&a.key_count[key[u]], __popc(grp));
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < kILP; ++u)
+                if (key[u] >= 0) atomicAdd(&a.key_count[key[u]], 1);
+        }
     }
 }
 
@@ -210,7 +231,28 @@ __global__ void __launch_bounds__(256) k_setpts_scatter(SetptsArgs a) {
             g[u][0] = g[u][1] = g[u][2] = 0.0;
             pos[u] = i < a.M ? point_key<DIM>(a, i, x[u], g[u], false) : -1;
         }
-        if (a.hints) {
+        // fill cursors: plain atomics, all in flight at once -- unless the warp
+        // holds runs of equal keys (clustered clouds), where the lanes of a key
+        // group take a block of slots with one atomic of their leader (their
+        // order inside the key is free)
+        const int lane = threadIdx.x & 31;
+        bool dup = false;
+#pragma unroll
+        for (int u = 0; u < kSILP; ++u) {
+            const int nb = __shfl_up_sync(0xffffffffu, pos[u], 1);
+            dup |= lane > 0 && nb == pos[u] && nb >= 0;
+        }
+        if (__any_sync(0xffffffffu, dup)) {
+#pragma unroll
+            for (int u = 0; u < kSILP; ++u) {  // (unrolled: pos[] must stay in registers)
+                const unsigned grp = __match_any_sync(0xffffffffu, pos[u]);
+                const int leader = __ffs(grp) - 1;
+                int base = 0;
+                if (pos[u] >= 0 && lane == leader) base = atomicAdd(a.key_count + pos[u], __popc(grp));
+                base = __shfl_sync(0xffffffffu, base, leader);
+                if (pos[u] >= 0) pos[u] = base + __popc(grp & ((1u << lane) - 1u));
+            }
+        } else if (a.hints) {
             // the fill cursors (L2-resident key array) evict-last, the
             // streaming record stores evict-first: without the hints about
             // half of the cursor atomics missed the near L2 (ncu, c2)
