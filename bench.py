@@ -82,11 +82,14 @@ def hot_kernel_name(cfg):
 # pipe / shared-memory utilisation); roofline.frac stays the HBM fraction
 BINDING = {
     "c1": "launch / latency (1e5 points; CUDA-graph replay)",
-    "c2": "shared-memory wavefronts (~75 % busy) + FP64 pipe (~37 %), not HBM",
-    "c3": "issue / shared-memory wavefronts (~44 instructions around 14 DFMA per point-warp pass; FP64 pipe ~25 %), not HBM",
-    "c3f": "issue / shared-memory wavefronts (per-pass overhead around 10 FFMA), not HBM",
-    "c4": "issue / FP64 pipe (~44 % active; 1000 cells per point at 45 % lane coverage), not HBM",
-    "c5": "issue (~80 instructions per point-strip visit, 45 % issue efficiency), DRAM ~ algorithmic bytes",
+    "c2": "shared-memory wavefronts (59.7 M: ~73 % of the LSU pipe over the kernel) + FP64 pipe (~32 %), not HBM",
+    "c3": "shared-memory wavefronts (14 per point-warp pass around 16 FP64 instructions; ~58 % of the LSU pipe) "
+          "+ FP64 pipe ~31 % at 16 warps per SM, not HBM",
+    "c3f": "shared-memory wavefronts (~53 % of the LSU pipe) / issue 55 % (two-point step: 32 instructions around "
+           "12 FFMA2 / FMUL2), not HBM",
+    "c4": "FP64 pipe 46 % + shared-memory wavefronts (~62 % of the LSU pipe; 1000 cells per point at ~56 % lane "
+          "coverage), not HBM",
+    "c5": "latency (12 warps per SM: short scoreboard 34 %, wait 26 %; issue 35 %), DRAM ~ algorithmic bytes",
 }
 
 
