@@ -143,9 +143,11 @@ int esn_spreader_create(int dim, const int64_t *nfine, int ntransf,
                         const esn_opts *opts, esn_plan *out);
 /* Fold, grid-scale and bin-sort M points (device arrays of coord_dtype);
  * replaces build_point_set + ensure_sorted (spreadinterp.py:79-114).
- * Stream contract: a type-2 plan sorts on a private side stream that first
- * waits for the work already queued on opts.stream; the coordinate arrays
- * are read by that side stream until the next call on this plan
+ * Stream contract: a type-2 plan sorts on private side streams (the count
+ * pass on one at the plan stream's priority, the scans and the record
+ * scatter on a high-priority one) that first wait for the work already
+ * queued on opts.stream; the coordinate arrays are read by those streams
+ * until the next call on this plan
  * (execute / interp / spread / check / setpts), which orders opts.stream
  * after the sort.  Do not modify or free x / y / z before that call (or a
  * stream synchronisation).  Each setpts first joins any earlier pending
